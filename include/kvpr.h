@@ -1,0 +1,135 @@
+/*
+ * kvpr.h — C-ABI of libkvpr.so, the B200 (sm_100a) kernels behind KVPR's
+ * per-layer decode path.
+ *
+ * The reference (`kvoverlap`, /root/reference/pkg) is a pure-Python planner
+ * with no FFI; its numeric contract lives in numerics.py and its cost model
+ * in costmodel.py / scheduler.py.  Each entry point below names the reference
+ * routine whose semantics it takes over on the GPU.  The Python package
+ * `paper_2411_17089_b200` binds these with ctypes (see _lib.py and
+ * INTEGRATION.md) — that is the boundary a `kvoverlap` maintainer would bind.
+ *
+ * Conventions
+ *  - The caller (Python / torch) owns every allocation, device and pinned
+ *    host.  The library borrows raw pointers; it never allocates device
+ *    memory, frees, or synchronises.
+ *  - Every launch goes on the caller's stream (`stream` is a cudaStream_t,
+ *    NULL = legacy default stream).
+ *  - Return 0 on success.  KVPR_EINVAL (bad shape / pointer / range) maps to
+ *    ValueError, as the reference raises ValueError for the same conditions
+ *    (numerics.py:22-32, costmodel.py:31-43); KVPR_ECUDA maps to RuntimeError.
+ *    kvpr_last_error() returns a thread-local message for the last failure.
+ *  - fp16 storage, fp32 accumulation.  No CPU fallback exists: every entry
+ *    point launches sm_100a code or fails.
+ *
+ * Layouts
+ *  - KV pages (one layer): position-major slabs, page p = [2][batch][hidden]
+ *    fp16 (K then V), i.e. element (p, kv, b, c) at ((p*2 + kv)*batch + b)*hidden + c.
+ *    A contiguous position range [l, s) is therefore one contiguous byte
+ *    range, so KV[l:s'-1] streams host->device as a single DMA.
+ *  - Layer inputs X (post-LN1 activations, the recompute source): [pos][batch][hidden] fp16.
+ *  - Linear weights: PyTorch layout [out_features, in_features] fp16 (K-major).
+ */
+#ifndef KVPR_H_
+#define KVPR_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVPR_OK 0
+#define KVPR_EINVAL 1
+#define KVPR_ECUDA 2
+
+/* epilogue flags for kvpr_linear */
+#define KVPR_EPI_RELU 1  /* max(0, .) after bias */
+#define KVPR_EPI_F32 2   /* fp32 output (default fp16) */
+#define KVPR_EPI_ACCUM 4 /* fp32 output accumulated in place: out += result (residual add) */
+
+/* One output column segment of kvpr_linear.  Output element (m, n) with
+ * seg = n / seg_width lands at
+ *   ptr + (m % row_group) * ld + (m / row_group) * group_stride + n % seg_width
+ * (elements of the output type). */
+typedef struct kvpr_out_seg {
+  void* ptr;
+  long long group_stride;
+} kvpr_out_seg;
+
+typedef struct kvpr_epilogue {
+  const void* bias;   /* fp16 [N] or NULL */
+  int seg_width;      /* columns per segment, multiple of 32 */
+  int row_group;      /* rows per group (>=1) */
+  long long ld;       /* row stride inside a group, elements */
+  kvpr_out_seg seg[3];
+  float scale;        /* applied to columns [0, scale_cols) after the bias */
+  int scale_cols;
+  int flags;          /* KVPR_EPI_* */
+} kvpr_epilogue;
+
+/* Thread-local description of the last failure ("" if none). */
+const char* kvpr_last_error(void);
+
+/* ABI version (bumped on any signature change). */
+int kvpr_version(void);
+
+/* Number of SMs of `device` (for grid sizing in the host runtime). */
+int kvpr_sm_count(int device);
+
+/* K1 — recompute GEMM (tcgen05 + TMEM, TMA-fed).
+ * Replaces numerics.split_merge_kv's prefix rebuild `X[:l] @ W_K`, `X[:l] @ W_V`
+ * (numerics.py:129-133), with OPT's k_proj/v_proj biases, FLOPs per
+ * costmodel.recompute_flops (costmodel.py:169-176).
+ * For positions [pos_begin, pos_end):
+ *   K[p, b, :] = X[p, b, :] . W_k^T + b_k,  V[p, b, :] = X[p, b, :] . W_v^T + b_v
+ * written in place into the KV pages.
+ *   x        : layer-input buffer, [pos][batch][hidden] fp16 (position 0 at x)
+ *   w_kv     : [2*hidden, hidden] fp16 = rows of W_k then W_v (torch layout)
+ *   b_kv     : [2*hidden] fp16 = b_k then b_v (may be NULL)
+ *   kv_pages : page buffer of the layer, position 0 at kv_pages
+ * pos_begin == pos_end is a no-op (split 0, numerics.py:127-128). */
+int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* kv_pages, int batch,
+                      int pos_begin, int pos_end, int hidden, void* stream);
+
+/* Fused projection: out = epilogue(A[M,K] . W[N,K]^T + bias), tcgen05 GEMM.
+ * Used for the decode-token q/k/v (K3), out-proj + residual (K4), fc1+ReLU and
+ * fc2 + residual (K6), LM head (K8), and the prefill that fills the host stores.
+ * bn selects the N tile (64, 128 or 256; 0 = auto). */
+int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                const kvpr_epilogue* epi, int bn, void* stream);
+
+/* K2 — split-KV decode attention over the merged cache, read in place.
+ * Replaces numerics.decode_attention's per-head loop (numerics.py:166-190):
+ * per (sequence b, head) softmax(scale * K q) V over positions [0, seq_len)
+ * of the page buffer, max-subtracted softmax (numerics.py:159-163).  Positions
+ * [0,l) hold recomputed K/V, [l, seq_len-1) the transferred tail, seq_len-1
+ * the new token — one buffer, no concatenation.
+ *   q   : [batch][hidden] fp16,  out : [batch][hidden] fp16 (heads concatenated)
+ *   ws  : fp32 scratch for split partials; ws_bytes sizes the split count.
+ * seq_len == 0 -> KVPR_EINVAL ("cannot attend over an empty cache"). */
+int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* ws, size_t ws_bytes, int batch,
+                          int heads, int head_dim, int seq_len, float scale, void* stream);
+
+/* Causal attention for the prompt (prefill that populates the host stores):
+ * q/out [pos][batch][hidden], kv pages as above, positions [0, seq_len). */
+int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,
+                           int seq_len, float scale, void* stream);
+
+/* K5 — LayerNorm of fp32 rows into fp16 (out row stride ldo). */
+int kvpr_layernorm(const float* x, long long ldx, const void* gamma, const void* beta, void* out, long long ldo,
+                   int rows, int hidden, float eps, void* stream);
+
+/* K7 — token + learned position embedding into the fp32 residual stream.
+ * Row r is (position pos_begin + r / batch, sequence r % batch). */
+int kvpr_embed(const int* tokens, const void* tok_emb, const void* pos_emb, float* out, int rows, int batch,
+               int pos_begin, int hidden, int pos_offset, void* stream);
+
+/* K8 tail — per-row argmax (greedy token) of fp32 logits. */
+int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVPR_H_ */

@@ -1,0 +1,140 @@
+"""ctypes binding of libkvpr.so (include/kvpr.h).
+
+This is the only place Python touches the C-ABI.  Every wrapper takes raw
+device pointers (ints) plus sizes, returns nothing, and raises ValueError for
+KVPR_EINVAL (the reference's error class for shape/range problems,
+numerics.py:22-32) or RuntimeError for CUDA failures.  There is no fallback:
+if the library is missing, loading fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libkvpr.so"
+
+KVPR_OK = 0
+KVPR_EINVAL = 1
+KVPR_ECUDA = 2
+
+EPI_RELU = 1
+EPI_F32 = 2
+EPI_ACCUM = 4
+
+# Every symbol include/kvpr.h declares (tests check the .so exports all of them).
+EXPORTS = (
+    "kvpr_last_error",
+    "kvpr_version",
+    "kvpr_sm_count",
+    "kvpr_recompute_kv",
+    "kvpr_linear",
+    "kvpr_decode_attention",
+    "kvpr_prefill_attention",
+    "kvpr_layernorm",
+    "kvpr_embed",
+    "kvpr_argmax",
+)
+
+
+class OutSeg(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("group_stride", ctypes.c_longlong)]
+
+
+class Epilogue(ctypes.Structure):
+    _fields_ = [
+        ("bias", ctypes.c_void_p),
+        ("seg_width", ctypes.c_int),
+        ("row_group", ctypes.c_int),
+        ("ld", ctypes.c_longlong),
+        ("seg", OutSeg * 3),
+        ("scale", ctypes.c_float),
+        ("scale_cols", ctypes.c_int),
+        ("flags", ctypes.c_int),
+    ]
+
+
+_lib: ctypes.CDLL | None = None
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+_f = ctypes.c_float
+_sz = ctypes.c_size_t
+
+_SIGS = {
+    "kvpr_last_error": ([], ctypes.c_char_p),
+    "kvpr_version": ([], _i),
+    "kvpr_sm_count": ([_i], _i),
+    "kvpr_recompute_kv": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp], _i),
+    "kvpr_linear": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp], _i),
+    "kvpr_decode_attention": ([_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
+    "kvpr_prefill_attention": ([_vp, _vp, _vp, _i, _i, _i, _i, _f, _vp], _i),
+    "kvpr_layernorm": ([_vp, _ll, _vp, _vp, _vp, _ll, _i, _i, _f, _vp], _i),
+    "kvpr_embed": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp], _i),
+    "kvpr_argmax": ([_vp, _ll, _i, _i, _vp, _vp, _vp], _i),
+}
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the shared library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"libkvpr.so not found at {p}; build it with `python -m paper_2411_17089_b200.csrc.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().kvpr_last_error().decode()
+
+
+def check(rc: int, what: str) -> None:
+    if rc == KVPR_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == KVPR_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def make_epilogue(
+    segs,
+    seg_width: int,
+    ld: int,
+    row_group: int,
+    bias: int | None = None,
+    scale: float = 1.0,
+    scale_cols: int = 0,
+    flags: int = 0,
+) -> Epilogue:
+    """segs: list of (ptr, group_stride) pairs, one per output column segment."""
+    e = Epilogue()
+    e.bias = bias or None
+    e.seg_width = seg_width
+    e.row_group = row_group
+    e.ld = ld
+    for i, (ptr, gs) in enumerate(segs):
+        e.seg[i].ptr = ptr
+        e.seg[i].group_stride = gs
+    e.scale = scale
+    e.scale_cols = scale_cols
+    e.flags = flags
+    return e

@@ -1,0 +1,160 @@
+// extern "C" boundary of libkvpr.so (declared in include/kvpr.h).
+//
+// Validation mirrors the reference's ValueError conditions where one exists
+// (numerics.py:22-32, 121-126, 172-182); everything else is a CUDA error.
+// No entry point allocates, frees or synchronises.
+
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "kvpr_internal.h"
+
+namespace kvpr {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device >= 0 && device < 64 && cache[device] > 0) return cache[device];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) n = 148;
+  if (device >= 0 && device < 64) cache[device] = n;
+  return n;
+}
+
+static GemmArgs to_args(const kvpr_epilogue* e) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.bias = static_cast<const __half*>(e->bias);
+  a.seg_width = e->seg_width;
+  a.row_group = e->row_group;
+  a.ld = e->ld;
+  for (int s = 0; s < 3; ++s) {
+    a.seg_ptr[s] = e->seg[s].ptr;
+    a.seg_group_stride[s] = e->seg[s].group_stride;
+  }
+  a.scale = e->scale;
+  a.scale_cols = e->scale_cols;
+  a.flags = e->flags;
+  return a;
+}
+
+}  // namespace kvpr
+
+using namespace kvpr;
+
+extern "C" {
+
+const char* kvpr_last_error(void) { return g_err; }
+
+int kvpr_version(void) { return 1; }
+
+int kvpr_sm_count(int device) { return sm_count(device); }
+
+int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* kv_pages, int batch, int pos_begin,
+                      int pos_end, int hidden, void* stream) {
+  g_err[0] = 0;
+  if (batch <= 0 || hidden <= 0 || pos_begin < 0 || pos_end < pos_begin) {
+    set_error("split must satisfy 0 <= pos_begin <= pos_end (got [%d, %d)), batch=%d hidden=%d", pos_begin, pos_end,
+              batch, hidden);
+    return KVPR_EINVAL;
+  }
+  if (pos_end == pos_begin) return KVPR_OK;  // split 0: nothing rebuilt (numerics.py:127-128)
+  if (x == nullptr || w_kv == nullptr || kv_pages == nullptr) {
+    set_error("recompute_kv: null pointer");
+    return KVPR_EINVAL;
+  }
+  const long long bh = (long long)batch * hidden;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.bias = static_cast<const __half*>(b_kv);
+  a.seg_width = hidden;                     // columns [0,h) -> K, [h,2h) -> V
+  a.row_group = batch;                      // rows of one position
+  a.ld = hidden;
+  __half* page0 = static_cast<__half*>(kv_pages) + (long long)pos_begin * 2 * bh;
+  a.seg_ptr[0] = page0;                     // K half of each page
+  a.seg_ptr[1] = page0 + bh;                // V half of each page
+  a.seg_group_stride[0] = 2 * bh;           // next position = next page
+  a.seg_group_stride[1] = 2 * bh;
+  a.scale = 1.f;
+  a.scale_cols = 0;
+  a.flags = 0;
+  const __half* a_ptr = static_cast<const __half*>(x) + (long long)pos_begin * bh;
+  const int M = (pos_end - pos_begin) * batch;
+  return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, 256, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                const kvpr_epilogue* epi, int bn, void* stream) {
+  g_err[0] = 0;
+  if (epi == nullptr || a == nullptr || w == nullptr) {
+    set_error("linear: null pointer");
+    return KVPR_EINVAL;
+  }
+  if (bn == 0) {
+    // small-M (decode) GEMMs are weight-streaming: narrow N tiles give more CTAs
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = sm_count(dev);
+    const long long m_blk = (M + 127) / 128;
+    bn = 256;
+    if (m_blk * ((N + 255) / 256) < sms) bn = 128;
+    if (m_blk * ((N + 127) / 128) < sms) bn = 64;
+  }
+  return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* ws, size_t ws_bytes, int batch,
+                          int heads, int head_dim, int seq_len, float scale, void* stream) {
+  g_err[0] = 0;
+  return decode_attention(static_cast<const __half*>(q), static_cast<const __half*>(kv_pages),
+                          static_cast<__half*>(out), static_cast<float*>(ws), ws_bytes, batch, heads, head_dim,
+                          seq_len, scale, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,
+                           int seq_len, float scale, void* stream) {
+  g_err[0] = 0;
+  return prefill_attention(static_cast<const __half*>(q), static_cast<const __half*>(kv_pages),
+                           static_cast<__half*>(out), batch, heads, head_dim, seq_len, scale,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_layernorm(const float* x, long long ldx, const void* gamma, const void* beta, void* out, long long ldo,
+                   int rows, int hidden, float eps, void* stream) {
+  g_err[0] = 0;
+  return layernorm(x, ldx, static_cast<const __half*>(gamma), static_cast<const __half*>(beta),
+                   static_cast<__half*>(out), ldo, rows, hidden, eps, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_embed(const int* tokens, const void* tok_emb, const void* pos_emb, float* out, int rows, int batch,
+               int pos_begin, int hidden, int pos_offset, void* stream) {
+  g_err[0] = 0;
+  return embed(tokens, static_cast<const __half*>(tok_emb), static_cast<const __half*>(pos_emb), out, rows, batch,
+               pos_begin, hidden, pos_offset, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val, void* stream) {
+  g_err[0] = 0;
+  return argmax_rows(logits, ld, rows, cols, out_idx, out_val, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,328 @@
+// K2: split-KV decode attention over the merged (recomputed + transferred)
+// KV pages, read in place; plus the causal prefill attention that fills the
+// host stores.
+//
+// Reference semantics: numerics.decode_attention (numerics.py:166-191) —
+// per head, softmax(K q / sqrt(d)) V with the max-subtracted softmax of
+// numerics.py:159-163; the merged cache of numerics.split_merge_kv
+// (numerics.py:134-137) is never materialised: positions [0,l) were written
+// by K1, [l,s'-1) by the H2D copy, s'-1 by the decode-token projection, all
+// into the same page buffer.
+//
+// Memory pattern: a page holds K (then V) of one position for all sequences,
+// so one (sequence, head) row of K is 2*head_dim contiguous bytes.  A group of
+// head_dim/8 lanes owns one position and each lane moves 16 B (128-bit
+// loads), so every request is whole 32-byte sectors.  Scores reduce with
+// xor-shuffles inside the lane group; the online softmax state (m, l, acc)
+// is merged across groups and warps at the end, and across splits by the
+// combine kernel (log-sum-exp merge).
+
+#include <math.h>
+
+#include "common.cuh"
+#include "kvpr_internal.h"
+
+namespace kvpr {
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void load8(const __half* p, float (&f)[8]) {
+  uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __half22float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// Streamed (read-once) variant for the big K/V sweep: bypass L1 allocation.
+__device__ __forceinline__ uint4 ld_stream(const __half* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __half22float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// Online-softmax state of one lane group: running max (log2 domain), sum, acc[8].
+struct Softmax8 {
+  float m, l, acc[8];
+  __device__ __forceinline__ void init() {
+    m = -INFINITY;
+    l = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  }
+};
+
+// Sweep positions p = first, first+step, ... < end with a group of LPP lanes
+// per position, U positions in flight per lane.  q8 is pre-multiplied by
+// scale*log2e so scores come out in the exp2 domain.
+// `first` must be warp-uniform (the shuffles below need the whole warp in every
+// trip); lane group `grp` owns positions first + grp + u*step + trip*U*step.
+template <int D, int U>
+__device__ __forceinline__ void sweep(const __half* __restrict__ kbase, long long page_stride, long long v_off,
+                                      int first, int end, int step, int grp, const float (&q8)[8], int glane,
+                                      Softmax8& st) {
+  constexpr int LPP = D / 8;
+  for (int pb = first; pb < end; pb += step * U) {
+    const int p0 = pb + grp;
+    uint4 kr[U], vr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * step;
+      kr[u] = make_uint4(0, 0, 0, 0);
+      vr[u] = make_uint4(0, 0, 0, 0);
+      if (p < end) {
+        const __half* kp = kbase + (long long)p * page_stride + glane * 8;
+        kr[u] = ld_stream(kp);
+        vr[u] = ld_stream(kp + v_off);
+      }
+    }
+    float s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float kf[8];
+      unpack8(kr[u], kf);
+      float d = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d = fmaf(q8[i], kf[i], d);
+#pragma unroll
+      for (int o = LPP / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      s[u] = (p0 + u * step < end) ? d : -INFINITY;
+    }
+    float mx = st.m;
+#pragma unroll
+    for (int u = 0; u < U; ++u) mx = fmaxf(mx, s[u]);
+    if (mx == -INFINITY) continue;  // whole block masked (only possible past `end`)
+    const float corr = exp2f(st.m - mx);
+    st.l *= corr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) st.acc[i] *= corr;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float pw = exp2f(s[u] - mx);
+      if (p0 + u * step < end) {
+        float vf[8];
+        unpack8(vr[u], vf);
+        st.l += pw;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st.acc[i] = fmaf(pw, vf[i], st.acc[i]);
+      }
+    }
+    st.m = mx;
+  }
+}
+
+// Merge softmax states of lanes that own the same 8 dims (xor over lane-group index bits).
+template <int LPP>
+__device__ __forceinline__ void merge_in_warp(Softmax8& st) {
+#pragma unroll
+  for (int o = LPP; o < 32; o <<= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, st.m, o);
+    const float ol = __shfl_xor_sync(0xffffffffu, st.l, o);
+    const float nm = fmaxf(st.m, om);
+    const float a = (st.m == -INFINITY) ? 0.f : exp2f(st.m - nm);
+    const float b = (om == -INFINITY) ? 0.f : exp2f(om - nm);
+    st.l = st.l * a + ol * b;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float oa = __shfl_xor_sync(0xffffffffu, st.acc[i], o);
+      st.acc[i] = st.acc[i] * a + oa * b;
+    }
+    st.m = nm;
+  }
+}
+
+// grid: (batch*heads, splits), block: 128 threads.
+template <int D>
+__global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
+                                                          __half* __restrict__ out, float* __restrict__ ws, int batch,
+                                                          int heads, int seq_len, int chunk, float qscale) {
+  constexpr int LPP = D / 8;
+  constexpr int PPW = 32 / LPP;  // positions per warp step
+  constexpr int NW = 4;
+  const int bh = blockIdx.x;
+  const int b = bh / heads;
+  const int hd = bh % heads;
+  const int hidden = heads * D;
+  const int split = blockIdx.y;
+  const int p_lo = split * chunk;
+  const int p_hi = min(seq_len, p_lo + chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int glane = lane % LPP, grp = lane / LPP;
+
+  float q8[8];
+  load8(q + (long long)b * hidden + hd * D + glane * 8, q8);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q8[i] *= qscale;
+
+  const long long page_stride = 2LL * batch * hidden;
+  const __half* kbase = kv + (long long)b * hidden + hd * D;
+  Softmax8 st;
+  st.init();
+  sweep<D, 4>(kbase, page_stride, (long long)batch * hidden, p_lo + warp * PPW, p_hi, NW * PPW, grp, q8, glane, st);
+  merge_in_warp<LPP>(st);
+
+  __shared__ float sm_m[NW], sm_l[NW];
+  __shared__ float sm_acc[NW][D];
+  if (lane < LPP) {
+    if (lane == 0) {
+      sm_m[warp] = st.m;
+      sm_l[warp] = st.l;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm_acc[warp][glane * 8 + i] = st.acc[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int dd = threadIdx.x;
+    float m = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) m = fmaxf(m, sm_m[w]);
+    float l = 0.f, a = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float f = (sm_m[w] == -INFINITY) ? 0.f : exp2f(sm_m[w] - m);
+      l += sm_l[w] * f;
+      a += sm_acc[w][dd] * f;
+    }
+    if (gridDim.y == 1) {
+      out[(long long)b * hidden + hd * D + dd] = __float2half_rn(a / l);
+    } else {
+      float* w = ws + ((long long)bh * gridDim.y + split) * (D + 2);
+      w[2 + dd] = a;
+      if (dd == 0) {
+        w[0] = m;
+        w[1] = l;
+      }
+    }
+  }
+}
+
+// grid: batch*heads, block: D threads — log-sum-exp merge of the split partials.
+template <int D>
+__global__ void decode_attn_combine_kernel(const float* __restrict__ ws, __half* __restrict__ out, int heads,
+                                           int splits) {
+  const int bh = blockIdx.x;
+  const int b = bh / heads, hd = bh % heads;
+  const int dd = threadIdx.x;
+  const float* w = ws + (long long)bh * splits * (D + 2);
+  float m = -INFINITY;
+  for (int s = 0; s < splits; ++s) m = fmaxf(m, w[s * (D + 2)]);
+  float l = 0.f, a = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float ms = w[s * (D + 2)];
+    const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - m);
+    l += w[s * (D + 2) + 1] * f;
+    a += w[s * (D + 2) + 2 + dd] * f;
+  }
+  out[(long long)b * heads * D + hd * D + dd] = __float2half_rn(a / l);
+}
+
+// Causal prefill: grid (batch*heads, ceil(seq/4)), block 128: one warp per query position.
+template <int D>
+__global__ void __launch_bounds__(128) prefill_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
+                                                           __half* __restrict__ out, int batch, int heads, int seq_len,
+                                                           float qscale) {
+  constexpr int LPP = D / 8;
+  constexpr int PPW = 32 / LPP;
+  const int bh = blockIdx.x;
+  const int b = bh / heads, hd = bh % heads;
+  const int hidden = heads * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qpos = blockIdx.y * 4 + warp;
+  if (qpos >= seq_len) return;
+  const int glane = lane % LPP, grp = lane / LPP;
+  const long long row = (long long)qpos * batch + b;
+  float q8[8];
+  load8(q + row * hidden + hd * D + glane * 8, q8);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q8[i] *= qscale;
+  Softmax8 st;
+  st.init();
+  sweep<D, 2>(kv + (long long)b * hidden + hd * D, 2LL * batch * hidden, (long long)batch * hidden, 0, qpos + 1, PPW,
+              grp, q8, glane, st);
+  merge_in_warp<LPP>(st);
+  if (lane < LPP) {
+    __half* o = out + row * hidden + hd * D + glane * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = __float2half_rn(st.acc[i] / st.l);
+  }
+}
+
+}  // namespace
+
+int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch, int heads,
+                     int head_dim, int seq_len, float scale, cudaStream_t stream) {
+  if (seq_len <= 0) {
+    set_error("cannot attend over an empty cache (seq_len=%d)", seq_len);
+    return KVPR_EINVAL;
+  }
+  if (batch <= 0 || heads <= 0 || (head_dim != 64 && head_dim != 128)) {
+    set_error("decode_attention: batch=%d heads=%d head_dim=%d (head_dim must be 64 or 128)", batch, heads, head_dim);
+    return KVPR_EINVAL;
+  }
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv)) & 15) {
+    set_error("decode_attention: q / kv must be 16-byte aligned");
+    return KVPR_EINVAL;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int bh = batch * heads;
+  // enough CTAs for ~8 resident per SM, each split at least 64 positions
+  const int target = 8 * sm_count(dev);
+  int splits = (target + bh - 1) / bh;
+  const int max_by_len = (seq_len + 63) / 64;
+  if (splits > max_by_len) splits = max_by_len;
+  const size_t per_split = (size_t)bh * (head_dim + 2) * sizeof(float);
+  if (ws == nullptr || ws_bytes < per_split) splits = 1;
+  else if ((size_t)splits * per_split > ws_bytes) splits = (int)(ws_bytes / per_split);
+  if (splits < 1) splits = 1;
+  const int chunk = (seq_len + splits - 1) / splits;
+  splits = (seq_len + chunk - 1) / chunk;
+  const float qscale = scale * kLog2e;
+  dim3 grid(bh, splits);
+  if (head_dim == 128)
+    decode_attn_kernel<128><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale);
+  else
+    decode_attn_kernel<64><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale);
+  int rc = check_launch("decode_attention");
+  if (rc || splits == 1) return rc;
+  if (head_dim == 128)
+    decode_attn_combine_kernel<128><<<bh, 128, 0, stream>>>(ws, out, heads, splits);
+  else
+    decode_attn_combine_kernel<64><<<bh, 64, 0, stream>>>(ws, out, heads, splits);
+  return check_launch("decode_attention_combine");
+}
+
+int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim, int seq_len,
+                      float scale, cudaStream_t stream) {
+  if (seq_len <= 0 || batch <= 0 || heads <= 0 || (head_dim != 64 && head_dim != 128)) {
+    set_error("prefill_attention: bad shape seq=%d batch=%d heads=%d head_dim=%d", seq_len, batch, heads, head_dim);
+    return KVPR_EINVAL;
+  }
+  dim3 grid(batch * heads, (seq_len + 3) / 4);
+  const float qscale = scale * kLog2e;
+  if (head_dim == 128)
+    prefill_attn_kernel<128><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
+  else
+    prefill_attn_kernel<64><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
+  return check_launch("prefill_attention");
+}
+
+}  // namespace kvpr

@@ -1,0 +1,196 @@
+// Row kernels of the OPT decode layer: LayerNorm (K5), token + learned
+// position embedding (K7) and the greedy argmax behind the LM head (K8).
+// All are HBM/latency bound; rows map to CTAs, columns to 128-bit vectors.
+//
+// OPT semantics (not in the reference package, which has no decoder —
+// SURVEY.md §8a note 2): pre-LN blocks, learned positions with offset 2,
+// fp32 residual stream here (HF keeps fp16; fp32 is closer to the oracle).
+
+#include <float.h>
+
+#include "common.cuh"
+#include "kvpr_internal.h"
+
+namespace kvpr {
+
+namespace {
+
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// one CTA per row; two-pass (mean, then centred variance) in fp32 from registers
+template <int VPT>  // float4 vectors per thread
+__global__ void __launch_bounds__(kRowThreads) layernorm_kernel(const float* __restrict__ x, long long ldx,
+                                                                const __half* __restrict__ gamma,
+                                                                const __half* __restrict__ beta, __half* __restrict__ out,
+                                                                long long ldo, int hidden, float eps) {
+  __shared__ float red[32];
+  const int row = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
+  const int nvec = hidden / 4;
+  float4 v[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * kRowThreads;
+    v[i] = (c < nvec) ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += v[i].x + v[i].y + v[i].z + v[i].w;
+  }
+  const float mean = block_sum(s, red) / hidden;
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * kRowThreads;
+    if (c < nvec) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      ss += a * a + b * b + cc * cc + d * d;
+    }
+  }
+  const float rstd = rsqrtf(block_sum(ss, red) / hidden + eps);
+  __half* o = out + row * ldo;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * kRowThreads;
+    if (c < nvec) {
+      const __half2* g2 = reinterpret_cast<const __half2*>(gamma + 4 * c);
+      const __half2* b2 = reinterpret_cast<const __half2*>(beta + 4 * c);
+      const float2 g0 = __half22float2(g2[0]), g1 = __half22float2(g2[1]);
+      const float2 c0 = __half22float2(b2[0]), c1 = __half22float2(b2[1]);
+      uint2 w;
+      w.x = pack_half2((v[i].x - mean) * rstd * g0.x + c0.x, (v[i].y - mean) * rstd * g0.y + c0.y);
+      w.y = pack_half2((v[i].z - mean) * rstd * g1.x + c1.x, (v[i].w - mean) * rstd * g1.y + c1.y);
+      *reinterpret_cast<uint2*>(o + 4 * c) = w;
+    }
+  }
+}
+
+__global__ void embed_kernel(const int* __restrict__ tokens, const __half* __restrict__ tok_emb,
+                             const __half* __restrict__ pos_emb, float* __restrict__ out, int batch, int pos_begin,
+                             int hidden, int pos_offset) {
+  const int row = blockIdx.x;
+  const int pos = pos_begin + row / batch;
+  const int tok = tokens[row];
+  const __half2* e = reinterpret_cast<const __half2*>(tok_emb + (long long)tok * hidden);
+  const __half2* p = reinterpret_cast<const __half2*>(pos_emb + (long long)(pos + pos_offset) * hidden);
+  float2* o = reinterpret_cast<float2*>(out + (long long)row * hidden);
+  for (int c = threadIdx.x; c < hidden / 2; c += blockDim.x) {
+    const float2 a = __half22float2(e[c]), b = __half22float2(p[c]);
+    o[c] = make_float2(a.x + b.x, a.y + b.y);
+  }
+}
+
+// one CTA per row; ties resolve to the smallest index (numpy/torch argmax convention)
+__global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* __restrict__ logits, long long ld, int cols,
+                                                             int* __restrict__ out_idx, float* __restrict__ out_val) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* r = logits + blockIdx.x * ld;
+  float best = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = r[c];
+    if (v > best || (v == best && c < bi)) {
+      best = v;
+      bi = c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = (l < nw) ? sv[l] : -FLT_MAX;
+    bi = (l < nw) ? si[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (threadIdx.x == 0) {
+      out_idx[blockIdx.x] = bi;
+      if (out_val) out_val[blockIdx.x] = best;
+    }
+  }
+}
+
+}  // namespace
+
+int layernorm(const float* x, long long ldx, const __half* gamma, const __half* beta, __half* out, long long ldo,
+              int rows, int hidden, float eps, cudaStream_t stream) {
+  if (rows < 0 || hidden <= 0 || hidden % 4 != 0 || ldx % 4 != 0 || ldo % 4 != 0) {
+    set_error("layernorm: rows=%d hidden=%d ldx=%lld ldo=%lld (hidden, strides must be multiples of 4)", rows, hidden,
+              ldx, ldo);
+    return KVPR_EINVAL;
+  }
+  if (rows == 0) return KVPR_OK;
+  const int nvec = hidden / 4;
+  const int vpt = (nvec + kRowThreads - 1) / kRowThreads;
+  if (vpt <= 1)
+    layernorm_kernel<1><<<rows, kRowThreads, 0, stream>>>(x, ldx, gamma, beta, out, ldo, hidden, eps);
+  else if (vpt <= 2)
+    layernorm_kernel<2><<<rows, kRowThreads, 0, stream>>>(x, ldx, gamma, beta, out, ldo, hidden, eps);
+  else if (vpt <= 4)
+    layernorm_kernel<4><<<rows, kRowThreads, 0, stream>>>(x, ldx, gamma, beta, out, ldo, hidden, eps);
+  else if (vpt <= 8)
+    layernorm_kernel<8><<<rows, kRowThreads, 0, stream>>>(x, ldx, gamma, beta, out, ldo, hidden, eps);
+  else {
+    set_error("layernorm: hidden=%d too large (max 8192)", hidden);
+    return KVPR_EINVAL;
+  }
+  return check_launch("layernorm");
+}
+
+int embed(const int* tokens, const __half* tok_emb, const __half* pos_emb, float* out, int rows, int batch,
+          int pos_begin, int hidden, int pos_offset, cudaStream_t stream) {
+  if (rows < 0 || batch <= 0 || hidden <= 0 || hidden % 2 != 0 || pos_begin < 0) {
+    set_error("embed: bad shape rows=%d batch=%d hidden=%d pos_begin=%d", rows, batch, hidden, pos_begin);
+    return KVPR_EINVAL;
+  }
+  if (rows == 0) return KVPR_OK;
+  embed_kernel<<<rows, 256, 0, stream>>>(tokens, tok_emb, pos_emb, out, batch, pos_begin, hidden, pos_offset);
+  return check_launch("embed");
+}
+
+int argmax_rows(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val,
+                cudaStream_t stream) {
+  if (rows < 0 || cols <= 0 || ld < cols) {
+    set_error("argmax: bad shape rows=%d cols=%d ld=%lld", rows, cols, ld);
+    return KVPR_EINVAL;
+  }
+  if (rows == 0) return KVPR_OK;
+  argmax_kernel<<<rows, kRowThreads, 0, stream>>>(logits, ld, cols, out_idx, out_val);
+  return check_launch("argmax");
+}
+
+}  // namespace kvpr

@@ -1,0 +1,343 @@
+// K1 and every other dense projection on the decode path: a persistent,
+// warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   D[m, n] = epilogue( sum_k A[m, k] * W[n, k] + bias[n] )
+//
+// A (activations, fp16, K-major) and W (weights, fp16, K-major, i.e. the
+// PyTorch Linear layout [out, in]) are streamed by TMA into a STAGES-deep
+// ring of 128B-swizzled shared-memory tiles.  One elected thread issues
+// tcgen05.mma (M=128, N=BN, K=16) into a double-buffered TMEM accumulator;
+// four epilogue warps drain TMEM with tcgen05.ld, add the bias, apply the
+// optional scale/ReLU/residual, convert, and scatter rows straight into the
+// caller's layout — for K1 that is the position-major KV page buffer, so the
+// recompute writes K and V where attention will read them with no separate
+// copy or cast kernel (reference semantics: numerics.py:129-137,
+// costmodel.py:169-176).
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
+// w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes [32*(w%4), +32)).
+
+#include "common.cuh"
+#include "kvpr_internal.h"
+
+namespace kvpr {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                        const GemmArgs p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::kBBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_blk * p.num_n_blk;
+  const int num_kb = p.num_k_blk;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / p.num_n_blk;
+        const int n_blk = tile % p.num_n_blk;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_2d(sA + stage * Cfg::kABytes, &tmap_a, &full[stage], kb * kBK, m_blk * kBM);
+          tma_load_2d(sB + stage * Cfg::kBBytes, &tmap_b, &full[stage], kb * kBK, n_blk * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread) ----------------
+      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, BN);
+      uint32_t stage = 0, phase = 0, local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // advancing K by 16 fp16 = 32 bytes inside the 128B swizzle atom
+            umma_f16(d_tmem, umma_desc_k_sw128(a_addr + k * 32), umma_desc_k_sw128(b_addr + k * 32), idesc,
+                     (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);  // frees this smem slot once the MMAs above retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> regs -> global ----------------
+    const uint32_t q = warp & 3;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int m_blk = tile / p.num_n_blk;
+      const int n_blk = tile % p.num_n_blk;
+      const uint32_t acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * kBM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      // row -> (group, offset) once per tile
+      const long long r_in = row_ok ? (row % p.row_group) : 0;
+      const long long r_grp = row_ok ? (row / p.row_group) : 0;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        __syncwarp();
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n0 = n_blk * BN + c * 32;
+        if (!row_ok || n0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (p.bias != nullptr) {
+          const uint4* bp = reinterpret_cast<const uint4*>(p.bias + n0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 bw = __ldg(bp + u);
+            const __half2* h2 = reinterpret_cast<const __half2*>(&bw);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float2 f = __half22float2(h2[e]);
+              v[u * 8 + e * 2] += f.x;
+              v[u * 8 + e * 2 + 1] += f.y;
+            }
+          }
+        }
+        if (n0 < p.scale_cols) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= p.scale;
+        }
+        if (p.flags & KVPR_EPI_RELU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+        }
+        const int seg = n0 / p.seg_width;
+        const int col = n0 - seg * p.seg_width;
+        const long long off = r_in * p.ld + r_grp * p.seg_group_stride[seg] + col;
+        if (p.flags & KVPR_EPI_F32) {
+          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.seg_ptr[seg]) + off);
+          if (p.flags & KVPR_EPI_ACCUM) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float4 old = o[u];
+              old.x += v[u * 4 + 0];
+              old.y += v[u * 4 + 1];
+              old.z += v[u * 4 + 2];
+              old.w += v[u * 4 + 3];
+              o[u] = old;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) o[u] = make_float4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+          }
+        } else {
+          uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.seg_ptr[seg]) + off);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack_half2(v[u * 8 + 0], v[u * 8 + 1]);
+            w.y = pack_half2(v[u * 8 + 2], v[u * 8 + 3]);
+            w.z = pack_half2(v[u * 8 + 4], v[u * 8 + 5]);
+            w.w = pack_half2(v[u * 8 + 6], v[u * 8 + 7]);
+            o[u] = w;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) != cudaSuccess ||
+        qres != cudaDriverEntryPointSuccess) {
+      return nullptr;
+    }
+    fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+  }
+  return fn;
+}
+
+// Row-major fp16 matrix [rows, cols] with row stride ld (elements) -> K-major 128B-swizzled boxes.
+static int make_tmap(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  if (enc == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return KVPR_ECUDA;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu ld=%llu", int(r),
+              (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld);
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
+template <int BN>
+static int launch_bn(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ta, tb;
+  int rc = make_tmap(&ta, a, args.M, args.K, lda, kBM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, w, args.N, args.K, ldw, BN);
+  if (rc) return rc;
+  args.num_m_blk = (args.M + kBM - 1) / kBM;
+  args.num_n_blk = (args.N + BN - 1) / BN;
+  args.num_k_blk = (args.K + kBK - 1) / kBK;
+  const int tiles = args.num_m_blk * args.num_n_blk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int attr_done[64] = {0};
+  if (dev < 64 && !attr_done[dev]) {
+    cudaFuncSetAttribute(gemm_tcgen05_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    attr_done[dev] = 1;
+  }
+  const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
+  gemm_tcgen05_kernel<BN><<<grid, 256, Cfg::kSmemBytes, stream>>>(ta, tb, args);
+  return check_launch("gemm_tcgen05");
+}
+
+int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
+             int bn, cudaStream_t stream) {
+  GemmArgs args = epi;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  if (M <= 0 || N <= 0 || K <= 0) {
+    set_error("gemm: non-positive shape M=%d N=%d K=%d", M, N, K);
+    return KVPR_EINVAL;
+  }
+  if (N % 32 != 0 || K % 8 != 0 || lda % 8 != 0 || ldw % 8 != 0) {
+    set_error("gemm: need N%%32==0, K%%8==0, lda/ldw%%8==0 (N=%d K=%d lda=%lld ldw=%lld)", N, K, lda, ldw);
+    return KVPR_EINVAL;
+  }
+  if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) {
+    set_error("gemm: operands must be 16-byte aligned");
+    return KVPR_EINVAL;
+  }
+  if (args.seg_width <= 0 || args.seg_width % 32 != 0 || args.row_group <= 0) {
+    set_error("gemm: epilogue seg_width must be a positive multiple of 32 and row_group > 0");
+    return KVPR_EINVAL;
+  }
+  const int nseg = (N + args.seg_width - 1) / args.seg_width;
+  if (nseg > 3) {
+    set_error("gemm: at most 3 output segments (N=%d seg_width=%d)", N, args.seg_width);
+    return KVPR_EINVAL;
+  }
+  for (int s = 0; s < nseg; ++s) {
+    if (args.seg_ptr[s] == nullptr || (reinterpret_cast<uintptr_t>(args.seg_ptr[s]) & 15)) {
+      set_error("gemm: output segment %d pointer null or misaligned", s);
+      return KVPR_EINVAL;
+    }
+  }
+  if (args.bias != nullptr && (reinterpret_cast<uintptr_t>(args.bias) & 15)) {
+    set_error("gemm: bias must be 16-byte aligned");
+    return KVPR_EINVAL;
+  }
+  switch (bn) {
+    case 256:
+      return launch_bn<256>(a, lda, w, ldw, args, stream);
+    case 128:
+      return launch_bn<128>(a, lda, w, ldw, args, stream);
+    case 64:
+      return launch_bn<64>(a, lda, w, ldw, args, stream);
+    default:
+      set_error("gemm: unsupported BN=%d", bn);
+      return KVPR_EINVAL;
+  }
+}
+
+}  // namespace kvpr

@@ -1,0 +1,51 @@
+// Internal (C++) declarations shared between the kernel translation units and
+// the extern "C" boundary in abi.cu.  Nothing here crosses the C-ABI.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kvpr.h"
+
+namespace kvpr {
+
+// Epilogue + shape bundle for the tcgen05 GEMM (passed by value as a kernel arg).
+//   out address of (m, n) = seg_ptr[n / seg_width]
+//                         + (m % row_group) * ld + (m / row_group) * seg_group_stride[seg]
+//                         + (n % seg_width)
+struct GemmArgs {
+  int M, N, K;
+  int num_m_blk, num_n_blk, num_k_blk;
+  const __half* bias;
+  int seg_width;
+  int row_group;
+  long long ld;
+  void* seg_ptr[3];
+  long long seg_group_stride[3];
+  float scale;
+  int scale_cols;
+  int flags;
+};
+
+int sm_count(int device);
+
+int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
+             int bn, cudaStream_t stream);
+
+int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch,
+                     int heads, int head_dim, int seq_len, float scale, cudaStream_t stream);
+
+int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim,
+                      int seq_len, float scale, cudaStream_t stream);
+
+int layernorm(const float* x, long long ldx, const __half* gamma, const __half* beta, __half* out, long long ldo,
+              int rows, int hidden, float eps, cudaStream_t stream);
+
+int embed(const int* tokens, const __half* tok_emb, const __half* pos_emb, float* out, int rows, int batch,
+          int pos_begin, int hidden, int pos_offset, cudaStream_t stream);
+
+int argmax_rows(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val,
+                cudaStream_t stream);
+
+}  // namespace kvpr

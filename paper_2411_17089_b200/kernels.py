@@ -1,0 +1,144 @@
+"""Torch-tensor front end over the C-ABI (device plumbing only).
+
+Each function checks dtype/device/contiguity, pulls raw pointers and the
+current CUDA stream, and calls exactly one libkvpr entry point.  Nothing here
+computes on the CPU; a missing library or a non-CUDA tensor is an error.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+
+
+def _stream(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def recompute_kv(x: torch.Tensor, w_kv: torch.Tensor, b_kv: torch.Tensor | None, kv_pages: torch.Tensor,
+                 batch: int, pos_begin: int, pos_end: int, stream=None) -> None:
+    """K1: K/V of positions [pos_begin, pos_end) from X, written into the page buffer."""
+    _need(x, torch.float16, "x")
+    _need(w_kv, torch.float16, "w_kv")
+    _need(kv_pages, torch.float16, "kv_pages")
+    hidden = w_kv.shape[1]
+    if w_kv.shape[0] != 2 * hidden or not w_kv.is_contiguous():
+        raise ValueError("w_kv must be contiguous [2*hidden, hidden]")
+    if b_kv is not None:
+        _need(b_kv, torch.float16, "b_kv")
+    need_x = pos_end * batch * hidden
+    need_kv = pos_end * 2 * batch * hidden
+    if x.numel() < need_x or kv_pages.numel() < need_kv:
+        raise ValueError("x / kv_pages too small for the requested positions")
+    _lib.call(
+        "kvpr_recompute_kv",
+        x.data_ptr(), w_kv.data_ptr(), b_kv.data_ptr() if b_kv is not None else None, kv_pages.data_ptr(),
+        batch, pos_begin, pos_end, hidden, _stream(stream),
+    )
+
+
+def linear(a: torch.Tensor, w: torch.Tensor, epi: _lib.Epilogue, M: int | None = None, bn: int = 0,
+           stream=None, lda: int | None = None) -> None:
+    """out = epilogue(A[M,K] . W[N,K]^T + bias) via the tcgen05 GEMM."""
+    _need(a, torch.float16, "a")
+    _need(w, torch.float16, "w")
+    N, K = w.shape
+    if M is None:
+        M = a.shape[0]
+    lda = K if lda is None else lda
+    _lib.call("kvpr_linear", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn, _stream(stream))
+
+
+def linear_simple(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, out: torch.Tensor,
+                  flags: int = 0, bn: int = 0, stream=None) -> torch.Tensor:
+    """Row-major out[M, N] (fp16 or fp32 per flags) = epilogue(a . w^T + bias)."""
+    N = w.shape[0]
+    M = a.shape[0]
+    if out.dtype == torch.float32:
+        flags |= _lib.EPI_F32
+    epi = _lib.make_epilogue([(out.data_ptr(), 0)], seg_width=_seg_width(N), ld=out.stride(0), row_group=M,
+                             bias=bias.data_ptr() if bias is not None else None, flags=flags)
+    # a single segment must cover all N columns
+    epi.seg_width = ((N + 31) // 32) * 32
+    linear(a, w, epi, M=M, bn=bn, stream=stream)
+    return out
+
+
+def _seg_width(n: int) -> int:
+    return ((n + 31) // 32) * 32
+
+
+def decode_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor, ws: torch.Tensor | None,
+                     batch: int, heads: int, head_dim: int, seq_len: int, scale: float | None = None,
+                     stream=None) -> torch.Tensor:
+    """K2: softmax(scale * K q) V per (sequence, head) over pages [0, seq_len)."""
+    _need(q, torch.float16, "q")
+    _need(kv_pages, torch.float16, "kv_pages")
+    _need(out, torch.float16, "out")
+    if scale is None:
+        scale = 1.0 / math.sqrt(head_dim)
+    ws_ptr, ws_bytes = (ws.data_ptr(), ws.numel() * ws.element_size()) if ws is not None else (None, 0)
+    _lib.call(
+        "kvpr_decode_attention",
+        q.data_ptr(), kv_pages.data_ptr(), out.data_ptr(), ws_ptr, ws_bytes,
+        batch, heads, head_dim, seq_len, float(scale), _stream(stream),
+    )
+    return out
+
+
+def prefill_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor, batch: int, heads: int,
+                      head_dim: int, seq_len: int, scale: float | None = None, stream=None) -> torch.Tensor:
+    if scale is None:
+        scale = 1.0 / math.sqrt(head_dim)
+    _lib.call(
+        "kvpr_prefill_attention",
+        q.data_ptr(), kv_pages.data_ptr(), out.data_ptr(), batch, heads, head_dim, seq_len, float(scale),
+        _stream(stream),
+    )
+    return out
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, out: torch.Tensor, rows: int | None = None,
+              eps: float = 1e-5, stream=None) -> torch.Tensor:
+    _need(x, torch.float32, "x")
+    _need(out, torch.float16, "out")
+    hidden = gamma.numel()
+    rows = x.shape[0] if rows is None else rows
+    _lib.call(
+        "kvpr_layernorm", x.data_ptr(), x.stride(0), gamma.data_ptr(), beta.data_ptr(), out.data_ptr(),
+        out.stride(0), rows, hidden, float(eps), _stream(stream),
+    )
+    return out
+
+
+def embed(tokens: torch.Tensor, tok_emb: torch.Tensor, pos_emb: torch.Tensor, out: torch.Tensor, batch: int,
+          pos_begin: int, pos_offset: int = 2, stream=None) -> torch.Tensor:
+    _need(tokens, torch.int32, "tokens")
+    rows = tokens.numel()
+    _lib.call(
+        "kvpr_embed", tokens.data_ptr(), tok_emb.data_ptr(), pos_emb.data_ptr(), out.data_ptr(), rows, batch,
+        pos_begin, tok_emb.shape[1], pos_offset, _stream(stream),
+    )
+    return out
+
+
+def argmax(logits: torch.Tensor, out_idx: torch.Tensor, out_val: torch.Tensor | None = None, cols: int | None = None,
+           stream=None) -> torch.Tensor:
+    _need(logits, torch.float32, "logits")
+    cols = logits.shape[1] if cols is None else cols
+    _lib.call(
+        "kvpr_argmax", logits.data_ptr(), logits.stride(0), logits.shape[0], cols, out_idx.data_ptr(),
+        out_val.data_ptr() if out_val is not None else None, _stream(stream),
+    )
+    return out_idx

@@ -1,0 +1,218 @@
+"""Per-kernel numerics on the B200 against plain PyTorch fp32 references.
+
+Tolerances (floating point, fp16 storage / fp32 accumulation):
+  GEMM / recompute / LN outputs: |out - ref| <= 2e-3 * max|ref| + 2e-3  (fp16 output rounding)
+  attention outputs:             |out - ref| <= 2e-3 * max|ref| + 2e-3
+The bit-level split/merge property (recomputed pages == prefill pages) is
+checked in test_runtime_gpu.py.
+"""
+
+from __future__ import annotations
+
+import math
+
+import pytest
+import torch
+
+from paper_2411_17089_b200 import _lib, kernels
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(out, ref, rtol=2e-3, atol=2e-3):
+    out = out.float()
+    ref = ref.float()
+    err = (out - ref).abs().max().item()
+    bound = rtol * ref.abs().max().item() + atol
+    assert err <= bound, f"max err {err:.3e} > {bound:.3e}"
+
+
+def _rand(*shape, scale=1.0, dev="cuda", seed=None, dtype=torch.float16):
+    g = torch.Generator(device="cpu")
+    g.manual_seed(seed if seed is not None else sum(shape))
+    return (torch.randn(*shape, generator=g) * scale).to(dtype).to(dev)
+
+
+@pytest.mark.parametrize(
+    "M,N,K,bn",
+    [
+        (128, 256, 64, 256),
+        (300, 512, 4096, 256),
+        (32, 768, 768, 64),
+        (32, 2304, 768, 128),
+        (4096, 4096, 512, 256),  # > 148 tiles: persistent loop + TMEM double buffer
+        (1, 64, 128, 64),
+        (5, 50272, 768, 0),  # vocab-sized N tail, auto BN
+        (777, 1024, 1000, 128),  # K tail (TMA zero fill)
+    ],
+)
+def test_linear_matches_fp32(dev, M, N, K, bn):
+    a = _rand(M, K, scale=0.5, seed=1)
+    w = _rand(N, K, scale=0.05, seed=2)
+    bias = _rand(N, scale=0.1, seed=3)
+    out = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, out, bn=bn)
+    ref = a.float() @ w.float().T + bias.float()
+    torch.cuda.synchronize()
+    _close(out, ref)
+
+
+def test_linear_epilogues(dev):
+    M, N, K = 96, 512, 256
+    a = _rand(M, K, scale=0.5, seed=4)
+    w = _rand(N, K, scale=0.05, seed=5)
+    bias = _rand(N, scale=0.1, seed=6)
+    ref = a.float() @ w.float().T + bias.float()
+    # relu, fp16
+    out = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, out, flags=_lib.EPI_RELU)
+    _close(out, ref.clamp_min(0))
+    # fp32 out
+    out32 = torch.empty(M, N, dtype=torch.float32, device=dev)
+    kernels.linear_simple(a, w, bias, out32)
+    _close(out32, ref, rtol=1e-5, atol=1e-4)
+    # residual accumulate
+    resid = torch.randn(M, N, device=dev)
+    acc = resid.clone()
+    kernels.linear_simple(a, w, bias, acc, flags=_lib.EPI_ACCUM)
+    _close(acc, resid + ref, rtol=1e-5, atol=1e-4)
+    # scaled leading columns + 3 segments with row groups (q | k | v scatter)
+    seg = 128
+    M2 = 4 * 3  # 3 positions x batch 4
+    a2 = _rand(M2, K, scale=0.5, seed=7)
+    w2 = _rand(3 * seg, K, scale=0.05, seed=8)
+    b2 = _rand(3 * seg, scale=0.1, seed=9)
+    qbuf = torch.zeros(M2, seg, dtype=torch.float16, device=dev)
+    pages = torch.zeros(3, 2, 4, seg, dtype=torch.float16, device=dev)
+    epi = _lib.make_epilogue(
+        [(qbuf.data_ptr(), 4 * seg), (pages[:, 0].data_ptr(), 2 * 4 * seg), (pages[:, 1].data_ptr(), 2 * 4 * seg)],
+        seg_width=seg, ld=seg, row_group=4, bias=b2.data_ptr(), scale=0.125, scale_cols=seg,
+    )
+    kernels.linear(a2, w2, epi)
+    ref2 = a2.float() @ w2.float().T + b2.float()
+    torch.cuda.synchronize()
+    _close(qbuf, ref2[:, :seg] * 0.125)
+    _close(pages[:, 0].reshape(M2, seg), ref2[:, seg:2 * seg])
+    _close(pages[:, 1].reshape(M2, seg), ref2[:, 2 * seg:])
+
+
+@pytest.mark.parametrize("batch,hidden,p0,p1", [(4, 768, 0, 257), (4, 768, 3, 250), (3, 256, 5, 6), (32, 512, 0, 40)])
+def test_recompute_kv_writes_pages(dev, batch, hidden, p0, p1):
+    S = p1 + 3
+    x = _rand(S, batch, hidden, scale=1.0, seed=10)
+    w_kv = _rand(2 * hidden, hidden, scale=0.03, seed=11)
+    b_kv = _rand(2 * hidden, scale=0.1, seed=12)
+    pages = torch.full((S, 2, batch, hidden), 7.0, dtype=torch.float16, device=dev)
+    kernels.recompute_kv(x, w_kv, b_kv, pages, batch, p0, p1)
+    torch.cuda.synchronize()
+    ref = x[p0:p1].float() @ w_kv.float().T + b_kv.float()  # [P, batch, 2h]
+    _close(pages[p0:p1, 0], ref[..., :hidden])
+    _close(pages[p0:p1, 1], ref[..., hidden:])
+    # positions outside [p0, p1) untouched
+    assert torch.all(pages[:p0] == 7.0) and torch.all(pages[p1:] == 7.0)
+
+
+def test_recompute_split_zero_is_noop(dev):
+    pages = torch.full((4, 2, 2, 64), 3.0, dtype=torch.float16, device=dev)
+    x = torch.zeros(4, 2, 64, dtype=torch.float16, device=dev)
+    w = torch.zeros(128, 64, dtype=torch.float16, device=dev)
+    kernels.recompute_kv(x, w, None, pages, 2, 2, 2)
+    assert torch.all(pages == 3.0)
+
+
+def test_recompute_rejects_bad_split(dev):
+    pages = torch.zeros(4, 2, 2, 64, dtype=torch.float16, device=dev)
+    x = torch.zeros(4, 2, 64, dtype=torch.float16, device=dev)
+    w = torch.zeros(128, 64, dtype=torch.float16, device=dev)
+    with pytest.raises(ValueError, match="split"):
+        kernels.recompute_kv(x, w, None, pages, 2, 3, 1)
+
+
+def _attn_ref(q, pages, batch, heads, d, seq):
+    # q [batch, h]; pages [S, 2, batch, h]
+    K = pages[:seq, 0].float().reshape(seq, batch, heads, d)
+    V = pages[:seq, 1].float().reshape(seq, batch, heads, d)
+    qh = q.float().reshape(batch, heads, d)
+    logits = torch.einsum("sbhd,bhd->bhs", K, qh) / math.sqrt(d)
+    w = torch.softmax(logits, dim=-1)
+    return torch.einsum("bhs,sbhd->bhd", w, V).reshape(batch, heads * d)
+
+
+@pytest.mark.parametrize(
+    "batch,heads,d,seq",
+    [(4, 12, 64, 257), (2, 32, 128, 1025), (32, 32, 128, 1025), (1, 2, 64, 1), (3, 4, 128, 70), (1, 1, 128, 8193)],
+)
+def test_decode_attention_matches_fp32(dev, batch, heads, d, seq):
+    h = heads * d
+    pages = _rand(seq + 5, 2, batch, h, scale=1.0, seed=seq)
+    q = _rand(batch, h, scale=1.0, seed=seq + 1)
+    out = torch.empty(batch, h, dtype=torch.float16, device=dev)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+    kernels.decode_attention(q, pages, out, ws, batch, heads, d, seq)
+    torch.cuda.synchronize()
+    _close(out, _attn_ref(q, pages, batch, heads, d, seq))
+    # without workspace (single split) gives the same answer
+    out1 = torch.empty_like(out)
+    kernels.decode_attention(q, pages, out1, None, batch, heads, d, seq)
+    torch.cuda.synchronize()
+    _close(out1, _attn_ref(q, pages, batch, heads, d, seq))
+
+
+def test_decode_attention_empty_cache_rejected(dev):
+    q = torch.zeros(1, 64, dtype=torch.float16, device=dev)
+    pages = torch.zeros(1, 2, 1, 64, dtype=torch.float16, device=dev)
+    with pytest.raises(ValueError, match="empty"):
+        kernels.decode_attention(q, pages, torch.empty_like(q), None, 1, 1, 64, 0)
+
+
+@pytest.mark.parametrize("batch,heads,d,seq", [(2, 4, 64, 37), (3, 2, 128, 130)])
+def test_prefill_attention_causal(dev, batch, heads, d, seq):
+    h = heads * d
+    pages = _rand(seq, 2, batch, h, seed=20)
+    q = _rand(seq, batch, h, seed=21)
+    out = torch.empty(seq, batch, h, dtype=torch.float16, device=dev)
+    kernels.prefill_attention(q, pages, out, batch, heads, d, seq)
+    torch.cuda.synchronize()
+    K = pages[:, 0].float().reshape(seq, batch, heads, d)
+    V = pages[:, 1].float().reshape(seq, batch, heads, d)
+    qh = q.float().reshape(seq, batch, heads, d)
+    logits = torch.einsum("tbhd,sbhd->bhts", qh, K) / math.sqrt(d)
+    mask = torch.triu(torch.ones(seq, seq, dtype=torch.bool, device=dev), 1)
+    logits = logits.masked_fill(mask, float("-inf"))
+    ref = torch.einsum("bhts,sbhd->tbhd", torch.softmax(logits, -1), V).reshape(seq, batch, h)
+    _close(out, ref)
+
+
+@pytest.mark.parametrize("rows,hidden", [(32, 4096), (7, 768), (3, 7168), (1, 5120)])
+def test_layernorm(dev, rows, hidden):
+    x = torch.randn(rows, hidden, device=dev) * 3 + 1
+    g = _rand(hidden, scale=0.1, seed=30) + 1
+    b = _rand(hidden, scale=0.1, seed=31)
+    out = torch.empty(rows, hidden, dtype=torch.float16, device=dev)
+    kernels.layernorm(x, g, b, out)
+    ref = torch.nn.functional.layer_norm(x, (hidden,), g.float(), b.float(), 1e-5)
+    torch.cuda.synchronize()
+    _close(out, ref)
+
+
+def test_embed_and_argmax(dev):
+    V, P, h, batch = 1000, 40, 256, 3
+    E = _rand(V, h, seed=40)
+    Pe = _rand(P, h, seed=41)
+    toks = torch.tensor([5, 999, 0, 17, 3, 3], dtype=torch.int32, device=dev)  # 2 positions x 3
+    out = torch.empty(6, h, device=dev)
+    kernels.embed(toks, E, Pe, out, batch=batch, pos_begin=7, pos_offset=2)
+    pos = torch.tensor([7, 7, 7, 8, 8, 8], device=dev) + 2
+    ref = E[toks.long()].float() + Pe[pos].float()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    logits = torch.randn(5, 50272, device=dev)
+    logits[2, 123] = 1e4
+    logits[3, 7] = logits[3, 9] = 1e4  # tie -> smallest index
+    idx = torch.empty(5, dtype=torch.int32, device=dev)
+    val = torch.empty(5, device=dev)
+    kernels.argmax(logits, idx, val)
+    torch.cuda.synchronize()
+    ref_idx = logits.argmax(dim=1)
+    assert idx.tolist() == ref_idx.tolist()
+    assert idx[3].item() == 7
