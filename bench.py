@@ -1,0 +1,382 @@
+"""Decode throughput of KVPR's offloaded decode path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kvpr|reference] [--model opt-6.7b]
+                    [--batch 32] [--prompt 1024]
+
+Metric (BASELINE.json): decode tokens/s + per-layer latency, OPT-6.7B b32
+prompt 1024, KV offloaded to host.  One "step" = one decode token for every
+sequence of the batch through all layers: per layer H2D X[:, :l] + KV[l:s'-1]
+from page-locked host stores, K1 recompute of K,V[0:l), K2 attention, the
+rest of the OPT layer, D2H of the new X row and K,V page.  l per step comes
+from the bit-exact split solver (column mode) fed by the live profile of
+this GPU (profiler.measure -> hwprofile.calibrate).
+
+value     device-timed (CUDA events, compute stream) tokens/s over K steps,
+          inputs = the host stores (the workload defines them to live in
+          host DRAM; they are streamed over PCIe inside every step).
+e2e       the same through the public per-step API: prompt/next-token ids
+          H2D from pinned host memory and the generated ids D2H every step,
+          host-synchronised per step.
+roofline  the per-layer overlap roofline of the north star,
+          T_roof(l) = max(H2D bytes / BW_h2d_measured, recompute FLOPs / F_peak):
+          achieved = algorithmic H2D bytes per layer / measured layer time.
+          Kernel rooflines (K1 tensor, K2 HBM) are measured in the same run.
+Multi-GPU (torchrun): batch-partitioned replicas, one per GPU, each with its
+own host stores and PCIe link; no data-path collective (scaling "weak").
+--impl reference: the reference's CPU path (split_merge_kv + decode_attention,
+fp64 NumPy, restated in oracle/numerics_ref.py) timed on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback"
+    return d
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm
+
+def cpu_reference_sample(hidden, heads, seq_len, split, budget_s=12.0, max_reps=40, seed=0):
+    """Time the reference CPU path for ONE sequence-layer: split_merge_kv + decode_attention (fp64)."""
+    import numpy as np
+
+    from oracle import numerics_ref as nr
+
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((seq_len, hidden))
+    w_k = rng.standard_normal((hidden, hidden)) * 0.02
+    w_v = rng.standard_normal((hidden, hidden)) * 0.02
+    w_o = rng.standard_normal((hidden, hidden)) * 0.02
+    q = rng.standard_normal(hidden)
+    k_suf = rng.standard_normal((heads, seq_len - split, hidden // heads))
+    v_suf = rng.standard_normal((heads, seq_len - split, hidden // heads))
+    suffix = nr.KVState(k_suf, v_suf)
+    ts = []
+    t_begin = time.perf_counter()
+    while len(ts) < max_reps and (time.perf_counter() - t_begin) < budget_s:
+        t0 = time.perf_counter()
+        kv = nr.split_merge_kv(x, split, w_k, w_v, suffix)
+        nr.decode_attention(q, kv, w_o)
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), len(ts)
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads") or 0) for i in threadpool_info()) or os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2411_17089_b200.costmodel import WorkloadSpec
+    from paper_2411_17089_b200.hwprofile import HardwareProfile
+    from paper_2411_17089_b200.scheduler import plan_generation
+    from paper_2411_17089_b200.weights import preset
+
+    cfg = preset(args.model)
+    wl = WorkloadSpec(batch_size=args.batch, prompt_len=args.prompt, gen_len=args.warmup + args.steps)
+    prof = HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=55e9)
+    plan = plan_generation(cfg.spec(), wl, prof, "column")
+    # each "step" = one decode token for the batch; bounded sample: one sequence-layer per step
+    per_step = []
+    t_wall0 = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        d = plan.decisions[i]
+        t, _ = cpu_reference_sample(cfg.hidden, cfg.heads, d.seq_len, d.recompute_len, budget_s=0.0, max_reps=1,
+                                    seed=i)
+        if i >= args.warmup:
+            per_step.append(t * cfg.layers * args.batch)  # extrapolated full step (b sequences x L layers)
+    step_s = sum(per_step) / len(per_step)
+    value = args.batch / step_s
+    cores = blas_threads()
+    sample = (f"1 sequence x 1 layer of split_merge_kv+decode_attention (fp64 NumPy) per step at the step's "
+              f"(s', l), x{args.batch} seqs x{cfg.layers} layers extrapolated")
+    line = {
+        "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "impl": "reference",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV offloaded to host",
+                   "mode": "column", "profile": "b200-guess (1391.2e12 FLOP/s, 55e9 B/s) for the split"},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample,
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_wall0,
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+
+class Clocks:
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms",
+                                       "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, gpu_index=0):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            c = [x.strip() for x in line.split(",")]
+            if len(c) >= 9 and c[0].isdigit() and int(c[0]) == gpu_index:
+                rows.append(c)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+def run_kvpr(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_17089_b200 import kernels, profiler
+    from paper_2411_17089_b200.costmodel import WorkloadSpec, activation_bytes, kv_remainder_bytes, recompute_flops
+    from paper_2411_17089_b200.runtime import DecodeTiming, KVPRRuntime
+    from paper_2411_17089_b200.scheduler import overlap_roofline, plan_generation
+    from paper_2411_17089_b200.weights import OPTWeights, preset
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    cfg = preset(args.model)
+    cfg = cfg.with_positions(args.prompt + args.warmup + args.steps + 8)
+    b = args.batch
+    total_steps = args.warmup + args.steps
+    wl = WorkloadSpec(batch_size=b, prompt_len=args.prompt, gen_len=total_steps)
+
+    # profiler -> scheduler (bit-exact solver on the live profile)
+    calib, recs = profiler.measure(cfg.hidden, b, device=dev)
+    prof = calib.profile
+    bw_peak = profiler.peak_h2d(recs)
+    plan = plan_generation(cfg.spec(), wl, prof, "column")
+    splits = plan.splits
+
+    w = OPTWeights.random(cfg, seed=0, device=dev)
+    g = torch.Generator().manual_seed(1 + rank)
+    prompt = torch.randint(0, cfg.vocab, (b, args.prompt), generator=g)
+    rt = KVPRRuntime(w, b, args.prompt + total_steps + 1, device=dev)
+    t0 = time.perf_counter()
+    first = rt.prefill(prompt)
+    prefill_s = time.perf_counter() - t0
+
+    # warmup steps (untimed)
+    rt.decode(splits[: args.warmup], tokens=first)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks() if rank == 0 else None
+    launches0 = rt.launches
+    tim = DecodeTiming()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    start.record(rt.cs)
+    rt.decode(splits[args.warmup:], timing=tim)
+    end.record(rt.cs)
+    torch.cuda.synchronize(dev)
+    launches = rt.launches - launches0
+    elapsed = start.elapsed_time(end) / 1e3
+    clk = clocks.stop(local) if clocks else None
+    if ws > 1:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = ws * b * args.steps / elapsed
+
+    # per-layer latency and overlap roofline over the timed steps
+    L = cfg.layers
+    layer_ms = [x for row in tim.layer_ms for x in row[1:]]  # drop each step's first layer (embed + fill)
+    steady_layer_s = (sorted(layer_ms)[len(layer_ms) // 2] / 1e3) if layer_ms else elapsed / (args.steps * L)
+    f_peak = peaks["bf16_tflops_sustained"] * 1e12
+    troof, h2d_alg, flops_alg = 0.0, 0.0, 0.0
+    for d in plan.decisions[args.warmup:]:
+        troof += overlap_roofline(cfg.spec(), wl, d.seq_len, d.recompute_len, bw_peak, f_peak) * L
+        lp = min(d.recompute_len, d.seq_len - 1)
+        h2d_alg += (activation_bytes(cfg.spec(), wl, lp) + kv_remainder_bytes(cfg.spec(), wl, d.seq_len - 1, lp)) * L
+        flops_alg += recompute_flops(cfg.spec(), wl, lp) * L
+    achieved_gbs = h2d_alg / elapsed / 1e9
+
+    # kernel rooflines, measured on the compute stream after the timed region
+    mid = plan.decisions[args.warmup + args.steps // 2]
+    lmid = min(mid.recompute_len, mid.seq_len - 1)
+    kern = {}
+    if rank == 0:
+        lw = w.layers[0]
+        xd, kvd = rt.x_dev[0], rt.kv_dev[0]
+
+        def ev_time(fn, reps=10):
+            for _ in range(3):
+                fn()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(rt.cs)
+            for _ in range(reps):
+                fn()
+            e.record(rt.cs)
+            e.synchronize()
+            return a.elapsed_time(e) / reps / 1e3
+
+        if lmid > 0:
+            t_k1 = ev_time(lambda: kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, 0, lmid, stream=rt.cs))
+            fl = recompute_flops(cfg.spec(), wl, lmid)
+            kern["k1_recompute_gemm"] = {"bound": "tensor", "achieved": fl / t_k1 / 1e12,
+                                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                                         "frac": fl / t_k1 / 1e12 / peaks["bf16_tflops"], "traffic": None,
+                                         "us": t_k1 * 1e6, "M": b * lmid, "N": 2 * cfg.hidden, "K": cfg.hidden}
+        s = mid.seq_len
+        t_k2 = ev_time(lambda: kernels.decode_attention(rt.q, kvd, rt.attn, rt.ws, b, cfg.heads, cfg.head_dim, s,
+                                                        stream=rt.cs))
+        by = 2 * b * s * cfg.hidden * 2
+        kern["k2_decode_attention"] = {"bound": "hbm", "achieved": by / t_k2 / 1e9, "peak": peaks["hbm_gbs"],
+                                       "unit": "GB/s", "frac": by / t_k2 / 1e9 / peaks["hbm_gbs"], "traffic": None,
+                                       "us": t_k2 * 1e6}
+
+    # e2e through the public per-step API (host token ids in/out every step)
+    rt.reset(args.prompt + args.warmup)
+    tok_host = torch.empty(b, dtype=torch.int32, pin_memory=True)
+    tok_host.copy_(first.cpu())
+    e2e_steps = min(args.steps, 4)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    te0 = time.perf_counter()
+    for i in range(e2e_steps):
+        out = rt.decode([splits[args.warmup + i]], tokens=tok_host.to(dev, non_blocking=True))
+        tok_host.copy_(out[0], non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    e2e_s = time.perf_counter() - te0
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = ws * b * e2e_steps / e2e_s
+    h2d_step = h2d_alg / args.steps + b * 4
+    d2h_step = (3 * b * cfg.hidden * 2) * L + b * 4
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        t_seq_layer, n = cpu_reference_sample(cfg.hidden, cfg.heads, mid.seq_len, mid.recompute_len,
+                                              budget_s=args.cpu_budget)
+        cpu_tok_s = 1.0 / (t_seq_layer * L)
+        cpu = {"value": cpu_tok_s, "unit": "tok/s", "cores": blas_threads(), "kind": "port",
+               "sample": (f"{n} reps of one sequence-layer split_merge_kv+decode_attention (fp64 NumPy, "
+                          f"oracle/numerics_ref.py) at s'={mid.seq_len}, l={mid.recompute_len}; "
+                          f"tok/s = 1/(t x {L} layers)"),
+               "host_cpus": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "config": {
+                "workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV+X offloaded to pinned host",
+                "model": args.model, "global_batch": b * ws, "seq_len": args.prompt, "parallelism": f"batch-partition x{ws}",
+                "mode": "column", "splits_timed": splits[args.warmup:],
+                "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
+                "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
+            },
+            "roofline": {
+                "bound": "pcie", "achieved": achieved_gbs, "peak": bw_peak / 1e9, "unit": "GB/s",
+                "frac": troof / elapsed, "traffic": None,
+                "note": "overlap roofline per layer max(H2D(X[:, :l]+KV[l:s'-1]) / measured pinned H2D peak, "
+                        "4bl h^2 / sustained bf16 peak); frac = T_roof / T_measured",
+                "kernels": kern,
+            },
+            "profile": {"gpu_flops": prof.gpu_flops, "h2d_bandwidth": prof.h2d_bandwidth,
+                        "d2h_bandwidth": prof.d2h_bandwidth, "transfer_latency": prof.transfer_latency},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": int(h2d_step),
+                    "d2h_bytes_per_step": int(d2h_step), "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "peaks_source": peaks["source"],
+        }
+        print(json.dumps(line))
+    rt.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kvpr", choices=["kvpr", "reference"])
+    ap.add_argument("--model", default="opt-6.7b")
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--prompt", type=int, default=1024)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_kvpr(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,13 @@ int kvpr_embed(const int* tokens, const void* tok_emb, const void* pos_emb, floa
 /* K8 tail — per-row argmax (greedy token) of fp32 logits. */
 int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val, void* stream);
 
+/* Enqueue one DMA (cudaMemcpyAsync, direction inferred from UVA) on `stream`.
+ * The runtime's H2D of X[:, :l] / KV[l:s'-1] and D2H of the new X row / K,V page
+ * (pipesim graph.py:266-347 load_activation_recompute / load_cache /
+ * store_activation / store_cache) go through here.  Host buffers must be
+ * page-locked for the copy to be asynchronous. */
+int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,7 @@ EXPORTS = (
     "kvpr_layernorm",
     "kvpr_embed",
     "kvpr_argmax",
+    "kvpr_copy_async",
 )
 
 
@@ -75,6 +76,7 @@ _SIGS = {
     "kvpr_layernorm": ([_vp, _ll, _vp, _vp, _vp, _ll, _i, _i, _f, _vp], _i),
     "kvpr_embed": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp], _i),
     "kvpr_argmax": ([_vp, _ll, _i, _i, _vp, _vp, _vp], _i),
+    "kvpr_copy_async": ([_vp, _vp, _sz, _vp], _i),
 }
 
 

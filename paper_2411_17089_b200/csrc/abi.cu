@@ -157,4 +157,19 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
   return argmax_rows(logits, ld, rows, cols, out_idx, out_val, static_cast<cudaStream_t>(stream));
 }
 
+int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  g_err[0] = 0;
+  if (bytes == 0) return KVPR_OK;
+  if (dst == nullptr || src == nullptr) {
+    set_error("copy_async: null pointer");
+    return KVPR_EINVAL;
+  }
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error("copy_async: %s", cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
 }  // extern "C"

@@ -1,0 +1,368 @@
+"""KVPR decode runtime on one B200: weights resident in HBM, each layer's
+inputs X and KV cache offloaded to page-locked host memory, and per layer
+
+    copy stream     H2D X[:, :l] (chunked)  ->  H2D KV[l:s'-1]          (one DMA each)
+    compute stream  LN1 -> q,k,v (k,v appended at page s'-1) -> K1 on each
+                    landed X chunk -> [wait KV] -> K2 attention -> out-proj
+                    -> LN2 -> fc1 -> fc2
+    d2h stream      new X row and new K,V page -> host stores
+
+ordered only by CUDA events, with layer u+1's transfers issued while layer u
+computes (double-buffered device pages).  This realises the task DAG of the
+reference simulator (pipesim/graph.py:1-28, 232-347; Algorithm 1 of the
+paper): MHA waits on recompute AND the KV load, the
+recompute waits on its staged activations, the KV load of step i waits on the
+store of step i-1, H2D issue order is activations-for-recompute before KV
+(graph.py:56-67), double-buffer depth 2 (graph.py:215-221).  The split l per
+step comes from the bit-exact solver (scheduler.plan_generation); the
+runtime executes whatever plan it is given (plan JSON, constant plans for
+sweeps).  Nothing here computes on the CPU and there is no fallback path:
+every kernel is a libkvpr.so launch.
+
+Device layouts (include/kvpr.h): pages [pos][2][batch][hidden] fp16 (K then V);
+X [pos][batch][hidden] fp16; residual stream fp32 [batch][hidden].
+Host stores use the same position-major layout per layer, so X[:, :l] and
+KV[l:s'-1] are single contiguous byte ranges.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib, kernels
+from .weights import OPTWeights
+
+F16 = torch.float16
+F32 = torch.float32
+
+
+def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) -> None:
+    if nbytes:
+        _lib.call("kvpr_copy_async", dst_ptr, src_ptr, nbytes, stream.cuda_stream)
+
+
+class HostStores:
+    """Per-layer X and KV stores in page-locked host memory (exact-size cudaHostRegister)."""
+
+    def __init__(self, layers: int, capacity: int, batch: int, hidden: int):
+        self.layers, self.capacity, self.batch, self.hidden = layers, capacity, batch, hidden
+        self.x = torch.empty(layers, capacity, batch, hidden, dtype=F16)
+        self.kv = torch.empty(layers, capacity, 2, batch, hidden, dtype=F16)
+        self._registered = []
+        for t in (self.x, self.kv):
+            rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * t.element_size(), 0)
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister failed ({rc}) for {t.numel() * 2 / 2**30:.1f} GiB")
+            self._registered.append(t)
+
+    @property
+    def nbytes(self) -> int:
+        return (self.x.numel() + self.kv.numel()) * 2
+
+    def close(self) -> None:
+        for t in self._registered:
+            torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+        self._registered = []
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class DecodeTiming:
+    """CUDA-event timings of a decode run (compute stream)."""
+
+    step_ms: list[float] = field(default_factory=list)
+    layer_ms: list[list[float]] = field(default_factory=list)  # per step, per layer (consecutive layer ends)
+
+
+def chunk_bounds(n: int, chunks: int, min_rows: int = 64) -> list[tuple[int, int]]:
+    """Split [0, n) into <= chunks contiguous position ranges (>= min_rows each when possible)."""
+    if n <= 0:
+        return []
+    c = max(1, min(chunks, n // min_rows if n >= min_rows else 1))
+    base, rem = divmod(n, c)
+    out, p = [], 0
+    for i in range(c):
+        q = p + base + (1 if i < rem else 0)
+        out.append((p, q))
+        p = q
+    return out
+
+
+class KVPRRuntime:
+    """One decoder replica on one GPU (the unit the batch-partitioned multi-GPU mode replicates)."""
+
+    def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
+                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None):
+        cfg = weights.cfg
+        if capacity > cfg.max_pos:
+            raise ValueError(f"capacity {capacity} exceeds the position table ({cfg.max_pos})")
+        self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
+        self.dev = torch.device(device) if device is not None else weights.embed.device
+        self.chunks, self.nbuf = chunks, nbuf
+        _lib.load()
+        h, b = cfg.hidden, batch
+        with torch.cuda.device(self.dev):
+            self.cs = torch.cuda.Stream(self.dev, priority=-1)  # compute
+            self.hs = torch.cuda.Stream(self.dev)              # H2D copy engine
+            self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
+        self.stores = stores or HostStores(cfg.layers, capacity, batch, h)
+        z = lambda *s, dt=F16: torch.empty(*s, dtype=dt, device=self.dev)  # noqa: E731
+        self.kv_dev = z(nbuf, capacity, 2, b, h)
+        self.x_dev = z(nbuf, capacity, b, h)
+        self.hres = z(b, h, dt=F32)
+        self.q = z(b, h)
+        self.attn = z(b, h)
+        self.y = z(b, h)
+        self.mid = z(b, cfg.ffn)
+        self.zf = z(b, h)
+        self.logits = z(b, cfg.vocab, dt=F32)
+        self.tok = z(b, dt=torch.int32)
+        self.ws = z(16 << 20, dt=torch.uint8)
+        self.len = 0
+        R = cfg.layers + nbuf + 2
+        self._R = R
+        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        self.ev_x = [[ev() for _ in range(chunks)] for _ in range(R)]
+        self.ev_kv = [ev() for _ in range(R)]
+        self.ev_qkv = [ev() for _ in range(R)]
+        self.ev_d2h = [ev() for _ in range(R)]
+        self.ev_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
+        self.launches = 0  # kernels issued (for bench's gpu_launches)
+
+    # ------------------------------------------------------------------ utils
+    def _k(self, n: int = 1) -> None:
+        self.launches += n
+
+    def reset(self, length: int) -> None:
+        """Rewind the logical cache length (positions >= length are overwritten by later steps)."""
+        torch.cuda.synchronize(self.dev)
+        self.len = length
+
+    # ---------------------------------------------------------------- prefill
+    def prefill(self, prompt: torch.Tensor) -> torch.Tensor:
+        """Run the prompt [batch, S0] through all layers on the GPU, filling the host stores.
+
+        Returns the first greedy token per sequence (device int32 [batch]).
+        Not on the timed decode path; uses the same kernels as decode.
+        """
+        cfg, b, h = self.cfg, self.batch, self.cfg.hidden
+        S0 = int(prompt.shape[1])
+        if prompt.shape[0] != b or S0 <= 0 or S0 >= self.capacity:
+            raise ValueError(f"prompt must be [batch={b}, 1 <= S0 < capacity={self.capacity}]")
+        rows = S0 * b
+        cs = self.cs
+        with torch.cuda.stream(cs):
+            toks = prompt.to(self.dev, non_blocking=True).to(torch.int32).t().contiguous()  # [S0, b] pos-major
+            hbuf = torch.empty(rows, h, dtype=F32, device=self.dev)
+            x = torch.empty(rows, h, dtype=F16, device=self.dev)
+            q = torch.empty(rows, h, dtype=F16, device=self.dev)
+            a = torch.empty(rows, h, dtype=F16, device=self.dev)
+            mid = torch.empty(rows, cfg.ffn, dtype=F16, device=self.dev)
+            pages = self.kv_dev[0]
+            kernels.embed(toks.view(-1), self.w.embed, self.w.pos, hbuf, batch=b, pos_begin=0, stream=cs)
+            for j, lw in enumerate(self.w.layers):
+                kernels.layernorm(hbuf, lw.ln1_g, lw.ln1_b, x, eps=cfg.eps, stream=cs)
+                self._qkv(x, rows, lw, q, pages[:S0], q_group=b * h, stream=cs)
+                _copy(self.stores.x[j].data_ptr(), x.data_ptr(), rows * h * 2, cs)
+                _copy(self.stores.kv[j].data_ptr(), pages.data_ptr(), S0 * 2 * b * h * 2, cs)
+                kernels.prefill_attention(q, pages, a, b, cfg.heads, cfg.head_dim, S0, stream=cs)
+                self._mlp(a, rows, lw, hbuf, x, mid, stream=cs)
+            last = hbuf[(S0 - 1) * b:]
+            self._head(last, stream=cs)
+        cs.synchronize()
+        self.len = S0
+        return self.tok.clone()
+
+    # ------------------------------------------------------------ layer pieces
+    def _qkv(self, x: torch.Tensor, M: int, lw, q_out: torch.Tensor, pages: torch.Tensor, q_group: int, stream):
+        """q -> q_out ([M, h] row-major), k/v -> pages (position-major, row m = (pos m // b, seq m % b))."""
+        b, h = self.batch, self.cfg.hidden
+        bh = b * h
+        kp = pages.data_ptr()
+        epi = _lib.make_epilogue(
+            [(q_out.data_ptr(), q_group), (kp, 2 * bh), (kp + bh * 2, 2 * bh)],
+            seg_width=h, ld=h, row_group=b, bias=lw.bqkv.data_ptr(),
+        )
+        kernels.linear(x, lw.wqkv, epi, M=M, stream=stream)
+        self._k()
+
+    def _mlp(self, attn: torch.Tensor, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
+        """h += attn W_o^T + b_o;  h += relu(LN2(h) W_1^T + b_1) W_2^T + b_2  (OPT pre-LN block)."""
+        cfg = self.cfg
+        acc = _lib.EPI_F32 | _lib.EPI_ACCUM
+        kernels.linear_simple(attn[:M], lw.wo, lw.bo, hres[:M], flags=acc, stream=stream)
+        kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, ybuf, rows=M, eps=cfg.eps, stream=stream)
+        kernels.linear_simple(ybuf[:M], lw.w1, lw.b1, mid[:M], flags=_lib.EPI_RELU, stream=stream)
+        kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream)
+        self._k(4)
+
+    def _head(self, hrows: torch.Tensor, stream) -> None:
+        """Final LN, tied LM head (fp32 logits) and greedy argmax into self.tok."""
+        cfg = self.cfg
+        kernels.layernorm(hrows, self.w.lnf_g, self.w.lnf_b, self.zf, eps=cfg.eps, stream=stream)
+        kernels.linear_simple(self.zf, self.w.embed, None, self.logits, stream=stream)
+        kernels.argmax(self.logits, self.tok, stream=stream)
+        self._k(3)
+
+    # ------------------------------------------------------------------ decode
+    def _unit(self, u: int, base_len: int, splits: list[int]):
+        L = self.cfg.layers
+        i, j = divmod(u, L)
+        s = base_len + i + 1
+        lp = min(splits[i], s - 1)
+        return i, j, s, lp, u % self.nbuf, u % self._R
+
+    def _issue_h2d(self, u: int, base_len: int, splits: list[int]) -> None:
+        """load_activation_recompute then load_cache for unit u (graph.py:266-293), on the copy stream."""
+        L, b, h = self.cfg.layers, self.batch, self.cfg.hidden
+        i, j, s, lp, buf, r = self._unit(u, base_len, splits)
+        hs = self.hs
+        if u >= self.nbuf:  # device buffer free: its previous user finished computing and storing
+            rp = (u - self.nbuf) % self._R
+            hs.wait_event(self.ev_done[rp])
+            hs.wait_event(self.ev_d2h[rp])
+        if u >= L:  # host store of the previous step's new position has landed (graph.py:286-287)
+            hs.wait_event(self.ev_d2h[(u - L) % self._R])
+        xh, kvh = self.stores.x[j], self.stores.kv[j]
+        xd, kvd = self.x_dev[buf], self.kv_dev[buf]
+        row = b * h * 2
+        for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
+            _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
+            self.ev_x[r][c].record(hs)
+        _copy(kvd[lp].data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * 2 * row, hs)
+        self.ev_kv[r].record(hs)
+
+    def _compute_layer(self, u: int, base_len: int, splits: list[int]) -> None:
+        cfg, b, h = self.cfg, self.batch, self.cfg.hidden
+        i, j, s, lp, buf, r = self._unit(u, base_len, splits)
+        lw = self.w.layers[j]
+        cs, ds = self.cs, self.ds
+        xd, kvd = self.x_dev[buf], self.kv_dev[buf]
+        x_slot, page = xd[s - 1], kvd[s - 1]
+        # new token: X = LN1(h) straight into the X slot of position s'-1, q/k/v with k,v into page s'-1
+        kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
+        self._k()
+        self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
+        self.ev_qkv[r].record(cs)
+        # store_activation / store_cache (graph.py:340-347) on the D2H engine
+        ds.wait_event(self.ev_qkv[r])
+        _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
+        _copy(self.stores.kv[j][s - 1].data_ptr(), page.data_ptr(), 2 * b * h * 2, ds)
+        self.ev_d2h[r].record(ds)
+        # K1: rebuild K,V[0:l) chunk by chunk as X lands
+        for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
+            cs.wait_event(self.ev_x[r][c])
+            kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, p0, p1, stream=cs)
+            self._k()
+        cs.wait_event(self.ev_kv[r])
+        # K2 over the merged pages [0, s') in place
+        kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
+        self._k(2)
+        self._mlp(self.attn, b, lw, self.hres, self.y, self.mid, stream=cs)
+        self.ev_done[r].record(cs)
+
+    def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
+               timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None) -> torch.Tensor:
+        """Enqueue len(splits) decode steps (no host sync); returns device int32 [steps, batch] tokens.
+
+        Step i attends over s' = len + i + 1 positions, rebuilding [0, min(l_i, s'-1)) with K1.
+        """
+        cfg, b, L = self.cfg, self.batch, self.cfg.layers
+        steps = len(splits)
+        base = self.len
+        if base + steps > self.capacity:
+            raise ValueError(f"cache capacity {self.capacity} exceeded ({base} + {steps} steps)")
+        for i, l in enumerate(splits):
+            if not 0 <= l <= base + i + 1:
+                raise ValueError(f"step {i + 1}: split {l} out of range [0, {base + i + 1}]")
+        cs = self.cs
+        if tokens is not None:
+            with torch.cuda.stream(cs):
+                self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
+        if out_tokens is None:
+            out_tokens = torch.empty(steps, b, dtype=torch.int32, device=self.dev)
+        logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
+        cs.wait_stream(torch.cuda.current_stream(self.dev))
+        self.hs.wait_stream(torch.cuda.current_stream(self.dev))
+        n_units = steps * L
+        t_start = torch.cuda.Event(enable_timing=True) if timing is not None else None
+        step_marks, layer_marks = [], []
+        if t_start is not None:
+            t_start.record(cs)
+        self._issue_h2d(0, base, splits)
+        for u in range(n_units):
+            if u + 1 < n_units:
+                self._issue_h2d(u + 1, base, splits)
+            i, j = divmod(u, L)
+            if j == 0:
+                kernels.embed(self.tok, self.w.embed, self.w.pos, self.hres, batch=b, pos_begin=base + i, stream=cs)
+                self._k()
+            self._compute_layer(u, base, splits)
+            if timing is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(cs)
+                layer_marks.append(e)
+            if j == L - 1:
+                self._head(self.hres, stream=cs)
+                with torch.cuda.stream(cs):
+                    out_tokens[i].copy_(self.tok, non_blocking=True)
+                    if logits is not None:
+                        logits[i].copy_(self.logits, non_blocking=True)
+                if timing is not None:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(cs)
+                    step_marks.append(e)
+        self.len = base + steps
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_stream(cs)
+        cur.wait_stream(self.ds)
+        if timing is not None:
+            cs.synchronize()
+            prev = t_start
+            for e in step_marks:
+                timing.step_ms.append(prev.elapsed_time(e))
+                prev = e
+            prev = t_start
+            for i in range(steps):
+                row = []
+                for e in layer_marks[i * L:(i + 1) * L]:
+                    row.append(prev.elapsed_time(e))
+                    prev = e
+                timing.layer_ms.append(row)
+                prev = step_marks[i]
+        self._last_logits = logits
+        return out_tokens
+
+    @property
+    def last_logits(self) -> torch.Tensor | None:
+        return getattr(self, "_last_logits", None)
+
+    def close(self) -> None:
+        self.stores.close()
+
+
+def generate(weights: OPTWeights, prompt: torch.Tensor, splits: list[int], runtime: KVPRRuntime | None = None,
+             keep_logits: bool = False):
+    """End-to-end public call: host prompt ids in, host generated ids out.
+
+    Returns (tokens int64 [steps + 1, batch] on the host — the prefill token then
+    one per decode step — and the runtime).
+    """
+    b, S0 = prompt.shape
+    rt = runtime or KVPRRuntime(weights, b, S0 + len(splits) + 1)
+    first = rt.prefill(prompt)
+    toks = rt.decode(splits, tokens=first, keep_logits=keep_logits)
+    host = torch.empty(len(splits) + 1, b, dtype=torch.int32, pin_memory=True)
+    with torch.cuda.stream(rt.cs):
+        host[0].copy_(first, non_blocking=True)
+        host[1:].copy_(toks, non_blocking=True)
+    rt.cs.synchronize()
+    return host.to(torch.int64), rt
