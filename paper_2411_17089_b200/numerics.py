@@ -1,0 +1,140 @@
+"""GPU drop-in for ``kvoverlap.numerics``' split/merge attention
+(/root/reference/pkg/src/kvoverlap/numerics.py), same names and arguments.
+
+``split_merge_kv`` rebuilds positions [0, split) with the K1 tcgen05 GEMM and
+``decode_attention`` runs K2 + the W_O projection, so the reference's own
+test style (pkg/tests/test_numerics.py) can be pointed at the B200 path.
+Differences, by design of the target: arithmetic is fp16 storage / fp32
+accumulation (the reference is fp64), so agreement is within the north-star
+tolerance (2e-2 relative), not 1e-12; arrays come back as float64 NumPy to
+keep the reference's types.  Validation (ValueError conditions and messages)
+follows numerics.py:22-32, 121-126, 172-182.  The reference matrices are
+[in, out] (``x @ w_k``); the kernels take the torch [out, in] layout, so
+weights are transposed on upload.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+
+
+def _mat(name, m, rows=None, cols=None):
+    a = np.asarray(m, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {a.shape}")
+    if rows is not None and a.shape[0] != rows:
+        raise ValueError(f"{name} must have {rows} rows, got {a.shape[0]}")
+    if cols is not None and a.shape[1] != cols:
+        raise ValueError(f"{name} must have {cols} cols, got {a.shape[1]}")
+    if not np.isfinite(a).all():
+        raise ValueError(f"{name} contains non-finite entries")
+    return a
+
+
+@dataclass(frozen=True)
+class KVState:
+    """(num_heads, seq_len, d_head) keys/values (numerics.py:43-72)."""
+
+    keys: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        k = np.asarray(self.keys, dtype=np.float64)
+        v = np.asarray(self.values, dtype=np.float64)
+        if k.ndim != 3 or v.ndim != 3:
+            raise ValueError("keys/values must be (num_heads, seq_len, d_head)")
+        if k.shape != v.shape:
+            raise ValueError(f"key shape {k.shape} != value shape {v.shape}")
+        if not (np.isfinite(k).all() and np.isfinite(v).all()):
+            raise ValueError("KV entries must be finite")
+        object.__setattr__(self, "keys", k)
+        object.__setattr__(self, "values", v)
+
+    @property
+    def num_heads(self):
+        return self.keys.shape[0]
+
+    @property
+    def seq_len(self):
+        return self.keys.shape[1]
+
+    @property
+    def head_dim(self):
+        return self.keys.shape[2]
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2411_17089_b200.numerics runs on the GPU only (no CPU fallback)")
+    _lib.load()
+    return torch.device("cuda")
+
+
+def _pad_to(n: int, m: int) -> int:
+    return (n + m - 1) // m * m
+
+
+def split_merge_kv(x_full, split: int, w_k, w_v, kv_suffix: KVState) -> KVState:
+    """K1 rebuild of [0, split) concatenated with the transferred suffix (numerics.py:107-137)."""
+    x_full = _mat("x_full", x_full)
+    seq, h = x_full.shape
+    if not 0 <= split <= seq:
+        raise ValueError(f"split must be in [0, {seq}], got {split}")
+    if kv_suffix.seq_len != seq - split:
+        raise ValueError(f"suffix covers {kv_suffix.seq_len} positions, expected {seq - split}")
+    if split == 0:
+        return kv_suffix
+    w_k = _mat("w_k", w_k, h, h)
+    w_v = _mat("w_v", w_v, h, h)
+    heads = kv_suffix.num_heads
+    dev = _dev()
+    hp = _pad_to(h, 64)  # GEMM needs K % 8 and N % 32; pad the hidden dim with zeros
+    x = torch.zeros(split, 1, hp, dtype=torch.float16, device=dev)
+    x[:, 0, :h] = torch.from_numpy(x_full[:split]).to(dev, torch.float16)
+    w = torch.zeros(2 * hp, hp, dtype=torch.float16, device=dev)
+    w[:h, :h] = torch.from_numpy(w_k.T.copy()).to(dev, torch.float16)
+    w[hp:hp + h, :h] = torch.from_numpy(w_v.T.copy()).to(dev, torch.float16)
+    pages = torch.empty(split, 2, 1, hp, dtype=torch.float16, device=dev)
+    kernels.recompute_kv(x, w, None, pages, 1, 0, split)
+    kv = pages[:, :, 0, :h].double().cpu().numpy()  # [split, 2, h]
+    d = h // heads
+    kp = kv[:, 0].reshape(split, heads, d).transpose(1, 0, 2)
+    vp = kv[:, 1].reshape(split, heads, d).transpose(1, 0, 2)
+    return KVState(np.concatenate([kp, kv_suffix.keys], axis=1), np.concatenate([vp, kv_suffix.values], axis=1))
+
+
+def decode_attention(q_token, kv: KVState, w_o) -> np.ndarray:
+    """K2 split-KV attention over the cache, then W_O (numerics.py:166-191)."""
+    if kv.seq_len == 0:
+        raise ValueError("cannot attend over an empty cache")
+    q = np.asarray(q_token, dtype=np.float64)
+    if q.ndim != 1:
+        raise ValueError("q_token must be a 1-D row of length h")
+    h = kv.num_heads * kv.head_dim
+    if q.shape[0] != h:
+        raise ValueError(f"q_token has length {q.shape[0]}, expected {h}")
+    if not np.isfinite(q).all():
+        raise ValueError("q_token contains non-finite entries")
+    w_o = _mat("w_o", w_o, h, h)
+    d = kv.head_dim
+    if d not in (64, 128):
+        raise ValueError(f"head_dim {d} unsupported by the decode-attention kernel (64 or 128)")
+    dev = _dev()
+    s = kv.seq_len
+    pages = torch.empty(s, 2, 1, h, dtype=torch.float16, device=dev)
+    pages[:, 0, 0] = torch.from_numpy(kv.keys.transpose(1, 0, 2).reshape(s, h)).to(dev, torch.float16)
+    pages[:, 1, 0] = torch.from_numpy(kv.values.transpose(1, 0, 2).reshape(s, h)).to(dev, torch.float16)
+    qd = torch.from_numpy(q).to(dev, torch.float16).view(1, h)
+    att = torch.empty(1, h, dtype=torch.float16, device=dev)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+    kernels.decode_attention(qd, pages, att, ws, 1, kv.num_heads, d, s, scale=1.0 / math.sqrt(d))
+    wo = torch.from_numpy(w_o.T.copy()).to(dev, torch.float16)  # [out, in]
+    out = torch.empty(1, h, dtype=torch.float32, device=dev)
+    kernels.linear_simple(att, wo, None, out)
+    return out[0].double().cpu().numpy()

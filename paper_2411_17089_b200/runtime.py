@@ -136,6 +136,7 @@ class KVPRRuntime:
         self.ev_d2h = [ev() for _ in range(R)]
         self.ev_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
         self.launches = 0  # kernels issued (for bench's gpu_launches)
+        self._trace = None
 
     # ------------------------------------------------------------------ utils
     def _k(self, n: int = 1) -> None:
@@ -196,13 +197,18 @@ class KVPRRuntime:
 
     def _mlp(self, attn: torch.Tensor, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
         """h += attn W_o^T + b_o;  h += relu(LN2(h) W_1^T + b_1) W_2^T + b_2  (OPT pre-LN block)."""
-        cfg = self.cfg
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.linear_simple(attn[:M], lw.wo, lw.bo, hres[:M], flags=acc, stream=stream)
+        self._k()
+        self._ffn(M, lw, hres, ybuf, mid, stream)
+
+    def _ffn(self, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
+        cfg = self.cfg
+        acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, ybuf, rows=M, eps=cfg.eps, stream=stream)
         kernels.linear_simple(ybuf[:M], lw.w1, lw.b1, mid[:M], flags=_lib.EPI_RELU, stream=stream)
         kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream)
-        self._k(4)
+        self._k(3)
 
     def _head(self, hrows: torch.Tensor, stream) -> None:
         """Final LN, tied LM head (fp32 logits) and greedy argmax into self.tok."""
@@ -234,10 +240,18 @@ class KVPRRuntime:
         xh, kvh = self.stores.x[j], self.stores.kv[j]
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         row = b * h * 2
+        tr = self._trace
         for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
+            sp = tr.begin(hs, "load_activation_recompute", i + 1, j + 1, f"c{c}") if tr else None
             _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
+            if sp:
+                tr.end(hs, sp)
             self.ev_x[r][c].record(hs)
-        _copy(kvd[lp].data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * 2 * row, hs)
+        if s - 1 > lp:
+            sp = tr.begin(hs, "load_cache", i + 1, j + 1) if tr else None
+            _copy(kvd[lp].data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * 2 * row, hs)
+            if sp:
+                tr.end(hs, sp)
         self.ev_kv[r].record(hs)
 
     def _compute_layer(self, u: int, base_len: int, splits: list[int]) -> None:
@@ -247,30 +261,54 @@ class KVPRRuntime:
         cs, ds = self.cs, self.ds
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         x_slot, page = xd[s - 1], kvd[s - 1]
+        tr = self._trace
+        I, J = i + 1, j + 1
         # new token: X = LN1(h) straight into the X slot of position s'-1, q/k/v with k,v into page s'-1
+        sp = tr.begin(cs, "compute_mha", I, J, "proj") if tr else None
         kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
         self._k()
         self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
+        if sp:
+            tr.end(cs, sp)
         self.ev_qkv[r].record(cs)
         # store_activation / store_cache (graph.py:340-347) on the D2H engine
         ds.wait_event(self.ev_qkv[r])
+        sp = tr.begin(ds, "store_activation", I, J) if tr else None
         _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
+        if sp:
+            tr.end(ds, sp)
+        sp = tr.begin(ds, "store_cache", I, J) if tr else None
         _copy(self.stores.kv[j][s - 1].data_ptr(), page.data_ptr(), 2 * b * h * 2, ds)
+        if sp:
+            tr.end(ds, sp)
         self.ev_d2h[r].record(ds)
         # K1: rebuild K,V[0:l) chunk by chunk as X lands
         for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
             cs.wait_event(self.ev_x[r][c])
+            sp = tr.begin(cs, "compute_recompute", I, J, f"c{c}") if tr else None
             kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, p0, p1, stream=cs)
+            if sp:
+                tr.end(cs, sp)
             self._k()
         cs.wait_event(self.ev_kv[r])
-        # K2 over the merged pages [0, s') in place
+        # K2 over the merged pages [0, s') in place, then W_O + residual
+        sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
         self._k(2)
-        self._mlp(self.attn, b, lw, self.hres, self.y, self.mid, stream=cs)
+        acc = _lib.EPI_F32 | _lib.EPI_ACCUM
+        kernels.linear_simple(self.attn, lw.wo, lw.bo, self.hres, flags=acc, stream=cs)
+        self._k()
+        if sp:
+            tr.end(cs, sp)
+        sp = tr.begin(cs, "compute_ffn", I, J) if tr else None
+        self._ffn(b, lw, self.hres, self.y, self.mid, stream=cs)
+        if sp:
+            tr.end(cs, sp)
         self.ev_done[r].record(cs)
 
     def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
-               timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None) -> torch.Tensor:
+               timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None,
+               trace=None) -> torch.Tensor:
         """Enqueue len(splits) decode steps (no host sync); returns device int32 [steps, batch] tokens.
 
         Step i attends over s' = len + i + 1 positions, rebuilding [0, min(l_i, s'-1)) with K1.
@@ -284,6 +322,7 @@ class KVPRRuntime:
             if not 0 <= l <= base + i + 1:
                 raise ValueError(f"step {i + 1}: split {l} out of range [0, {base + i + 1}]")
         cs = self.cs
+        self._trace = trace
         if tokens is not None:
             with torch.cuda.stream(cs):
                 self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
@@ -321,6 +360,7 @@ class KVPRRuntime:
                     e.record(cs)
                     step_marks.append(e)
         self.len = base + steps
+        self._trace = None
         cur = torch.cuda.current_stream(self.dev)
         cur.wait_stream(cs)
         cur.wait_stream(self.ds)

@@ -1,0 +1,97 @@
+"""The C-ABI boundary without a GPU: libkvpr.so loads, exports every symbol
+include/kvpr.h declares, the ctypes struct layout equals the C layout, the
+SASS is Blackwell-native, and the product path has no CPU fallback."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2411_17089_b200 import _lib
+
+from .conftest import ROOT
+
+HEADER = ROOT / "include" / "kvpr.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(kvpr_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert names, "no declarations parsed from include/kvpr.h"
+    for n in names:
+        assert hasattr(lib, n), f"libkvpr.so does not export {n}"
+    assert set(names) == set(_lib.EXPORTS), "ctypes binding and header disagree"
+
+
+def test_version_and_error_string(lib):
+    assert lib.kvpr_version() == 1
+    assert isinstance(_lib.last_error(), str)
+
+
+def test_ctypes_struct_layout_matches_c(tmp_path):
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "kvpr.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(kvpr_epilogue),"
+        " offsetof(kvpr_epilogue, seg_width), offsetof(kvpr_epilogue, ld), offsetof(kvpr_epilogue, seg),"
+        " offsetof(kvpr_epilogue, scale), offsetof(kvpr_epilogue, scale_cols), offsetof(kvpr_epilogue, flags),"
+        " sizeof(kvpr_out_seg)); return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run([gcc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    E = _lib.Epilogue
+    want = [ctypes.sizeof(E), E.seg_width.offset, E.ld.offset, E.seg.offset, E.scale.offset, E.scale_cols.offset,
+            E.flags.offset, ctypes.sizeof(_lib.OutSeg)]
+    assert got == want
+
+
+def test_sass_is_tcgen05_tma(lib):
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    try:
+        out = subprocess.run([cuobjdump, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                             timeout=120).stdout
+    except (FileNotFoundError, subprocess.TimeoutExpired):
+        pytest.skip("cuobjdump unavailable")
+    assert "UTCHMMA" in out, "no tcgen05.mma in SASS"
+    assert "UTMALDG" in out, "no TMA loads in SASS"
+    assert "LDTM" in out, "no tcgen05.ld in SASS"
+    assert "HMMA" not in out.replace("UTCHMMA", ""), "legacy mma.sync path present"
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    saved = _lib._lib
+    _lib._lib = None
+    try:
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            _lib.load(tmp_path / "nope.so")
+    finally:
+        _lib._lib = saved
+
+
+def test_product_path_rejects_cpu_tensors():
+    import torch
+
+    from paper_2411_17089_b200 import kernels
+
+    x = torch.zeros(4, 2, 64, dtype=torch.float16)
+    w = torch.zeros(128, 64, dtype=torch.float16)
+    with pytest.raises(ValueError, match="CUDA"):
+        kernels.recompute_kv(x, w, None, torch.zeros(4, 2, 2, 64, dtype=torch.float16), 2, 0, 2)
+
+
+def test_product_never_imports_oracle():
+    pkg = ROOT / "paper_2411_17089_b200"
+    for p in pkg.rglob("*.py"):
+        text = p.read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle", text, flags=re.M), f"{p} imports the oracle"

@@ -1,0 +1,70 @@
+"""The reference's numeric contract (pkg/tests/test_numerics.py) run against the
+GPU drop-in paper_2411_17089_b200.numerics, checked against the fp64 oracle
+restatement (oracle/numerics_ref.py, itself pinned to the live reference).
+
+Tolerance: fp16 storage / fp32 accumulation vs fp64 —
+|gpu - oracle| <= 2e-2 * max|oracle| (the north-star relative bound).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import numerics_ref as nr
+from paper_2411_17089_b200 import numerics as gn
+
+pytestmark = pytest.mark.gpu
+RTOL = 2e-2
+
+
+def _case(seed, heads=4, d=64, seq=70):
+    rng = np.random.default_rng(seed)
+    h = heads * d
+    s = 1.0 / np.sqrt(h)
+    return (rng.standard_normal((seq, h)), rng.standard_normal((h, h)) * s, rng.standard_normal((h, h)) * s,
+            rng.standard_normal((h, h)) * s, rng.standard_normal(h))
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.mark.parametrize("heads,d,seq", [(4, 64, 70), (2, 128, 33), (1, 64, 1)])
+def test_split_merge_matches_full_cache(heads, d, seq):
+    x, w_k, w_v, w_o, q = _case(3, heads, d, seq)
+    full = nr.build_kv(x, w_k, w_v, heads)
+    ref = nr.decode_attention(q, full, w_o)
+    for split in sorted({0, 1, seq // 3, seq // 2, seq - 1, seq}):
+        if split > seq:
+            continue
+        suffix = gn.KVState(full.keys[:, split:], full.values[:, split:])
+        merged = gn.split_merge_kv(x, split, w_k, w_v, suffix)
+        assert merged.keys.shape == full.keys.shape
+        assert _rel(merged.keys, full.keys) <= RTOL and _rel(merged.values, full.values) <= RTOL
+        out = gn.decode_attention(q, merged, w_o)
+        assert _rel(out, ref) <= RTOL, (split, _rel(out, ref))
+
+
+def test_split_zero_passes_suffix_through():
+    x, w_k, w_v, _, _ = _case(4)
+    full = gn.KVState(*[a for a in (nr.build_kv(x, w_k, w_v, 4).keys, nr.build_kv(x, w_k, w_v, 4).values)])
+    assert gn.split_merge_kv(x, 0, w_k, w_v, full) is full
+
+
+def test_validation_matches_reference():
+    x, w_k, w_v, w_o, q = _case(6)
+    full = gn.KVState(nr.build_kv(x, w_k, w_v, 4).keys, nr.build_kv(x, w_k, w_v, 4).values)
+    with pytest.raises(ValueError, match="suffix"):
+        gn.split_merge_kv(x, 2, w_k, w_v, full)
+    with pytest.raises(ValueError, match="split"):
+        gn.split_merge_kv(x, 71, w_k, w_v, full)
+    empty = gn.KVState(full.keys[:, :0], full.values[:, :0])
+    with pytest.raises(ValueError, match="empty"):
+        gn.decode_attention(q, empty, w_o)
+    with pytest.raises(ValueError, match="length"):
+        gn.decode_attention(q[:-1], full, w_o)
+    bad = w_k.copy()
+    bad[0, 0] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        gn.split_merge_kv(x, 3, bad, w_v, gn.KVState(full.keys[:, 3:], full.values[:, 3:]))

@@ -1,0 +1,96 @@
+"""Host-side runtime logic without a GPU: X chunking, plan plumbing, and the
+batch-partitioned multi-process path over gloo (world_size 2)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_17089_b200 import multigpu
+from paper_2411_17089_b200.costmodel import WorkloadSpec, opt_preset
+from paper_2411_17089_b200.hwprofile import HardwareProfile
+from paper_2411_17089_b200.runtime import chunk_bounds
+from paper_2411_17089_b200.scheduler import solve_split
+
+
+@pytest.mark.parametrize("n,chunks", [(0, 4), (1, 4), (63, 4), (64, 4), (882, 4), (1000, 3), (257, 8)])
+def test_chunk_bounds_partition(n, chunks):
+    b = chunk_bounds(n, chunks)
+    if n == 0:
+        assert b == []
+        return
+    assert b[0][0] == 0 and b[-1][1] == n
+    assert all(p1 > p0 for p0, p1 in b)
+    assert all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+    assert len(b) <= chunks
+    sizes = [p1 - p0 for p0, p1 in b]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_partition_slices():
+    s = multigpu.partition(32, 8)
+    assert [x.count for x in s] == [4] * 8 and s[-1].start == 28
+    s = multigpu.partition(10, 4)
+    assert [x.count for x in s] == [3, 3, 2, 2] and [x.start for x in s] == [0, 3, 6, 8]
+    with pytest.raises(ValueError):
+        multigpu.partition(3, 4)
+
+
+def test_rank_plan_is_reference_solver_on_the_slice():
+    spec = opt_preset("opt-13b")
+    wl = WorkloadSpec(batch_size=32, prompt_len=1024, gen_len=4)
+    prof = HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=55e9, transfer_latency=1e-5)
+    for world in (1, 2, 4, 8):
+        for r in range(world):
+            plan = multigpu.rank_plan(spec, wl, prof, world, r)
+            b = multigpu.partition(32, world)[r].count
+            wl_r = WorkloadSpec(batch_size=b, prompt_len=1024, gen_len=4)
+            assert plan.decisions[0] == solve_split(spec, wl_r, prof, 1025, "column", step=1)
+    # OPT-13B b4 (G=8 shard) with 10 us latency -> l = 858
+    assert multigpu.rank_plan(spec, wl, prof, 8, 0).decisions[0].recompute_len == 858
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, global_batch, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sl = multigpu.partition(global_batch, world)[rank]
+        steps = 3
+        # stand-in for this rank's replica output: token = 1000*step + global sequence id
+        local = torch.tensor([[1000 * i + sl.start + k for k in range(sl.count)] for i in range(steps)])
+        full = multigpu.gather_tokens(local, global_batch)
+        t = multigpu.max_over_ranks(float(rank + 1))
+        q.put((rank, full.tolist(), t))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("global_batch", [8, 7])
+def test_partitioned_gather_over_gloo(global_batch):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, global_batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [[1000 * i + k for k in range(global_batch)] for i in range(3)]
+    for rank, full, t in res:
+        assert full == want
+        assert t == float(world)
