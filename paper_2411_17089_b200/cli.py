@@ -1,0 +1,320 @@
+"""Operator front end (§8f rank 4), mirroring ``kvoverlap``'s CLI contract
+(/root/reference/pkg/src/kvoverlap/cli.py): one JSON config with
+model / workload / hardware / policy sections (unknown keys rejected,
+cli.py:73-164), plan JSON on stdout or --out, exit codes 0 ok, 1 invalid
+input, 2 GPU memory budget exceeded, 3 validation failure (cli.py:45-48).
+
+    python -m paper_2411_17089_b200 plan      --config cfg.json [--l N] [--out plan.json]
+    python -m paper_2411_17089_b200 calibrate --measurements m.csv
+    python -m paper_2411_17089_b200 profile   [--hidden 4096 --batch 32] [--out m.csv]   (GPU)
+    python -m paper_2411_17089_b200 run       --config cfg.json [--plan plan.json] [--trace t.json] (GPU)
+    python -m paper_2411_17089_b200 validate  [--cases N] [--seed S]                       (GPU)
+
+`plan` / `calibrate` print byte-identical documents to the reference's for
+the same config.  `run` executes the plan on the B200 (random-init weights,
+synthetic prompt) instead of simulating it and prints the reference's
+`key=value` report style with measured numbers.  An optional "runtime"
+section adds {"seed", "weights_std", "chunks", "device"}.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import logging
+import os
+import sys
+from dataclasses import dataclass
+
+from .costmodel import ModelSpec, WorkloadSpec, opt_preset
+from .hwprofile import HardwareProfile, calibrate, profile_to_json, read_measurements_csv
+from .scheduler import SplitPlan, constant_plan, import_plan, plan_generation, plan_to_json
+
+log = logging.getLogger("paper_2411_17089_b200")
+
+EXIT_OK, EXIT_INVALID, EXIT_BUDGET, EXIT_VALIDATION = 0, 1, 2, 3
+
+
+class ConfigError(ValueError):
+    """Configuration file or flag value is invalid."""
+
+
+class GpuMemoryBudgetError(RuntimeError):
+    """Device residency of the run exceeds the configured budget."""
+
+
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):  # argparse would exit 2, which the contract reserves
+        raise ConfigError(message)
+
+
+@dataclass(frozen=True)
+class Setup:
+    spec: ModelSpec
+    wl: WorkloadSpec
+    profile: HardwareProfile
+    schedule: str
+    recompute: bool
+    budget: float | None
+    runtime: dict
+
+
+def _only(section: str, given: dict, allowed) -> None:
+    extra = sorted(set(given) - set(allowed))
+    if extra:
+        raise ConfigError(f"unknown {section} keys: {', '.join(extra)}")
+
+
+def _sec(doc, name, required):
+    if name not in doc:
+        if required:
+            raise ConfigError(f"config missing required section {name!r}")
+        return {}
+    if not isinstance(doc[name], dict):
+        raise ConfigError(f"config section {name!r} must be an object")
+    return doc[name]
+
+
+def load_config(path: str) -> Setup:
+    try:
+        with open(path) as fh:
+            doc = json.load(fh)
+    except json.JSONDecodeError as exc:
+        raise ConfigError(f"{path}: not valid JSON ({exc})") from exc
+    if not isinstance(doc, dict):
+        raise ConfigError(f"{path}: config must be a JSON object")
+    _only("config", doc, ("model", "workload", "hardware", "policy", "runtime"))
+    try:
+        m = _sec(doc, "model", True)
+        fields = ("hidden_dim", "num_layers", "num_heads", "ffn_dim", "precision_bytes")
+        _only("model", m, fields + ("preset",))
+        if "preset" in m:
+            base = opt_preset(m["preset"])
+            spec = ModelSpec(**{**{f: getattr(base, f) for f in fields}, **{k: v for k, v in m.items() if k != "preset"}})
+        else:
+            missing = [f for f in fields[:-1] if f not in m]
+            if missing:
+                raise ConfigError(f"model section missing: {', '.join(missing)}")
+            spec = ModelSpec(**m)
+        w = _sec(doc, "workload", True)
+        _only("workload", w, ("batch_size", "num_batches", "prompt_len", "gen_len", "kv_bytes_per_element"))
+        wl = WorkloadSpec(**w)
+        hw = _sec(doc, "hardware", True)
+        _only("hardware", hw, ("gpu_flops", "h2d_bw", "d2h_bw", "transfer_latency_s", "gpu_efficiency",
+                               "gpu_mem_budget_bytes"))
+        for k in ("gpu_flops", "h2d_bw", "d2h_bw"):
+            if k not in hw:
+                raise ConfigError(f"hardware section missing {k!r}")
+        prof = HardwareProfile(gpu_flops=hw["gpu_flops"], h2d_bandwidth=hw["h2d_bw"], d2h_bandwidth=hw["d2h_bw"],
+                               transfer_latency=hw.get("transfer_latency_s", 0.0),
+                               gpu_efficiency=hw.get("gpu_efficiency", 1.0))
+        pol = _sec(doc, "policy", False)
+        _only("policy", pol, ("schedule", "recompute", "granularity", "weights_resident"))
+        rec = pol.get("recompute", "on")
+        if isinstance(rec, str):
+            if rec not in ("on", "off"):
+                raise ConfigError("policy.recompute must be 'on' or 'off'")
+            rec = rec == "on"
+        if pol.get("granularity", "coarse") not in ("coarse", "fine"):
+            raise ConfigError("policy.granularity must be 'coarse' or 'fine'")
+        if not pol.get("weights_resident", True):
+            raise ConfigError("policy.weights_resident=false (streamed weights) is not implemented on the B200 path")
+        schedule = pol.get("schedule", "row")
+        if schedule not in ("row", "column"):
+            raise ConfigError("policy.schedule must be 'row' or 'column'")
+        rt = _sec(doc, "runtime", False)
+        _only("runtime", rt, ("seed", "weights_std", "chunks", "device"))
+    except ConfigError:
+        raise
+    except (ValueError, TypeError) as exc:
+        raise ConfigError(str(exc)) from exc
+    return Setup(spec, wl, prof, schedule, bool(rec), hw.get("gpu_mem_budget_bytes"), rt)
+
+
+def _plan(s: Setup, l_override: int | None) -> SplitPlan:
+    if l_override is not None:
+        if l_override < 0:
+            raise ConfigError("--l must be nonnegative")
+        return constant_plan(s.wl, s.schedule, l_override)
+    if not s.recompute:
+        return constant_plan(s.wl, s.schedule, 0)
+    return plan_generation(s.spec, s.wl, s.profile, s.schedule)
+
+
+def _out(text: str, path: str | None) -> None:
+    if path:
+        with open(path, "w") as fh:
+            fh.write(text)
+    else:
+        sys.stdout.write(text)
+
+
+def cmd_plan(a) -> int:
+    s = load_config(a.config)
+    _out(plan_to_json(_plan(s, a.l), s.spec, s.wl, s.profile) + "\n", a.out)
+    return EXIT_OK
+
+
+def cmd_calibrate(a) -> int:
+    _out(profile_to_json(calibrate(read_measurements_csv(a.measurements))) + "\n", a.out)
+    return EXIT_OK
+
+
+def cmd_profile(a) -> int:
+    from . import profiler
+    from .hwprofile import write_measurements_csv
+
+    res, recs = profiler.measure(a.hidden, a.batch)
+    if a.out:
+        write_measurements_csv(recs, a.out)
+    sys.stdout.write(profile_to_json(res) + "\n")
+    return EXIT_OK
+
+
+def _device_bytes(s: Setup, capacity: int) -> float:
+    h, L, f, b = s.spec.hidden_dim, s.spec.num_layers, s.spec.ffn_dim, s.wl.batch_size
+    weights = L * (4 * h * h + 2 * h * f) * 2 + 2 * 50272 * h * 2
+    buffers = 2 * capacity * 3 * b * h * 2 + b * 50272 * 4
+    return float(weights + buffers)
+
+
+def cmd_run(a) -> int:
+    import torch
+
+    from . import trace as tr
+    from .runtime import KVPRRuntime
+    from .weights import OPTConfig, OPTWeights
+
+    s = load_config(a.config)
+    if a.plan:
+        with open(a.plan) as fh:
+            plan, pspec, pwl, _ = import_plan(json.load(fh))
+        if (pspec, pwl) != (s.spec, s.wl):
+            raise ConfigError("plan context does not match the config")
+    else:
+        plan = _plan(s, a.l)
+    cap = s.wl.prompt_len + s.wl.gen_len + 1
+    need = _device_bytes(s, cap)
+    if s.budget is not None and need > s.budget:
+        raise GpuMemoryBudgetError(f"estimated device residency {need:.0f} B exceeds budget {s.budget:.0f} B")
+    rt_cfg = s.runtime
+    dev = torch.device(rt_cfg.get("device", "cuda:0"))
+    cfg = OPTConfig(s.spec.hidden_dim, s.spec.num_layers, s.spec.num_heads, s.spec.ffn_dim,
+                    max_pos=max(2048, cap + 8))
+    w = OPTWeights.random(cfg, seed=int(rt_cfg.get("seed", 0)), device=dev, std=float(rt_cfg.get("weights_std", 0.02)))
+    prompt = torch.randint(0, cfg.vocab, (s.wl.batch_size, s.wl.prompt_len),
+                           generator=torch.Generator().manual_seed(int(rt_cfg.get("seed", 0)) + 1))
+    rt = KVPRRuntime(w, s.wl.batch_size, cap, device=dev, chunks=int(rt_cfg.get("chunks", 4)))
+    first = rt.prefill(prompt)
+    tracer = tr.Tracer()
+    rt.decode(plan.splits, tokens=first, trace=tracer)
+    torch.cuda.synchronize(dev)
+    ents = tracer.entries()
+    rep = tr.report(ents, s.wl.batch_size * s.wl.gen_len)
+    rt.close()
+    if a.trace:
+        tr.write_trace(ents, a.trace)
+    if a.metrics:
+        with open(a.metrics, "w") as fh:
+            tr.write_metrics_csv([tr.metrics_row("kvpr" if s.recompute else "naive", rep, s.schedule, need)], fh)
+    lines = [f"makespan_s={rep['makespan_s']!r}", f"decode_throughput_tok_s={rep['throughput_tok_s']!r}",
+             f"gpu_utilization={rep['gpu_util']!r}", f"peak_gpu_bytes={need!r}",
+             f"splits={','.join(str(x) for x in plan.splits)}"]
+    lines += [f"busy_{k}={v!r}" for k, v in sorted(rep["breakdown"].items())]
+    sys.stdout.write("\n".join(lines) + "\n")
+    return EXIT_OK
+
+
+def cmd_validate(a) -> int:
+    """Device split/merge exactness: K1-rebuilt pages == the prefill's stored pages, bit for bit, and the
+    decode output is identical for every split, on randomized small geometries (cli.py:343-390 analogue)."""
+    import random
+
+    import torch
+
+    from . import kernels
+    from .runtime import KVPRRuntime
+    from .weights import OPTConfig, OPTWeights
+
+    rng = random.Random(a.seed)
+    failures = []
+    for case in range(a.cases):
+        heads = rng.choice([1, 2, 4, 8])
+        d = rng.choice([64, 128])
+        h = heads * d
+        b = rng.randint(1, 4)
+        S0 = rng.randint(1, 48)
+        cfg = OPTConfig(hidden=h, layers=2, heads=heads, ffn=4 * h, vocab=256, max_pos=128)
+        w = OPTWeights.random(cfg, seed=case, device="cuda", std=0.1, emb_std=0.1)
+        prompt = torch.randint(0, 256, (b, S0), generator=torch.Generator().manual_seed(case))
+        outs = []
+        for l in sorted({0, rng.randint(0, S0 + 1), S0 + 1}):
+            rt = KVPRRuntime(w, b, S0 + 2)
+            first = rt.prefill(prompt)
+            if not outs:
+                for j in range(cfg.layers):
+                    pages = torch.zeros(S0 + 2, 2, b, h, dtype=torch.float16, device="cuda")
+                    kernels.recompute_kv(rt.stores.x[j].cuda(), w.layers[j].w_kv, w.layers[j].b_kv, pages, b, 0, S0)
+                    if not torch.equal(pages[:S0].cpu(), rt.stores.kv[j][:S0]):
+                        failures.append(f"case={case} layer={j} h={h} b={b} s={S0}: rebuilt pages differ")
+            rt.decode([l], tokens=first, keep_logits=True)
+            torch.cuda.synchronize()
+            outs.append((l, rt.last_logits.cpu()))
+            rt.close()
+        for l, lg in outs[1:]:
+            if not torch.equal(lg, outs[0][1]):
+                failures.append(f"case={case} h={h} b={b} s'={S0 + 1} l={l}: logits differ from l=0")
+    if failures:
+        for f in failures:
+            print(f"FAIL {f}", file=sys.stderr)
+        print(f"validation failed: {len(failures)} case(s)", file=sys.stderr)
+        return EXIT_VALIDATION
+    print(f"ok: {a.cases} cases, rebuilt pages and decode logits bit-exact for every split")
+    return EXIT_OK
+
+
+def build_parser() -> argparse.ArgumentParser:
+    p = _Parser(prog="paper_2411_17089_b200", description="KVPR decode path on B200")
+    sub = p.add_subparsers(dest="command", required=True)
+    sp = sub.add_parser("plan")
+    sp.add_argument("--config", required=True)
+    sp.add_argument("--l", type=int, default=None)
+    sp.add_argument("--out")
+    sp.set_defaults(fn=cmd_plan)
+    sp = sub.add_parser("calibrate")
+    sp.add_argument("--measurements", required=True)
+    sp.add_argument("--out")
+    sp.set_defaults(fn=cmd_calibrate)
+    sp = sub.add_parser("profile")
+    sp.add_argument("--hidden", type=int, default=4096)
+    sp.add_argument("--batch", type=int, default=32)
+    sp.add_argument("--out")
+    sp.set_defaults(fn=cmd_profile)
+    sp = sub.add_parser("run")
+    sp.add_argument("--config", required=True)
+    sp.add_argument("--plan")
+    sp.add_argument("--l", type=int, default=None)
+    sp.add_argument("--trace")
+    sp.add_argument("--metrics")
+    sp.set_defaults(fn=cmd_run)
+    sp = sub.add_parser("validate")
+    sp.add_argument("--cases", type=int, default=20)
+    sp.add_argument("--seed", type=int, default=0)
+    sp.set_defaults(fn=cmd_validate)
+    return p
+
+
+def main(argv=None) -> int:
+    level = os.environ.get("KVPR_LOG", "error").upper()
+    logging.basicConfig(level=getattr(logging, level, logging.ERROR), stream=sys.stderr)
+    try:
+        args = build_parser().parse_args(argv)
+        if getattr(args, "cases", 1) < 1:
+            raise ConfigError("--cases must be >= 1")
+        return args.fn(args)
+    except GpuMemoryBudgetError as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_BUDGET
+    except (ConfigError, ValueError, OSError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_INVALID

@@ -35,6 +35,85 @@ struct GemmCfg {
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
+
+// Epilogue for one thread: 32 fp32 accumulators of row (r_in, r_grp) at columns [n0, n0+32):
+// + bias, optional scale / ReLU, convert, scatter into the caller's layout (see GemmArgs).
+__device__ __forceinline__ void store_chunk(const GemmArgs& p, const uint32_t (&r)[32], int n0, long long r_in,
+                                            long long r_grp) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (p.bias != nullptr) {
+    const uint4* bp = reinterpret_cast<const uint4*>(p.bias + n0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint4 bw = __ldg(bp + u);
+      const __half2* h2 = reinterpret_cast<const __half2*>(&bw);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __half22float2(h2[e]);
+        v[u * 8 + e * 2] += f.x;
+        v[u * 8 + e * 2 + 1] += f.y;
+      }
+    }
+  }
+  if (n0 < p.scale_cols) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= p.scale;
+  }
+  if (p.flags & KVPR_EPI_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  const int seg = n0 / p.seg_width;
+  const int col = n0 - seg * p.seg_width;
+  // select the segment without dynamic indexing of the param arrays (keeps them out of local memory)
+  void* sp = seg == 0 ? p.seg_ptr[0] : (seg == 1 ? p.seg_ptr[1] : p.seg_ptr[2]);
+  const long long gs = seg == 0 ? p.seg_group_stride[0] : (seg == 1 ? p.seg_group_stride[1] : p.seg_group_stride[2]);
+  const long long off = r_in * p.ld + r_grp * gs + col;
+  if (p.flags & KVPR_EPI_F32) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(sp) + off);
+    if (p.flags & KVPR_EPI_ACCUM) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float4 old = o[u];
+        old.x += v[u * 4 + 0];
+        old.y += v[u * 4 + 1];
+        old.z += v[u * 4 + 2];
+        old.w += v[u * 4 + 3];
+        o[u] = old;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[u] = make_float4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+    }
+  } else {
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(sp) + off);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint4 w;
+      w.x = pack_half2(v[u * 8 + 0], v[u * 8 + 1]);
+      w.y = pack_half2(v[u * 8 + 2], v[u * 8 + 3]);
+      w.z = pack_half2(v[u * 8 + 4], v[u * 8 + 5]);
+      w.w = pack_half2(v[u * 8 + 6], v[u * 8 + 7]);
+      o[u] = w;
+    }
+  }
+}
+
+// Tile order: groups of kGroupM m-blocks, n-major inside a group, so the CTAs in flight share
+// a small band of A (reused across n from L2) and a few B column blocks.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
+  constexpr int kGroupM = 16;
+  const int per_group = kGroupM * num_n;
+  const int g = tile / per_group;
+  const int first_m = g * kGroupM;
+  const int gm = min(kGroupM, num_m - first_m);
+  const int local = tile - g * per_group;
+  m_blk = first_m + local % gm;
+  n_blk = local / gm;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(256, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -83,8 +162,8 @@ __global__ void __launch_bounds__(256, 1)
       // ---------------- TMA producer ----------------
       uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_blk = tile / p.num_n_blk;
-        const int n_blk = tile % p.num_n_blk;
+        int m_blk, n_blk;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
@@ -133,8 +212,8 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t q = warp & 3;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m_blk = tile / p.num_n_blk;
-      const int n_blk = tile % p.num_n_blk;
+      int m_blk, n_blk;
+      tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
       const uint32_t acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -152,62 +231,7 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
         const int n0 = n_blk * BN + c * 32;
         if (!row_ok || n0 >= p.N) continue;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.bias != nullptr) {
-          const uint4* bp = reinterpret_cast<const uint4*>(p.bias + n0);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 bw = __ldg(bp + u);
-            const __half2* h2 = reinterpret_cast<const __half2*>(&bw);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float2 f = __half22float2(h2[e]);
-              v[u * 8 + e * 2] += f.x;
-              v[u * 8 + e * 2 + 1] += f.y;
-            }
-          }
-        }
-        if (n0 < p.scale_cols) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= p.scale;
-        }
-        if (p.flags & KVPR_EPI_RELU) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-        }
-        const int seg = n0 / p.seg_width;
-        const int col = n0 - seg * p.seg_width;
-        const long long off = r_in * p.ld + r_grp * p.seg_group_stride[seg] + col;
-        if (p.flags & KVPR_EPI_F32) {
-          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.seg_ptr[seg]) + off);
-          if (p.flags & KVPR_EPI_ACCUM) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              float4 old = o[u];
-              old.x += v[u * 4 + 0];
-              old.y += v[u * 4 + 1];
-              old.z += v[u * 4 + 2];
-              old.w += v[u * 4 + 3];
-              o[u] = old;
-            }
-          } else {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) o[u] = make_float4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
-          }
-        } else {
-          uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.seg_ptr[seg]) + off);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 w;
-            w.x = pack_half2(v[u * 8 + 0], v[u * 8 + 1]);
-            w.y = pack_half2(v[u * 8 + 2], v[u * 8 + 3]);
-            w.z = pack_half2(v[u * 8 + 4], v[u * 8 + 5]);
-            w.w = pack_half2(v[u * 8 + 6], v[u * 8 + 7]);
-            o[u] = w;
-          }
-        }
+        store_chunk(p, r, n0, r_in, r_grp);
       }
       tc_fence_before();
       __syncwarp();
@@ -220,6 +244,165 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for the large-M GEMMs (K1, prefill): a
+// cluster of 2 CTAs computes a 256 x 256 tile with one tcgen05.mma M=256
+// issued by the leader.  Each CTA stages its 128-row half of A and its
+// 128-row half of B (so per-SM smem/L2 operand traffic drops by a third vs the
+// 1-CTA 128x256 tile) in a 6-deep ring; each CTA's TMEM holds the 128 x 256
+// accumulator of its own rows (double buffered, 512 columns).
+//   full[s]   (leader)  : leader arrive.expect_tx(both CTAs' bytes) + both CTAs' TMA complete_tx
+//   empty[s]  (both)    : leader's tcgen05.commit multicast to the pair
+//   tfull[a]  (both)    : leader's commit multicast after the last k-block of a tile
+//   tempty[a] (leader)  : 8 epilogue warps (4 per CTA) arrive, the peer's remotely
+
+constexpr int k2BN = 256;             // N of the pair tile (each CTA stages 128 rows of B)
+constexpr int k2Stages = 6;
+constexpr uint32_t k2ABytes = kBM * kBK * 2;          // 16 KB: this CTA's 128 rows of A
+constexpr uint32_t k2BBytes = (k2BN / 2) * kBK * 2;   // 16 KB: this CTA's 128 rows of B
+constexpr uint32_t k2StageBytes = k2ABytes + k2BBytes;
+constexpr uint32_t k2SmemBytes = k2Stages * k2StageBytes + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                            const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + k2Stages * k2ABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + k2Stages * k2BBytes);
+  uint64_t* empty = full + k2Stages;
+  uint64_t* tfull = empty + k2Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = p.num_m_blk * p.num_n_blk;
+  const int num_kb = p.num_k_blk;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      uint32_t stage = 0, phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        int m_blk, n_blk;
+        tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+        const int a_row = m_blk * 2 * kBM + rank * kBM;
+        const int b_row = n_blk * k2BN + rank * (k2BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
+          tma_load_2d_2sm(sA + stage * k2ABytes, &tmap_a, &full[stage], kb * kBK, a_row);
+          tma_load_2d_2sm(sB + stage * k2BBytes, &tmap_b, &full[stage], kb * kBK, b_row);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA, single thread) ----------------
+      constexpr uint32_t idesc = umma_idesc_f16_f32(2 * kBM, k2BN);
+      uint32_t stage = 0, phase = 0, local = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * k2BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * k2ABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * k2BBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_f16_2sm(d_tmem, umma_desc_k_sw128(a_addr + k * 32), umma_desc_k_sw128(b_addr + k * 32), idesc,
+                         (kb | k) != 0);
+          }
+          umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs, own 128 rows) ----------------
+    const uint32_t q = warp & 3;
+    uint32_t local = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+      int m_blk, n_blk;
+      tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+      const uint32_t acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * 2 * kBM + rank * kBM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      const long long r_in = row_ok ? (row % p.row_group) : 0;
+      const long long r_grp = row_ok ? (row / p.row_group) : 0;
+#pragma unroll 1
+      for (int c = 0; c < k2BN / 32; ++c) {
+        __syncwarp();
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * k2BN + c * 32, r);
+        tmem_ld_wait();
+        const int n0 = n_blk * k2BN + c * 32;
+        if (!row_ok || n0 >= p.N) continue;
+        store_chunk(p, r, n0, r_in, r_grp);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[acc]);
+        else
+          mbar_arrive_remote(&tempty[acc], 0);
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no MMA in flight, both epilogues done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<512>(tmem_base);
   }
 }
 
@@ -290,6 +473,30 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
   return check_launch("gemm_tcgen05");
 }
 
+
+static int launch_2sm(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  int rc = make_tmap(&ta, a, args.M, args.K, lda, kBM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, w, args.N, args.K, ldw, k2BN / 2);
+  if (rc) return rc;
+  args.num_m_blk = (args.M + 2 * kBM - 1) / (2 * kBM);
+  args.num_n_blk = (args.N + k2BN - 1) / k2BN;
+  args.num_k_blk = (args.K + kBK - 1) / kBK;
+  const int tiles = args.num_m_blk * args.num_n_blk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int attr_done[64] = {0};
+  if (dev < 64 && !attr_done[dev]) {
+    cudaFuncSetAttribute(gemm_tcgen05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2SmemBytes);
+    attr_done[dev] = 1;
+  }
+  const int pairs = sm_count(dev) / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  gemm_tcgen05_2sm_kernel<<<grid, 256, k2SmemBytes, stream>>>(ta, tb, args);
+  return check_launch("gemm_tcgen05_2sm");
+}
+
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream) {
   GemmArgs args = epi;
@@ -328,6 +535,8 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
     return KVPR_EINVAL;
   }
   switch (bn) {
+    case 512:  // 256 x 256 pair tile on a CTA pair (cta_group::2)
+      return launch_2sm(a, lda, w, ldw, args, stream);
     case 256:
       return launch_bn<256>(a, lda, w, ldw, args, stream);
     case 128:

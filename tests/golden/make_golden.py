@@ -33,6 +33,11 @@ from kvoverlap import numerics as rn  # noqa: E402
 from kvoverlap import scheduler as rs  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
+# the reference's shipped calibration sample (pkg/configs/measurements.csv), as data
+SAMPLE = [("h2d", 16777216, 0.000503), ("h2d", 67108864, 0.001967), ("h2d", 268435456, 0.007826),
+          ("h2d", 1073741824, 0.031262), ("d2h", 16777216, 0.000524), ("d2h", 67108864, 0.002041),
+          ("d2h", 268435456, 0.008103), ("d2h", 1073741824, 0.032391), ("gemm", 1099511627776, 0.004405),
+          ("gemm", 4398046511104, 0.017612), ("gemm", 17592186044416, 0.070442)]
 GIB = 2**30
 
 
@@ -131,7 +136,8 @@ def scheduler_cases():
             out["latency"].append(case(spec, wl, pl, 1024, mode))
 
     # calibrate(): the shipped sample CSV (values inlined) and a synthetic noisy set
-    sample = [("h2d", 16777216, 0.000503), ("h2d", 67108864, 0.001967), ("h2d", 268435456, 0.007826),
+    sample = SAMPLE
+    _unused = [("h2d", 16777216, 0.000503), ("h2d", 67108864, 0.001967), ("h2d", 268435456, 0.007826),
               ("h2d", 1073741824, 0.031262), ("d2h", 16777216, 0.000524), ("d2h", 67108864, 0.002041),
               ("d2h", 268435456, 0.008103), ("d2h", 1073741824, 0.032391), ("gemm", 1099511627776, 0.004405),
               ("gemm", 4398046511104, 0.017612), ("gemm", 17592186044416, 0.070442)]
@@ -175,8 +181,33 @@ def numerics_cases():
     return arrs
 
 
+def cli_cases():
+    """stdout of the reference CLI (`kvoverlap plan|calibrate`) for configs shipped with this repo."""
+    import contextlib
+    import io
+
+    from kvoverlap import cli as rcli
+
+    root = OUT.parents[1]
+    out = {}
+    for name, argv in (
+        ("plan_opt6.7b", ["plan", "--config", str(root / "configs" / "opt6.7b_b32_s1024.json")]),
+        ("plan_opt6.7b_l500", ["plan", "--config", str(root / "configs" / "opt6.7b_b32_s1024.json"), "--l", "500"]),
+        ("calibrate_sample", ["calibrate", "--measurements", str(OUT / "measurements_sample.csv")]),
+    ):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = rcli.main(argv)
+        out[name] = {"argv": argv[:1] + [a.replace(str(root) + "/", "") for a in argv[1:]], "rc": rc,
+                     "stdout": buf.getvalue()}
+    return out
+
+
 def main():
+    (OUT / "measurements_sample.csv").write_text(
+        "kind,size,elapsed_s\n" + "".join(f"{k},{s},{e}\n" for k, s, e in SAMPLE))
     doc = scheduler_cases()
+    doc["cli"] = cli_cases()
     (OUT / "scheduler_golden.json").write_text(json.dumps(doc, sort_keys=True) + "\n")
     np.savez_compressed(OUT / "numerics_golden.npz", **numerics_cases())
     print("wrote", OUT / "scheduler_golden.json", OUT / "numerics_golden.npz")

@@ -1,0 +1,60 @@
+"""CLI contract (no GPU): byte-identical plan / calibrate documents vs the
+reference CLI's stdout (tests/golden/scheduler_golden.json["cli"], produced by
+running `kvoverlap plan|calibrate` on the same files), config validation and
+the exit-code contract of pkg/src/kvoverlap/cli.py:45-48."""
+
+from __future__ import annotations
+
+import json
+
+import pytest
+
+from paper_2411_17089_b200 import cli
+
+from .conftest import GOLDEN, ROOT
+
+G = json.loads((GOLDEN / "scheduler_golden.json").read_text())["cli"]
+
+
+@pytest.mark.parametrize("name", sorted(G))
+def test_cli_output_identical_to_reference(name, capsys, monkeypatch):
+    monkeypatch.chdir(ROOT)
+    case = G[name]
+    rc = cli.main(case["argv"])
+    out = capsys.readouterr().out
+    assert rc == case["rc"] == 0
+    assert out == case["stdout"]
+
+
+def _cfg(tmp_path, doc):
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps(doc))
+    return str(p)
+
+
+BASE = {"model": {"preset": "opt-6.7b"}, "workload": {"batch_size": 4, "prompt_len": 8, "gen_len": 2},
+        "hardware": {"gpu_flops": 1e15, "h2d_bw": 5e10, "d2h_bw": 5e10}}
+
+
+def test_exit_codes(tmp_path, capsys):
+    assert cli.main(["plan", "--config", _cfg(tmp_path, BASE)]) == cli.EXIT_OK
+    bad = dict(BASE, model={"preset": "opt-6.7b", "bogus": 1})
+    assert cli.main(["plan", "--config", _cfg(tmp_path, bad)]) == cli.EXIT_INVALID
+    assert "unknown model keys" in capsys.readouterr().err
+    assert cli.main(["plan", "--config", _cfg(tmp_path, {"model": BASE["model"]})]) == cli.EXIT_INVALID
+    assert cli.main(["plan", "--config", _cfg(tmp_path, BASE), "--l", "-1"]) == cli.EXIT_INVALID
+    assert cli.main(["plan"]) == cli.EXIT_INVALID  # argparse usage error is 1, not 2
+    assert cli.main(["validate", "--cases", "0"]) == cli.EXIT_INVALID
+    p = tmp_path / "x.json"
+    p.write_text("{not json")
+    assert cli.main(["plan", "--config", str(p)]) == cli.EXIT_INVALID
+    budget = dict(BASE, hardware=dict(BASE["hardware"], gpu_mem_budget_bytes=1e6))
+    assert cli.main(["run", "--config", _cfg(tmp_path, budget)]) == cli.EXIT_BUDGET
+
+
+def test_plan_round_trip_through_file(tmp_path, capsys):
+    out = tmp_path / "plan.json"
+    assert cli.main(["plan", "--config", _cfg(tmp_path, BASE), "--out", str(out)]) == 0
+    doc = json.loads(out.read_text())
+    assert [d["seq_len"] for d in doc["decisions"]] == [9, 10]
+    assert doc["mode"] == "row"

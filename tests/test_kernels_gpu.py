@@ -44,6 +44,10 @@ def _rand(*shape, scale=1.0, dev="cuda", seed=None, dtype=torch.float16):
         (1, 64, 128, 64),
         (5, 50272, 768, 0),  # vocab-sized N tail, auto BN
         (777, 1024, 1000, 128),  # K tail (TMA zero fill)
+        (28224, 8192, 4096, 512),  # K1 at OPT-6.7B config 2 (l=882): CTA-pair tcgen05 (cta_group::2)
+        (300, 512, 4096, 512),  # pair tile with an M tail inside the peer CTA
+        (100, 768, 768, 512),  # M < 128: the peer CTA's rows are all out of range
+        (4096, 2304, 768, 512),  # N tail within the pair tile (2304 = 9 x 256)
     ],
 )
 def test_linear_matches_fp32(dev, M, N, K, bn):
@@ -55,6 +59,19 @@ def test_linear_matches_fp32(dev, M, N, K, bn):
     ref = a.float() @ w.float().T + bias.float()
     torch.cuda.synchronize()
     _close(out, ref)
+
+
+def test_pair_tile_bitwise_equals_single_cta(dev):
+    """The CTA-pair kernel and the 1-CTA kernel accumulate K in the same order: identical bits."""
+    M, N, K = 1000, 1024, 2048
+    a = _rand(M, K, scale=0.5, seed=41)
+    w = _rand(N, K, scale=0.05, seed=42)
+    o1 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    o2 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, None, o1, bn=256)
+    kernels.linear_simple(a, w, None, o2, bn=512)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
 
 
 def test_linear_epilogues(dev):

@@ -231,3 +231,32 @@ def test_overlap_roofline_appendix_a():
     wl = cm.WorkloadSpec(batch_size=32, prompt_len=1024, gen_len=1)
     t = sc.overlap_roofline(spec, wl, 1025, 882, 55e9, 1391.2e12)
     assert abs(t - 5.567e-3) < 1e-6
+
+
+@settings(max_examples=60, deadline=None)
+@given(
+    seq=st.integers(0, 400),
+    b=st.integers(1, 64),
+    hidden=st.sampled_from([256, 768, 4096]),
+    v=st.sampled_from([1e11, 1e13, 1.19e15, math.inf]),
+    bw=st.sampled_from([2 * GIB, 55e9]),
+    lat=st.sampled_from([0.0, 1e-5, 1e-3]),
+    q=st.sampled_from([None, 1.0, 0.5625]),
+)
+def test_overlap_solver_matches_scan(seq, b, hidden, v, bw, lat, q):
+    """Extension objective max(t_act + t_kv, t_rec): closed-form candidates == exhaustive scan."""
+    spec = cm.ModelSpec(hidden_dim=hidden, num_layers=1, num_heads=8, ffn_dim=4 * hidden)
+    wl = cm.WorkloadSpec(batch_size=b, prompt_len=seq, gen_len=1, kv_bytes_per_element=q)
+    p = hp.HardwareProfile(gpu_flops=v, h2d_bandwidth=bw, d2h_bandwidth=bw, transfer_latency=lat)
+    got = sc.solve_split_overlap(spec, wl, p, seq)
+    best = min(range(seq + 1), key=lambda l: (sc.overlap_layer_time(spec, wl, p, seq, l).total, l))
+    assert got.recompute_len == best
+    assert got.t_total == sc.overlap_layer_time(spec, wl, p, seq, best).total
+
+
+def test_overlap_mode_prefers_full_recompute_on_b200():
+    # SURVEY.md Appendix A finding: with X chunked under K1, l = s' minimises the per-layer time
+    spec = cm.opt_preset("opt-6.7b")
+    wl = cm.WorkloadSpec(batch_size=32, prompt_len=1024, gen_len=2)
+    p = hp.HardwareProfile(gpu_flops=1.19e15, h2d_bandwidth=55.3e9, d2h_bandwidth=55e9)
+    assert [d.recompute_len for d in sc.plan_generation_overlap(spec, wl, p).decisions] == [1025, 1026]

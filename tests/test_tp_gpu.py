@@ -1,0 +1,103 @@
+"""Head-sharded TP runtime (config 4) on GPUs.
+
+* world 1 (always runnable on one B200): TPRuntime reduces to the 1-GPU
+  runtime and must reproduce its tokens and logits bit for bit (same
+  kernels, same K order; only the X rounds / chunking differ).
+* world 2 (needs >= 2 GPUs; skipped otherwise): NCCL all-gather + all-reduce,
+  logits within 2e-2 relative of the unsharded runtime, tokens identical.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2411_17089_b200.runtime import KVPRRuntime
+from paper_2411_17089_b200.tp import TPRuntime
+from paper_2411_17089_b200.weights import OPTConfig, OPTWeights
+
+pytestmark = pytest.mark.gpu
+
+CFG = OPTConfig(hidden=512, layers=3, heads=8, ffn=2048, vocab=2048, max_pos=512)
+B, S0 = 4, 200
+SPLITS = [150, 0, 201, 77, 203, 5]
+
+
+def _weights(dev):
+    return OPTWeights.random(CFG, seed=13, device=dev, std=0.1, emb_std=0.1)
+
+
+def _prompt():
+    return torch.randint(0, CFG.vocab, (B, S0), generator=torch.Generator().manual_seed(14))
+
+
+def _reference(dev="cuda:0"):
+    w = _weights(dev)
+    rt = KVPRRuntime(w, B, S0 + len(SPLITS) + 1, device=dev)
+    first = rt.prefill(_prompt())
+    toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
+    torch.cuda.synchronize()
+    out = (first.cpu(), toks.cpu(), rt.last_logits.cpu())
+    rt.close()
+    return out
+
+
+def test_tp_world1_equals_single_gpu_runtime_bitwise():
+    f0, t0, l0 = _reference()
+    w = _weights("cuda:0")
+    rt = TPRuntime(w, B, S0 + len(SPLITS) + 1, block=16)
+    first = rt.prefill(_prompt())
+    toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(first.cpu(), f0)
+    assert torch.equal(toks.cpu(), t0)
+    assert torch.equal(rt.last_logits.cpu(), l0)
+    rt.close()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _tp_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        rt = TPRuntime(_weights(dev), B, S0 + len(SPLITS) + 1, block=16, device=dev)
+        first = rt.prefill(_prompt())
+        toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
+        torch.cuda.synchronize(dev)
+        q.put((rank, first.cpu(), toks.cpu(), rt.last_logits.cpu()))
+        rt.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_tp_world2_matches_unsharded():
+    f0, t0, l0 = _reference()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, first, toks, lg in res:
+        assert torch.equal(first, f0) and torch.equal(toks, t0), rank
+        rel = ((lg - l0).abs().amax(dim=-1) / l0.abs().amax(dim=-1)).max().item()
+        assert rel <= 2e-2, rel

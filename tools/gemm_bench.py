@@ -1,0 +1,37 @@
+"""Time the tcgen05 GEMM variants at the K1 shapes (CUDA events, warm, L2-cold inputs > L2).
+
+    python tools/gemm_bench.py        # prints JSON lines: shape, bn, us, TFLOP/s
+"""
+import json
+import sys
+
+sys.path.insert(0, ".")
+import torch
+
+from paper_2411_17089_b200 import kernels
+
+
+def bench(M, N, K, bn, reps=10):
+    dev = torch.device("cuda")
+    a = (torch.randn(M, K, device=dev) * 0.5).half()
+    w = (torch.randn(N, K, device=dev) * 0.02).half()
+    o = torch.empty(M, N, device=dev, dtype=torch.float16)
+    for _ in range(3):
+        kernels.linear_simple(a, w, None, o, bn=bn)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        kernels.linear_simple(a, w, None, o, bn=bn)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / reps / 1e3
+    return t, 2 * M * N * K / t / 1e12
+
+
+shapes = [(28224, 8192, 4096), (32 * 220, 8192, 4096), (64 * 1596, 1792, 7168), (32 * 1024, 12288, 4096),
+          (8192, 8192, 8192)]
+for M, N, K in shapes:
+    for bn in (256, 512):
+        t, tf = bench(M, N, K, bn)
+        print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "us": t * 1e6, "tflops": tf}), flush=True)
