@@ -208,17 +208,30 @@ def run_kvpr(args):
     total_steps = args.warmup + args.steps
     wl = WorkloadSpec(batch_size=b, prompt_len=args.prompt, gen_len=total_steps)
 
-    # profiler -> scheduler (bit-exact solver on the live profile)
-    calib, recs = profiler.measure(cfg.hidden, b, device=dev)
+    # profiler -> scheduler (bit-exact solver on the live profile); under TP every rank
+    # must run the same plan, so rank 0's profile is broadcast
+    calib, recs = profiler.measure(cfg.hidden, b if not args.tp else max(1, b // ws), device=dev)
     prof = calib.profile
     bw_peak = profiler.peak_h2d(recs)
+    if args.tp and ws > 1:
+        obj = [prof, bw_peak]
+        dist.broadcast_object_list(obj, src=0)
+        prof, bw_peak = obj
     plan = plan_generation(cfg.spec(), wl, prof, "column")
     splits = plan.splits
 
     w = OPTWeights.random(cfg, seed=0, device=dev)
-    g = torch.Generator().manual_seed(1 + rank)
+    g = torch.Generator().manual_seed(1 + (0 if args.tp else rank))
     prompt = torch.randint(0, cfg.vocab, (b, args.prompt), generator=g)
-    rt = KVPRRuntime(w, b, args.prompt + total_steps + 1, device=dev)
+    if args.tp:
+        from paper_2411_17089_b200.tp import TPRuntime
+
+        rt = TPRuntime(w, b, args.prompt + total_steps + 1, device=dev)
+        del w.layers[:]  # full-width layer weights are no longer needed once sharded
+        torch.cuda.empty_cache()
+        args.no_alt = True
+    else:
+        rt = KVPRRuntime(w, b, args.prompt + total_steps + 1, device=dev)
     t0 = time.perf_counter()
     first = rt.prefill(prompt)
     prefill_s = time.perf_counter() - t0
@@ -244,7 +257,8 @@ def run_kvpr(args):
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    value = ws * b * args.steps / elapsed
+    jobs = 1 if args.tp else ws  # TP: one batch across all GPUs; batch partition: one batch per GPU
+    value = jobs * b * args.steps / elapsed
 
     # per-layer latency and overlap roofline over the timed steps
     L = cfg.layers
@@ -289,7 +303,7 @@ def run_kvpr(args):
     mid = plan.decisions[args.warmup + args.steps // 2]
     lmid = min(mid.recompute_len, mid.seq_len - 1)
     kern = {}
-    if rank == 0:
+    if rank == 0 and not args.tp:
         lw = w.layers[0]
         xd, kvd = rt.x_dev[0], rt.kv_dev[0]
 
@@ -337,7 +351,7 @@ def run_kvpr(args):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = ws * b * e2e_steps / e2e_s
+    e2e_value = jobs * b * e2e_steps / e2e_s
     h2d_step = h2d_alg / args.steps + b * 4
     d2h_step = (3 * b * cfg.hidden * 2) * L + b * 4
 
@@ -356,10 +370,11 @@ def run_kvpr(args):
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "scaling": "strong" if args.tp else "weak", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
             "config": {
                 "workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV+X offloaded to pinned host",
-                "model": args.model, "global_batch": b * ws, "seq_len": args.prompt, "parallelism": f"batch-partition x{ws}",
+                "model": args.model, "global_batch": b * jobs, "seq_len": args.prompt,
+                "parallelism": f"tp{ws} (head-sharded, NCCL)" if args.tp else f"batch-partition x{ws}",
                 "mode": "column", "splits_timed": splits[args.warmup:],
                 "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
                 "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
@@ -399,6 +414,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the extension-objective measurement")
+    ap.add_argument("--tp", action="store_true",
+                    help="config 4: head-sharded tensor parallelism over the torchrun ranks (NCCL)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

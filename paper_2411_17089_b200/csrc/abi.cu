@@ -99,7 +99,9 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
   a.flags = 0;
   const __half* a_ptr = static_cast<const __half*>(x) + (long long)pos_begin * bh;
   const int M = (pos_end - pos_begin) * batch;
-  return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, 256, static_cast<cudaStream_t>(stream));
+  // CTA-pair 256x256 tiles once there are rows for a pair tile; 1-CTA 128x256 below that
+  const int bn = M >= 256 ? 512 : 256;
+  return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, bn, static_cast<cudaStream_t>(stream));
 }
 
 int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
@@ -110,14 +112,19 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
     return KVPR_EINVAL;
   }
   if (bn == 0) {
-    // small-M (decode) GEMMs are weight-streaming: narrow N tiles give more CTAs
+    // large GEMMs: CTA-pair 256x256 tiles when they fill the SM pairs; small-M (decode) GEMMs are
+    // weight-streaming, so narrower N tiles give more CTAs
     int dev = 0;
     cudaGetDevice(&dev);
     const int sms = sm_count(dev);
     const long long m_blk = (M + 127) / 128;
-    bn = 256;
-    if (m_blk * ((N + 255) / 256) < sms) bn = 128;
-    if (m_blk * ((N + 127) / 128) < sms) bn = 64;
+    if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {
+      bn = 512;
+    } else {
+      bn = 256;
+      if (m_blk * ((N + 255) / 256) < sms) bn = 128;
+      if (m_blk * ((N + 127) / 128) < sms) bn = 64;
+    }
   }
   return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream));
 }

@@ -177,6 +177,7 @@ class TPRuntime:
         self.ws = z(16 << 20, dt=torch.uint8)
         self.len = 0
         self._works = {}
+        self.launches = 0
 
     # ---------------------------------------------------------------- helpers
     def _allreduce_h(self, rows: torch.Tensor) -> None:
@@ -326,7 +327,12 @@ class TPRuntime:
         ev["done"][u] = torch.cuda.Event()
         ev["done"][u].record(cs)
 
-    def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False):
+    def reset(self, length: int) -> None:
+        torch.cuda.synchronize(self.dev)
+        self.len = length
+
+    def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
+               timing=None):
         cfg, b, L = self.cfg, self.batch, self.cfg.layers
         steps, base = len(splits), self.len
         if base + steps > self.capacity:
@@ -344,6 +350,10 @@ class TPRuntime:
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         ev = {"done": {}, "d2h": {}}
         n = steps * L
+        marks = []
+        t0 = torch.cuda.Event(enable_timing=True) if timing is not None else None
+        if t0 is not None:
+            t0.record(cs)
         self._issue_loads(0, base, splits, ev)
         for u in range(n):
             if u + 1 < n:
@@ -352,6 +362,11 @@ class TPRuntime:
             if j == 0:
                 kernels.embed(self.tok, self.embed, self.pos, self.hres, batch=b, pos_begin=base + i, stream=cs)
             self._compute(u, base, splits, ev)
+            self.launches += 12 + len(self.lay.rounds(min(splits[i], base + i)))
+            if timing is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(cs)
+                marks.append(e)
             if j == L - 1:
                 self._head(self.hres)
                 with torch.cuda.stream(cs):
@@ -366,6 +381,16 @@ class TPRuntime:
         cur.wait_stream(cs)
         cur.wait_stream(self.ds)
         self.last_logits = logits
+        if timing is not None:
+            cs.synchronize()
+            prev = t0
+            for i in range(steps):
+                row = []
+                for e in marks[i * L:(i + 1) * L]:
+                    row.append(prev.elapsed_time(e))
+                    prev = e
+                timing.layer_ms.append(row)
+                timing.step_ms.append(sum(row))
         return out
 
     def close(self):
