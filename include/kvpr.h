@@ -137,6 +137,21 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
  * page-locked for the copy to be asynchronous. */
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
+/* 4-bit groupwise KV pages (compressed KV offload; costmodel.py:109-118:
+ * kv_bytes_per_element = 4/8 + 4/64 = 0.5625).  Compressed page = codes
+ * [2][batch][hidden/2] bytes (element 2i low nibble) then params
+ * [2][batch][hidden/64] x (fp16 min, fp16 scale); hidden % 64 == 0.
+ * x^ = half(min + q*scale), q = clamp(rint((x - min)/scale), 0, 15). */
+size_t kvpr_kv4_page_bytes(int batch, int hidden);
+
+/* fp16 pages [pos_begin, pos_end) -> compressed pages (both buffers indexed from position 0). */
+int kvpr_kv4_quantize(const void* pages, void* qpages, int batch, int hidden, int pos_begin, int pos_end,
+                      void* stream);
+
+/* compressed pages [pos_begin, pos_end) -> fp16 pages, in place for K2 to read. */
+int kvpr_kv4_dequantize(const void* qpages, void* pages, int batch, int hidden, int pos_begin, int pos_end,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,7 +62,12 @@ class OPTOracle:
     """Weights dict uses the runtime's names (paper_2411_17089_b200.weights), torch layout [out, in]."""
 
     def __init__(self, shape: OPTShape, weights: dict[str, np.ndarray], batch: int, storage=np.float16,
-                 compute=np.float32):
+                 compute=np.float32, kv_bits: int | None = None):
+        if kv_bits not in (None, 4):
+            raise ValueError("kv_bits must be None or 4")
+        if kv_bits and storage is not np.float16:
+            raise ValueError("4-bit KV emulation needs fp16 storage")
+        self.kv_bits = kv_bits
         self.s = shape
         self.b = batch
         self.storage = storage
@@ -75,6 +80,14 @@ class OPTOracle:
     # -- helpers ------------------------------------------------------------
     def _st(self, a):
         return a.astype(self.storage).astype(self.compute)
+
+    def _kv_store(self, kv):
+        """What the host KV store holds: the fp16 page, or its 4-bit groupwise round trip."""
+        if self.kv_bits == 4:
+            from . import kvquant_ref
+
+            return kvquant_ref.roundtrip(np.asarray(kv, dtype=np.float16))
+        return kv
 
     def _lw(self, j, name):
         return self.w[f"layers.{j}.{name}"]
@@ -118,8 +131,7 @@ class OPTOracle:
             Xs = np.zeros((capacity, b, hd), dtype=self.storage)
             KVs = np.zeros((capacity, 2, b, hd), dtype=self.storage)
             Xs[:S0] = x
-            KVs[:S0, 0] = k
-            KVs[:S0, 1] = v
+            KVs[:S0] = self._kv_store(np.stack([k, v], axis=1).astype(self.storage))
             self.X.append(Xs)
             self.KV.append(KVs)
             qh = q.reshape(S0, b, H, d)
@@ -133,8 +145,11 @@ class OPTOracle:
         return self._logits(h[-1])
 
     # -- one decode step ---------------------------------------------------------
-    def decode_step(self, tokens: np.ndarray, split: int) -> np.ndarray:
-        """Input tokens [b] at position self.len; s' = self.len + 1; returns logits [b, V]."""
+    def decode_step(self, tokens: np.ndarray, split: int, write_stores: bool = True) -> np.ndarray:
+        """Input tokens [b] at position self.len; s' = self.len + 1; returns logits [b, V].
+
+        write_stores=False keeps externally supplied store rows for the new position
+        (teacher-forced comparison against another run's stores)."""
         seq = self.len + 1
         if not 0 <= split <= seq:
             raise ValueError(f"split must be in [0, {seq}], got {split}")
@@ -152,9 +167,9 @@ class OPTOracle:
             V[lp:seq - 1] = self.KV[j][lp:seq - 1, 1]
             K[seq - 1], V[seq - 1] = k, v
             # store the new position (store_activation / store_cache, graph.py:340-347)
-            self.X[j][seq - 1] = x
-            self.KV[j][seq - 1, 0] = k
-            self.KV[j][seq - 1, 1] = v
+            if write_stores:
+                self.X[j][seq - 1] = x
+                self.KV[j][seq - 1] = self._kv_store(np.stack([k, v])[None].astype(self.storage))[0]
             lg = np.einsum("sbhd,bhd->bhs", K.reshape(seq, b, H, d), q.reshape(b, H, d)) / np.sqrt(d)
             a = self._st(np.einsum("bhs,sbhd->bhd", _softmax(lg), V.reshape(seq, b, H, d)).reshape(b, hd))
             h = self._mlp_tail(j, h, a)
@@ -173,17 +188,18 @@ def margins(logits: np.ndarray) -> np.ndarray:
 
 
 def generate(shape: OPTShape, weights, prompt: np.ndarray, splits: list[int], storage=np.float16,
-             compute=np.float32, forced: np.ndarray | None = None, stores=None):
+             compute=np.float32, forced: np.ndarray | None = None, stores=None, kv_bits: int | None = None):
     """Prefill + len(splits) decode steps. Returns (tokens [steps+1, b], logits list, margins list).
 
     forced  [steps+1, b]: teacher forcing — step i consumes forced[i] instead of the
             previous greedy token (compares logits on identical inputs).
-    stores  (X [L][S][b][h], KV [L][S][2][b][h], first_tokens [b]): start decode from
-            externally produced host stores (e.g. the GPU prefill) instead of the
-            oracle's own prefill; logits[0] is then None.
+    stores  (X [L][S][b][h], KV [L][S][2][b][h], first_tokens [b]): decode from
+            externally produced host stores (e.g. the GPU run's final stores, which
+            also hold the rows it wrote during decode) instead of the oracle's own
+            prefill; those rows are read, never overwritten; logits[0] is then None.
     """
     b, S0 = prompt.shape
-    o = OPTOracle(shape, weights, b, storage=storage, compute=compute)
+    o = OPTOracle(shape, weights, b, storage=storage, compute=compute, kv_bits=kv_bits)
     if stores is None:
         lg = o.prefill(prompt, capacity=S0 + len(splits) + 1)
         toks = [greedy(lg)]
@@ -198,7 +214,7 @@ def generate(shape: OPTShape, weights, prompt: np.ndarray, splits: list[int], st
         logits = [None]
     for i, l in enumerate(splits):
         inp = toks[-1] if forced is None else np.asarray(forced[i], dtype=np.int64)
-        lg = o.decode_step(inp, l)
+        lg = o.decode_step(inp, l, write_stores=stores is None)
         logits.append(lg)
         toks.append(greedy(lg))
     return np.stack(toks), logits, [margins(x) if x is not None else None for x in logits]

@@ -37,6 +37,9 @@ EXPORTS = (
     "kvpr_embed",
     "kvpr_argmax",
     "kvpr_copy_async",
+    "kvpr_kv4_page_bytes",
+    "kvpr_kv4_quantize",
+    "kvpr_kv4_dequantize",
 )
 
 
@@ -77,6 +80,9 @@ _SIGS = {
     "kvpr_embed": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp], _i),
     "kvpr_argmax": ([_vp, _ll, _i, _i, _vp, _vp, _vp], _i),
     "kvpr_copy_async": ([_vp, _vp, _sz, _vp], _i),
+    "kvpr_kv4_page_bytes": ([_i, _i], _sz),
+    "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
+    "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
 }
 
 

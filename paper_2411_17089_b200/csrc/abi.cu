@@ -179,4 +179,20 @@ int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   return KVPR_OK;
 }
 
+size_t kvpr_kv4_page_bytes(int batch, int hidden) { return kv4_page_bytes(batch, hidden); }
+
+int kvpr_kv4_quantize(const void* pages, void* qpages, int batch, int hidden, int pos_begin, int pos_end,
+                      void* stream) {
+  g_err[0] = 0;
+  return kv4_quantize(static_cast<const __half*>(pages), static_cast<uint8_t*>(qpages), batch, hidden, pos_begin,
+                      pos_end, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_kv4_dequantize(const void* qpages, void* pages, int batch, int hidden, int pos_begin, int pos_end,
+                        void* stream) {
+  g_err[0] = 0;
+  return kv4_dequantize(static_cast<const uint8_t*>(qpages), static_cast<__half*>(pages), batch, hidden, pos_begin,
+                        pos_end, static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

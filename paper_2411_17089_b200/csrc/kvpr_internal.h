@@ -48,4 +48,10 @@ int embed(const int* tokens, const __half* tok_emb, const __half* pos_emb, float
 int argmax_rows(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val,
                 cudaStream_t stream);
 
+size_t kv4_page_bytes(int batch, int hidden);
+int kv4_quantize(const __half* pages, uint8_t* qpages, int batch, int hidden, int pos_begin, int pos_end,
+                 cudaStream_t stream);
+int kv4_dequantize(const uint8_t* qpages, __half* pages, int batch, int hidden, int pos_begin, int pos_end,
+                   cudaStream_t stream);
+
 }  // namespace kvpr

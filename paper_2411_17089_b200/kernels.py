@@ -67,16 +67,11 @@ def linear_simple(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, o
     M = a.shape[0]
     if out.dtype == torch.float32:
         flags |= _lib.EPI_F32
-    epi = _lib.make_epilogue([(out.data_ptr(), 0)], seg_width=_seg_width(N), ld=out.stride(0), row_group=M,
+    # one output segment covering all N columns, rows at out.stride(0)
+    epi = _lib.make_epilogue([(out.data_ptr(), 0)], seg_width=((N + 31) // 32) * 32, ld=out.stride(0), row_group=M,
                              bias=bias.data_ptr() if bias is not None else None, flags=flags)
-    # a single segment must cover all N columns
-    epi.seg_width = ((N + 31) // 32) * 32
     linear(a, w, epi, M=M, bn=bn, stream=stream)
     return out
-
-
-def _seg_width(n: int) -> int:
-    return ((n + 31) // 32) * 32
 
 
 def decode_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor, ws: torch.Tensor | None,
@@ -142,3 +137,26 @@ def argmax(logits: torch.Tensor, out_idx: torch.Tensor, out_val: torch.Tensor | 
         out_val.data_ptr() if out_val is not None else None, _stream(stream),
     )
     return out_idx
+
+
+def kv4_page_bytes(batch: int, hidden: int) -> int:
+    """Bytes of one compressed (4-bit groupwise) KV page: 2*batch*hidden*0.5625."""
+    return int(_lib.load().kvpr_kv4_page_bytes(batch, hidden))
+
+
+def kv4_quantize(pages: torch.Tensor, qpages: torch.Tensor, batch: int, pos_begin: int, pos_end: int,
+                 stream=None) -> None:
+    _need(pages, torch.float16, "pages")
+    _need(qpages, torch.uint8, "qpages")
+    hidden = pages.shape[-1]
+    _lib.call("kvpr_kv4_quantize", pages.data_ptr(), qpages.data_ptr(), batch, hidden, pos_begin, pos_end,
+              _stream(stream))
+
+
+def kv4_dequantize(qpages: torch.Tensor, pages: torch.Tensor, batch: int, pos_begin: int, pos_end: int,
+                   stream=None) -> None:
+    _need(pages, torch.float16, "pages")
+    _need(qpages, torch.uint8, "qpages")
+    hidden = pages.shape[-1]
+    _lib.call("kvpr_kv4_dequantize", qpages.data_ptr(), pages.data_ptr(), batch, hidden, pos_begin, pos_end,
+              _stream(stream))

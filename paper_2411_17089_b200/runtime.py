@@ -47,20 +47,23 @@ def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) ->
 class HostStores:
     """Per-layer X and KV stores in page-locked host memory (exact-size cudaHostRegister)."""
 
-    def __init__(self, layers: int, capacity: int, batch: int, hidden: int):
+    def __init__(self, layers: int, capacity: int, batch: int, hidden: int, kv_page_bytes: int | None = None):
         self.layers, self.capacity, self.batch, self.hidden = layers, capacity, batch, hidden
         self.x = torch.empty(layers, capacity, batch, hidden, dtype=F16)
-        self.kv = torch.empty(layers, capacity, 2, batch, hidden, dtype=F16)
+        if kv_page_bytes is None:  # fp16 pages [pos][2][b][h]
+            self.kv = torch.empty(layers, capacity, 2, batch, hidden, dtype=F16)
+        else:  # compressed pages (4-bit groupwise), kv_page_bytes each
+            self.kv = torch.empty(layers, capacity, kv_page_bytes, dtype=torch.uint8)
         self._registered = []
         for t in (self.x, self.kv):
             rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * t.element_size(), 0)
             if int(rc) != 0:
-                raise RuntimeError(f"cudaHostRegister failed ({rc}) for {t.numel() * 2 / 2**30:.1f} GiB")
+                raise RuntimeError(f"cudaHostRegister failed ({rc}) for {t.numel() * t.element_size() / 2**30:.1f} GiB")
             self._registered.append(t)
 
     @property
     def nbytes(self) -> int:
-        return (self.x.numel() + self.kv.numel()) * 2
+        return self.x.numel() * 2 + self.kv.numel() * self.kv.element_size()
 
     def close(self) -> None:
         for t in self._registered:
@@ -100,8 +103,12 @@ class KVPRRuntime:
     """One decoder replica on one GPU (the unit the batch-partitioned multi-GPU mode replicates)."""
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
-                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None):
+                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None):
+        """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625)."""
         cfg = weights.cfg
+        if kv_bits not in (None, 4):
+            raise ValueError("kv_bits must be None (fp16) or 4")
+        self.kv_bits = kv_bits
         if capacity > cfg.max_pos:
             raise ValueError(f"capacity {capacity} exceeds the position table ({cfg.max_pos})")
         self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
@@ -113,9 +120,14 @@ class KVPRRuntime:
             self.cs = torch.cuda.Stream(self.dev, priority=-1)  # compute
             self.hs = torch.cuda.Stream(self.dev)              # H2D copy engine
             self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
-        self.stores = stores or HostStores(cfg.layers, capacity, batch, h)
+        self.qbytes = kernels.kv4_page_bytes(b, h) if kv_bits == 4 else None
+        self.page_bytes = self.qbytes if kv_bits == 4 else 2 * b * h * 2
+        self.stores = stores or HostStores(cfg.layers, capacity, batch, h, self.qbytes)
         z = lambda *s, dt=F16: torch.empty(*s, dtype=dt, device=self.dev)  # noqa: E731
         self.kv_dev = z(nbuf, capacity, 2, b, h)
+        if kv_bits == 4:  # compressed staging: the transferred tail, and the new page on its way out
+            self.kvq_dev = z(nbuf, capacity, self.qbytes, dt=torch.uint8)
+            self.qnew = z(nbuf, self.qbytes, dt=torch.uint8)
         self.x_dev = z(nbuf, capacity, b, h)
         self.hres = z(b, h, dt=F32)
         self.q = z(b, h)
@@ -173,7 +185,11 @@ class KVPRRuntime:
                 kernels.layernorm(hbuf, lw.ln1_g, lw.ln1_b, x, eps=cfg.eps, stream=cs)
                 self._qkv(x, rows, lw, q, pages[:S0], q_group=b * h, stream=cs)
                 _copy(self.stores.x[j].data_ptr(), x.data_ptr(), rows * h * 2, cs)
-                _copy(self.stores.kv[j].data_ptr(), pages.data_ptr(), S0 * 2 * b * h * 2, cs)
+                if self.kv_bits == 4:
+                    kernels.kv4_quantize(pages, self.kvq_dev[0], b, 0, S0, stream=cs)
+                    _copy(self.stores.kv[j].data_ptr(), self.kvq_dev[0].data_ptr(), S0 * self.qbytes, cs)
+                else:
+                    _copy(self.stores.kv[j].data_ptr(), pages.data_ptr(), S0 * 2 * b * h * 2, cs)
                 kernels.prefill_attention(q, pages, a, b, cfg.heads, cfg.head_dim, S0, stream=cs)
                 self._mlp(a, rows, lw, hbuf, x, mid, stream=cs)
             last = hbuf[(S0 - 1) * b:]
@@ -249,7 +265,8 @@ class KVPRRuntime:
             self.ev_x[r][c].record(hs)
         if s - 1 > lp:
             sp = tr.begin(hs, "load_cache", i + 1, j + 1) if tr else None
-            _copy(kvd[lp].data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * 2 * row, hs)
+            dst = self.kvq_dev[buf][lp] if self.kv_bits == 4 else kvd[lp]
+            _copy(dst.data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * self.page_bytes, hs)
             if sp:
                 tr.end(hs, sp)
         self.ev_kv[r].record(hs)
@@ -263,11 +280,16 @@ class KVPRRuntime:
         x_slot, page = xd[s - 1], kvd[s - 1]
         tr = self._trace
         I, J = i + 1, j + 1
+        if u >= self.nbuf:  # the previous user's D2H has read this buffer's slot s'-1 / staging page
+            cs.wait_event(self.ev_d2h[(u - self.nbuf) % self._R])
         # new token: X = LN1(h) straight into the X slot of position s'-1, q/k/v with k,v into page s'-1
         sp = tr.begin(cs, "compute_mha", I, J, "proj") if tr else None
         kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
         self._k()
         self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
+        if self.kv_bits == 4:  # the stored copy of the new page is compressed; K2 reads the exact fp16 page
+            kernels.kv4_quantize(kvd[s - 1:s], self.qnew[buf:buf + 1], b, 0, 1, stream=cs)
+            self._k()
         if sp:
             tr.end(cs, sp)
         self.ev_qkv[r].record(cs)
@@ -278,7 +300,8 @@ class KVPRRuntime:
         if sp:
             tr.end(ds, sp)
         sp = tr.begin(ds, "store_cache", I, J) if tr else None
-        _copy(self.stores.kv[j][s - 1].data_ptr(), page.data_ptr(), 2 * b * h * 2, ds)
+        src = self.qnew[buf] if self.kv_bits == 4 else page
+        _copy(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes, ds)
         if sp:
             tr.end(ds, sp)
         self.ev_d2h[r].record(ds)
@@ -291,6 +314,9 @@ class KVPRRuntime:
                 tr.end(cs, sp)
             self._k()
         cs.wait_event(self.ev_kv[r])
+        if self.kv_bits == 4 and s - 1 > lp:  # expand the transferred 4-bit tail into fp16 pages
+            kernels.kv4_dequantize(self.kvq_dev[buf], kvd, b, lp, s - 1, stream=cs)
+            self._k()
         # K2 over the merged pages [0, s') in place, then W_O + residual
         sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)

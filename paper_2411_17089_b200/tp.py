@@ -300,6 +300,8 @@ class TPRuntime:
         cs, ds = self.cs, self.ds
         xd, kvd, xn = self.x_dev[buf], self.kv_dev[buf], self.x_new[buf]
         page = kvd[s - 1]
+        if u >= 2:  # the D2H of this buffer's previous user has read x_new / page
+            cs.wait_event(ev["d2h"][u - 2])
         kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, xn, eps=cfg.eps, stream=cs)
         self._qkv(xn, b, lw, self.q, page, cs)
         eq = torch.cuda.Event()

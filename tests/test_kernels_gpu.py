@@ -233,3 +233,30 @@ def test_embed_and_argmax(dev):
     ref_idx = logits.argmax(dim=1)
     assert idx.tolist() == ref_idx.tolist()
     assert idx[3].item() == 7
+
+
+@pytest.mark.parametrize("P,batch,hidden", [(3, 4, 768), (17, 32, 4096), (1, 1, 64)])
+def test_kv4_codec_bitwise_vs_oracle(dev, P, batch, hidden):
+    """4-bit groupwise KV pages: GPU codec == oracle/kvquant_ref.py byte for byte, both directions."""
+    import numpy as np
+
+    from oracle import kvquant_ref
+
+    g = torch.Generator().manual_seed(P * 31 + hidden)
+    x = (torch.randn(P + 2, 2, batch, hidden, generator=g) * 2).half()
+    x[0, 0, 0, :64] = 1.5  # a constant group (scale 0)
+    pages = x.to(dev)
+    qb = kernels.kv4_page_bytes(batch, hidden)
+    assert qb == kvquant_ref.page_bytes(batch, hidden) == int(2 * batch * hidden * 0.5625)
+    q = torch.zeros(P + 2, qb, dtype=torch.uint8, device=dev)
+    kernels.kv4_quantize(pages, q, batch, 1, P + 1)
+    back = torch.zeros_like(pages)
+    kernels.kv4_dequantize(q, back, batch, 1, P + 1)
+    torch.cuda.synchronize()
+    want_q = kvquant_ref.quantize(x[1:P + 1].numpy())
+    assert np.array_equal(q[1:P + 1].cpu().numpy(), want_q)
+    assert torch.all(q[0] == 0) and torch.all(q[P + 1] == 0)  # outside [pos_begin, pos_end) untouched
+    want_x = kvquant_ref.dequantize(want_q, batch, hidden)
+    assert np.array_equal(back[1:P + 1].cpu().numpy(), want_x)
+    err = (back[1:P + 1].float() - pages[1:P + 1].float()).abs().max().item()
+    assert err <= (x.float().max() - x.float().min()).item() / 15 / 2 + 1e-2
