@@ -366,6 +366,38 @@ def run_kvpr(args):
                           f"tok/s = 1/(t x {L} layers)"),
                "host_cpus": os.cpu_count()}
 
+    # row schedule (the reference's other mode, graph.py:16-17): X resident in HBM, only KV[l:] on PCIe
+    alt_row = None
+    if not args.no_alt and not args.tp:
+        rt.close()
+        del rt
+        torch.cuda.empty_cache()
+        plan_r = plan_generation(cfg.spec(), wl, prof, "row")
+        rt = KVPRRuntime(w, b, args.prompt + total_steps + 1, device=dev, x_resident=True)
+        fr = rt.prefill(prompt)
+        rt.decode(plan_r.splits[: args.warmup], tokens=fr)
+        if ws > 1:
+            dist.barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        r0.record(rt.cs)
+        rt.decode(plan_r.splits[args.warmup:])
+        r1.record(rt.cs)
+        torch.cuda.synchronize(dev)
+        row_s = r0.elapsed_time(r1) / 1e3
+        if ws > 1:
+            t = torch.tensor([row_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            row_s = float(t.item())
+        troof_r = 0.0
+        for d in plan_r.decisions[args.warmup:]:
+            troof_r += max(kv_remainder_bytes(cfg.spec(), wl, d.seq_len, d.recompute_len) / bw_peak,
+                           recompute_flops(cfg.spec(), wl, d.recompute_len) / f_peak) * L
+        alt_row = {"value": jobs * b * args.steps / row_s, "unit": "tok/s", "splits": plan_r.splits[args.warmup:],
+                   "ms_per_step": row_s / args.steps * 1e3, "roofline_frac": troof_r / row_s,
+                   "note": "row schedule: layer inputs X resident in HBM (8.9 GB), only KV[l:s'] over PCIe; "
+                           "reference solver in mode 'row' (t_act = 0); roofline max(KV bytes/BW, FLOPs/F_sust)"}
+
     # compressed KV offload (§8f: 4-bit groupwise KV, kv_bytes_per_element 0.5625), same model / batch
     alt_kv4 = None
     if not args.no_alt and not args.tp:
@@ -423,6 +455,7 @@ def run_kvpr(args):
             "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": int(h2d_step),
                     "d2h_bytes_per_step": int(d2h_step), "steps": e2e_steps},
             "alt_overlap_plan": alt,
+            "alt_row_schedule": alt_row,
             "alt_kv4": alt_kv4,
             "gpu_launches": launches,
             "clocks": clk,

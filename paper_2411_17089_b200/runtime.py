@@ -47,15 +47,18 @@ def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) ->
 class HostStores:
     """Per-layer X and KV stores in page-locked host memory (exact-size cudaHostRegister)."""
 
-    def __init__(self, layers: int, capacity: int, batch: int, hidden: int, kv_page_bytes: int | None = None):
+    def __init__(self, layers: int, capacity: int, batch: int, hidden: int, kv_page_bytes: int | None = None,
+                 with_x: bool = True):
         self.layers, self.capacity, self.batch, self.hidden = layers, capacity, batch, hidden
-        self.x = torch.empty(layers, capacity, batch, hidden, dtype=F16)
+        self.x = torch.empty(layers, capacity if with_x else 0, batch, hidden, dtype=F16)
         if kv_page_bytes is None:  # fp16 pages [pos][2][b][h]
             self.kv = torch.empty(layers, capacity, 2, batch, hidden, dtype=F16)
         else:  # compressed pages (4-bit groupwise), kv_page_bytes each
             self.kv = torch.empty(layers, capacity, kv_page_bytes, dtype=torch.uint8)
         self._registered = []
         for t in (self.x, self.kv):
+            if t.numel() == 0:
+                continue
             rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * t.element_size(), 0)
             if int(rc) != 0:
                 raise RuntimeError(f"cudaHostRegister failed ({rc}) for {t.numel() * t.element_size() / 2**30:.1f} GiB")
@@ -103,8 +106,13 @@ class KVPRRuntime:
     """One decoder replica on one GPU (the unit the batch-partitioned multi-GPU mode replicates)."""
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
-                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None):
-        """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625)."""
+                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None,
+                 x_resident: bool = False):
+        """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
+
+        x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
+        inputs X stay in HBM (no activation traffic, t_act = 0), only KV[l:s'-1] crosses PCIe, and K1
+        reads X[0:l] from the resident store; plan it with mode "row"."""
         cfg = weights.cfg
         if kv_bits not in (None, 4):
             raise ValueError("kv_bits must be None (fp16) or 4")
@@ -122,9 +130,11 @@ class KVPRRuntime:
             self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
         self.qbytes = kernels.kv4_page_bytes(b, h) if kv_bits == 4 else None
         self.page_bytes = self.qbytes if kv_bits == 4 else 2 * b * h * 2
-        self.stores = stores or HostStores(cfg.layers, capacity, batch, h, self.qbytes)
+        self.x_resident = x_resident
+        self.stores = stores or HostStores(cfg.layers, capacity, batch, h, self.qbytes, with_x=not x_resident)
         z = lambda *s, dt=F16: torch.empty(*s, dtype=dt, device=self.dev)  # noqa: E731
         self.kv_dev = z(nbuf, capacity, 2, b, h)
+        self.x_store = z(cfg.layers, capacity, b, h) if x_resident else None
         if kv_bits == 4:  # compressed staging: the transferred tail, and the new page on its way out
             self.kvq_dev = z(nbuf, capacity, self.qbytes, dt=torch.uint8)
             self.qnew = z(nbuf, self.qbytes, dt=torch.uint8)
@@ -184,7 +194,8 @@ class KVPRRuntime:
             for j, lw in enumerate(self.w.layers):
                 kernels.layernorm(hbuf, lw.ln1_g, lw.ln1_b, x, eps=cfg.eps, stream=cs)
                 self._qkv(x, rows, lw, q, pages[:S0], q_group=b * h, stream=cs)
-                _copy(self.stores.x[j].data_ptr(), x.data_ptr(), rows * h * 2, cs)
+                xs = self.x_store[j] if self.x_resident else self.stores.x[j]
+                _copy(xs.data_ptr(), x.data_ptr(), rows * h * 2, cs)
                 if self.kv_bits == 4:
                     kernels.kv4_quantize(pages, self.kvq_dev[0], b, 0, S0, stream=cs)
                     _copy(self.stores.kv[j].data_ptr(), self.kvq_dev[0].data_ptr(), S0 * self.qbytes, cs)
@@ -257,7 +268,7 @@ class KVPRRuntime:
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         row = b * h * 2
         tr = self._trace
-        for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
+        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks)):
             sp = tr.begin(hs, "load_activation_recompute", i + 1, j + 1, f"c{c}") if tr else None
             _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
             if sp:
@@ -276,7 +287,8 @@ class KVPRRuntime:
         i, j, s, lp, buf, r = self._unit(u, base_len, splits)
         lw = self.w.layers[j]
         cs, ds = self.cs, self.ds
-        xd, kvd = self.x_dev[buf], self.kv_dev[buf]
+        xd = self.x_store[j] if self.x_resident else self.x_dev[buf]
+        kvd = self.kv_dev[buf]
         x_slot, page = xd[s - 1], kvd[s - 1]
         tr = self._trace
         I, J = i + 1, j + 1
@@ -295,19 +307,21 @@ class KVPRRuntime:
         self.ev_qkv[r].record(cs)
         # store_activation / store_cache (graph.py:340-347) on the D2H engine
         ds.wait_event(self.ev_qkv[r])
-        sp = tr.begin(ds, "store_activation", I, J) if tr else None
-        _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
-        if sp:
-            tr.end(ds, sp)
+        if not self.x_resident:  # row schedule: the X row already sits in the resident store
+            sp = tr.begin(ds, "store_activation", I, J) if tr else None
+            _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
+            if sp:
+                tr.end(ds, sp)
         sp = tr.begin(ds, "store_cache", I, J) if tr else None
         src = self.qnew[buf] if self.kv_bits == 4 else page
         _copy(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes, ds)
         if sp:
             tr.end(ds, sp)
         self.ev_d2h[r].record(ds)
-        # K1: rebuild K,V[0:l) chunk by chunk as X lands
-        for c, (p0, p1) in enumerate(chunk_bounds(lp, self.chunks)):
-            cs.wait_event(self.ev_x[r][c])
+        # K1: rebuild K,V[0:l) chunk by chunk as X lands (one launch when X is resident)
+        for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks)):
+            if not self.x_resident:
+                cs.wait_event(self.ev_x[r][c])
             sp = tr.begin(cs, "compute_recompute", I, J, f"c{c}") if tr else None
             kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, p0, p1, stream=cs)
             if sp:

@@ -198,3 +198,24 @@ def test_kv4_decode_parity_teacher_forced(criterion):
                     f"<= 2e-2 over splits {splits}", ok)
     assert max(errs) <= LOGIT_RTOL, errs
     assert not bad, bad
+
+
+def test_row_schedule_x_resident_equals_column_bitwise():
+    """Row schedule (X resident in HBM, only KV[l:] over PCIe; graph.py:16-17): same tokens and logits,
+    bit for bit, as the column runtime on the same splits."""
+    cfg = OPTConfig(hidden=512, layers=3, heads=8, ffn=2048, vocab=2048)
+    batch, S0 = 3, 90
+    splits = [45, 0, 92, 3, 94]
+    w, prompt = _setup(cfg, batch, S0, seed=9)
+    outs = []
+    for resident in (False, True):
+        rt = KVPRRuntime(w, batch, S0 + len(splits) + 1, x_resident=resident)
+        first = rt.prefill(prompt)
+        toks = rt.decode(splits, tokens=first, keep_logits=True)
+        torch.cuda.synchronize()
+        outs.append((first.cpu(), toks.cpu(), rt.last_logits.cpu()))
+        if resident:
+            assert rt.stores.x.numel() == 0  # no host activation store in the row schedule
+        rt.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
