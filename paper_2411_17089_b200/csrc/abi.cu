@@ -124,6 +124,7 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
       bn = 256;
       if (m_blk * ((N + 255) / 256) < sms) bn = 128;
       if (m_blk * ((N + 127) / 128) < sms) bn = 64;
+      if (m_blk * ((N + 63) / 64) < sms && N % 32 == 0) bn = 32;
     }
   }
   return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream));

@@ -27,7 +27,7 @@ constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : (BN >= 64 ? 8 : 10));
   static constexpr uint32_t kABytes = kBM * kBK * 2;
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -543,6 +543,8 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
       return launch_bn<128>(a, lda, w, ldw, args, stream);
     case 64:
       return launch_bn<64>(a, lda, w, ldw, args, stream);
+    case 32:  // small-M weight streaming with few output columns: more CTAs in flight
+      return launch_bn<32>(a, lda, w, ldw, args, stream);
     default:
       set_error("gemm: unsupported BN=%d", bn);
       return KVPR_EINVAL;

@@ -48,6 +48,8 @@ def _rand(*shape, scale=1.0, dev="cuda", seed=None, dtype=torch.float16):
         (300, 512, 4096, 512),  # pair tile with an M tail inside the peer CTA
         (100, 768, 768, 512),  # M < 128: the peer CTA's rows are all out of range
         (4096, 2304, 768, 512),  # N tail within the pair tile (2304 = 9 x 256)
+        (32, 4096, 16384, 32),  # decode fc2 shape on narrow 128x32 tiles
+        (32, 4096, 4096, 0),  # decode out-proj, auto BN
     ],
 )
 def test_linear_matches_fp32(dev, M, N, K, bn):

@@ -29,6 +29,12 @@ def bench(M, N, K, bn, reps=10):
     return t, 2 * M * N * K / t / 1e12
 
 
+for M, N, K in ((32, 12288, 4096), (32, 4096, 4096), (32, 16384, 4096), (32, 4096, 16384), (32, 50272, 4096)):
+    for bn in (32, 64, 128, 0):
+        t, tf = bench(M, N, K, bn, reps=50)
+        print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "us": t * 1e6, "weight_gbs": N * K * 2 / t / 1e9}),
+              flush=True)
+
 shapes = [(28224, 8192, 4096), (32 * 220, 8192, 4096), (64 * 1596, 1792, 7168), (32 * 1024, 12288, 4096),
           (8192, 8192, 8192)]
 for M, N, K in shapes:
