@@ -48,6 +48,25 @@ def _views(flat: torch.Tensor, h: int, f: int) -> LayerWeights:
     return LayerWeights(**out)
 
 
+def weight_regions(h: int, f: int, part: str) -> list[tuple[int, int]]:
+    """(byte offset, bytes) DMA ranges of one layer's flat weight buffer.
+
+    'kv' = W_k|W_v rows and b_k|b_v (what K1 needs, loaded first under fine granularity);
+    'rest' = W_q rows, b_q, and W_o .. b2; 'all' = the whole layer.  kv + rest tile the buffer.
+    """
+    total = sum(_numel(s) for s in _shapes(h, f).values()) * 2
+    if part == "all":
+        return [(0, total)]
+    wq = h * h * 2  # bytes of W_q rows (wqkv rows [0:h])
+    bqkv0 = 3 * h * h * 2  # byte offset of bqkv
+    if part == "kv":
+        return [(wq, 2 * h * h * 2), (bqkv0 + 2 * h, 4 * h)]
+    if part == "rest":
+        rest0 = bqkv0 + 6 * h
+        return [(0, wq), (bqkv0, 2 * h), (rest0, total - rest0)]
+    raise ValueError(f"unknown weight part {part!r}")
+
+
 class StreamedRuntime:
     """num_batches x batch sequences; layer weights streamed from host each layer."""
 
@@ -96,23 +115,11 @@ class StreamedRuntime:
         self.h2d_bytes = 0
 
     # ------------------------------------------------------------ weight DMA
-    def _w_regions(self, part: str):
-        """(byte offset, bytes) ranges of a layer's flat buffer for part 'kv', 'rest' or 'all'."""
-        h, f = self.cfg.hidden, self.cfg.ffn
-        if part == "all":
-            return [(0, self.layer_numel * 2)]
-        wq = h * h * 2  # bytes of W_q rows (wqkv rows [0:h])
-        bqkv0 = 3 * h * h * 2  # byte offset of bqkv
-        if part == "kv":
-            return [(wq, 2 * h * h * 2), (bqkv0 + 2 * h, 4 * h)]
-        rest0 = bqkv0 + 6 * h
-        return [(0, wq), (bqkv0, 2 * h), (rest0, self.layer_numel * 2 - rest0)]
-
     def _load_w(self, g: int, part: str, stream) -> None:
         j, slot = g % self.cfg.layers, g % 2
         src = self.host_w[j].data_ptr()
         dst = self.dev_w[slot].data_ptr()
-        for off, n in self._w_regions(part):
+        for off, n in weight_regions(self.cfg.hidden, self.cfg.ffn, part):
             _copy(dst + off, src + off, n, stream)
             self.h2d_bytes += n
 

@@ -94,3 +94,24 @@ def test_partitioned_gather_over_gloo(global_batch):
     for rank, full, t in res:
         assert full == want
         assert t == float(world)
+
+
+@pytest.mark.parametrize("h,f", [(4096, 16384), (768, 3072), (64, 256)])
+def test_streamed_weight_regions_tile_the_layer(h, f):
+    """Fine-grained loads: the W_KV part and the rest cover every byte of a layer exactly once,
+    and the W_KV part is exactly what K1 reads (rows [h, 3h) of wqkv and b_k|b_v)."""
+    from paper_2411_17089_b200.streamed import weight_regions
+
+    total = weight_regions(h, f, "all")[0][1]
+    assert total == (3 * h * h + 3 * h + h * h + h + 4 * h + f * h + f + h * f + h) * 2
+    covered = sorted(weight_regions(h, f, "kv") + weight_regions(h, f, "rest"))
+    pos = 0
+    for off, n in covered:
+        assert off == pos and n > 0
+        pos += n
+    assert pos == total
+    kv = weight_regions(h, f, "kv")
+    assert kv[0] == (h * h * 2, 2 * h * h * 2) and kv[1] == (3 * h * h * 2 + 2 * h, 4 * h)
+    assert all(off % 16 == 0 for off, _ in covered)  # DMA / TMA friendly alignment
+    with pytest.raises(ValueError):
+        weight_regions(h, f, "ffn")
