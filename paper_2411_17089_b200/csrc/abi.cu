@@ -120,11 +120,14 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
     const long long m_blk = (M + 127) / 128;
     if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {
       bn = 512;
+    } else if (m_blk == 1) {
+      // one row block (decode): weight-streaming; per-CTA k-loop throughput, not CTA count, limits
+      // it, so wide N tiles win (measured: tools/gemm_bench.py, profiles/r01_gemm_variants.jsonl)
+      bn = 128;
     } else {
       bn = 256;
       if (m_blk * ((N + 255) / 256) < sms) bn = 128;
       if (m_blk * ((N + 127) / 128) < sms) bn = 64;
-      if (m_blk * ((N + 63) / 64) < sms && N % 32 == 0) bn = 32;
     }
   }
   return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream));

@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(256, 1)
         tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          // small-M GEMMs load only the live rows of A; the rest of the 128-row operand is stale smem
+          // that only produces accumulator rows the epilogue never stores
+          mbar_arrive_expect_tx(&full[stage], p.a_box_rows * kBK * 2 + Cfg::kBBytes);
           tma_load_2d(sA + stage * Cfg::kABytes, &tmap_a, &full[stage], kb * kBK, m_blk * kBM);
           tma_load_2d(sB + stage * Cfg::kBBytes, &tmap_b, &full[stage], kb * kBK, n_blk * BN);
           if (++stage == STAGES) {
@@ -453,7 +455,8 @@ template <int BN>
 static int launch_bn(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ta, tb;
-  int rc = make_tmap(&ta, a, args.M, args.K, lda, kBM);
+  args.a_box_rows = args.M < kBM ? ((args.M + 7) / 8) * 8 : kBM;
+  int rc = make_tmap(&ta, a, args.M, args.K, lda, args.a_box_rows);
   if (rc) return rc;
   rc = make_tmap(&tb, w, args.N, args.K, ldw, BN);
   if (rc) return rc;

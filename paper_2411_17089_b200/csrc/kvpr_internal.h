@@ -26,6 +26,7 @@ struct GemmArgs {
   float scale;
   int scale_cols;
   int flags;
+  int a_box_rows;  // rows of A per TMA box (128, or M rounded up to 8 for single-tile small-M GEMMs)
 };
 
 int sm_count(int device);

@@ -30,7 +30,7 @@ def bench(M, N, K, bn, reps=10):
 
 
 for M, N, K in ((32, 12288, 4096), (32, 4096, 4096), (32, 16384, 4096), (32, 4096, 16384), (32, 50272, 4096)):
-    for bn in (32, 64, 128, 0):
+    for bn in (64, 128, 256, 0):
         t, tf = bench(M, N, K, bn, reps=50)
         print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "us": t * 1e6, "weight_gbs": N * K * 2 / t / 1e9}),
               flush=True)
