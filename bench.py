@@ -201,6 +201,7 @@ def run_kvpr(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
+        args.no_alt = True  # alt lines are single-GPU context; N ranks x their host stores would crowd host DRAM
     peaks = load_peaks()
     cfg = preset(args.model)
     cfg = cfg.with_positions(args.prompt + args.warmup + args.steps + 8)

@@ -101,6 +101,11 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
 int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                 const kvpr_epilogue* epi, int bn, void* stream);
 
+/* kvpr_linear with an fp32 scratch buffer: single-row-block (decode) GEMMs may then split K
+ * across CTAs (deterministic: partials reduced in slice order, then the same epilogue). */
+int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                   const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream);
+
 /* K2 — split-KV decode attention over the merged cache, read in place.
  * Replaces numerics.decode_attention's per-head loop (numerics.py:166-190):
  * per (sequence b, head) softmax(scale * K q) V over positions [0, seq_len)

@@ -31,6 +31,7 @@ EXPORTS = (
     "kvpr_sm_count",
     "kvpr_recompute_kv",
     "kvpr_linear",
+    "kvpr_linear_ws",
     "kvpr_decode_attention",
     "kvpr_prefill_attention",
     "kvpr_layernorm",
@@ -74,6 +75,7 @@ _SIGS = {
     "kvpr_sm_count": ([_i], _i),
     "kvpr_recompute_kv": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_linear": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp], _i),
+    "kvpr_linear_ws": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp, _sz, _vp], _i),
     "kvpr_decode_attention": ([_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
     "kvpr_prefill_attention": ([_vp, _vp, _vp, _i, _i, _i, _i, _f, _vp], _i),
     "kvpr_layernorm": ([_vp, _ll, _vp, _vp, _vp, _ll, _i, _i, _f, _vp], _i),

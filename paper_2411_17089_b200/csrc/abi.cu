@@ -106,6 +106,11 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
 
 int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                 const kvpr_epilogue* epi, int bn, void* stream) {
+  return kvpr_linear_ws(a, lda, w, ldw, M, N, K, epi, bn, nullptr, 0, stream);
+}
+
+int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                   const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
   if (epi == nullptr || a == nullptr || w == nullptr) {
     set_error("linear: null pointer");
@@ -130,7 +135,8 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
       if (m_blk * ((N + 127) / 128) < sms) bn = 64;
     }
   }
-  return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream));
+  return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream),
+                  static_cast<float*>(ws), ws_bytes);
 }
 
 int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* ws, size_t ws_bytes, int batch,

@@ -38,11 +38,8 @@ struct GemmCfg {
 
 // Epilogue for one thread: 32 fp32 accumulators of row (r_in, r_grp) at columns [n0, n0+32):
 // + bias, optional scale / ReLU, convert, scatter into the caller's layout (see GemmArgs).
-__device__ __forceinline__ void store_chunk(const GemmArgs& p, const uint32_t (&r)[32], int n0, long long r_in,
-                                            long long r_grp) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+__device__ __forceinline__ void store_chunk_f(const GemmArgs& p, float (&v)[32], int n0, long long r_in,
+                                              long long r_grp) {
   if (p.bias != nullptr) {
     const uint4* bp = reinterpret_cast<const uint4*>(p.bias + n0);
 #pragma unroll
@@ -101,6 +98,44 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& p, const uint32_t (&
   }
 }
 
+__device__ __forceinline__ void store_chunk(const GemmArgs& p, const uint32_t (&r)[32], int n0, int row,
+                                            long long r_in, long long r_grp, int ks) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (p.k_splits > 1) {  // raw partial of this K slice; split_k_reduce applies the epilogue
+    float4* o = reinterpret_cast<float4*>(p.ws + (static_cast<long long>(ks) * p.M + row) * p.ws_ld + n0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o[u] = make_float4(v[u * 4], v[u * 4 + 1], v[u * 4 + 2], v[u * 4 + 3]);
+    return;
+  }
+  store_chunk_f(p, v, n0, r_in, r_grp);
+}
+
+// Deterministic split-K reduction: partials summed in slice order, then the GEMM epilogue.
+__global__ void split_k_reduce_kernel(const GemmArgs p) {
+  const int chunks = p.N / 32;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(p.M) * chunks) return;
+  const int row = static_cast<int>(t / chunks);
+  const int n0 = static_cast<int>(t % chunks) * 32;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  for (int ks = 0; ks < p.k_splits; ++ks) {
+    const float4* w = reinterpret_cast<const float4*>(p.ws + (static_cast<long long>(ks) * p.M + row) * p.ws_ld + n0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4 x = w[u];
+      v[u * 4] += x.x;
+      v[u * 4 + 1] += x.y;
+      v[u * 4 + 2] += x.z;
+      v[u * 4 + 3] += x.w;
+    }
+  }
+  store_chunk_f(p, v, n0, row % p.row_group, row / p.row_group);
+}
+
 // Tile order: groups of kGroupM m-blocks, n-major inside a group, so the CTAs in flight share
 // a small band of A (reused across n from L2) and a few B column blocks.
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
@@ -154,8 +189,9 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = p.num_m_blk * p.num_n_blk;
-  const int num_kb = p.num_k_blk;
+  const int splits = p.k_splits > 1 ? p.k_splits : 1;
+  const int num_tiles = p.num_m_blk * p.num_n_blk * splits;
+  const int kb_per = (p.num_k_blk + splits - 1) / splits;  // host guarantees every slice is non-empty
 
   if (warp == 0) {
     if (lane == 0) {
@@ -163,8 +199,10 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int m_blk, n_blk;
-        tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+        const int kb0 = (tile % splits) * kb_per;
+        const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           // small-M GEMMs load only the live rows of A; the rest of the 128-row operand is stale smem
           // that only produces accumulator rows the epilogue never stores
@@ -189,7 +227,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = (tile % splits) * kb_per;
+        const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
@@ -198,7 +238,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             // advancing K by 16 fp16 = 32 bytes inside the 128B swizzle atom
             umma_f16(d_tmem, umma_desc_k_sw128(a_addr + k * 32), umma_desc_k_sw128(b_addr + k * 32), idesc,
-                     (kb | k) != 0);
+                     (kb != kb0) || (k != 0));
           }
           umma_commit(&empty[stage]);  // frees this smem slot once the MMAs above retire
           if (++stage == STAGES) {
@@ -215,7 +255,8 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int m_blk, n_blk;
-      tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+      tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+      const int ks = tile % splits;
       const uint32_t acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -233,7 +274,7 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
         const int n0 = n_blk * BN + c * 32;
         if (!row_ok || n0 >= p.N) continue;
-        store_chunk(p, r, n0, r_in, r_grp);
+        store_chunk(p, r, n0, row, r_in, r_grp, ks);
       }
       tc_fence_before();
       __syncwarp();
@@ -387,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         tmem_ld_wait();
         const int n0 = n_blk * k2BN + c * 32;
         if (!row_ok || n0 >= p.N) continue;
-        store_chunk(p, r, n0, r_in, r_grp);
+        store_chunk(p, r, n0, row, r_in, r_grp, 0);
       }
       tc_fence_before();
       __syncwarp();
@@ -463,7 +504,8 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
   args.num_m_blk = (args.M + kBM - 1) / kBM;
   args.num_n_blk = (args.N + BN - 1) / BN;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
-  const int tiles = args.num_m_blk * args.num_n_blk;
+  const int splits = args.k_splits > 1 ? args.k_splits : 1;
+  const int tiles = args.num_m_blk * args.num_n_blk * splits;
   int dev = 0;
   cudaGetDevice(&dev);
   static int attr_done[64] = {0};
@@ -473,7 +515,11 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
   }
   const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
   gemm_tcgen05_kernel<BN><<<grid, 256, Cfg::kSmemBytes, stream>>>(ta, tb, args);
-  return check_launch("gemm_tcgen05");
+  int rc2 = check_launch("gemm_tcgen05");
+  if (rc2 || splits == 1) return rc2;
+  const long long work = static_cast<long long>(args.M) * (args.N / 32);
+  split_k_reduce_kernel<<<static_cast<unsigned>((work + 127) / 128), 128, 0, stream>>>(args);
+  return check_launch("split_k_reduce");
 }
 
 
@@ -501,11 +547,30 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
 }
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
-             int bn, cudaStream_t stream) {
+             int bn, cudaStream_t stream, float* ws, size_t ws_bytes) {
   GemmArgs args = epi;
   args.M = M;
   args.N = N;
   args.K = K;
+  args.k_splits = 1;
+  args.ws = nullptr;
+  args.ws_ld = N;
+  if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256) {
+    // one row block, weight-streaming: each CTA's k-loop is latency bound, so slice K until the
+    // CTAs fill the SMs (deterministic: partials reduced in slice order by a second kernel)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int n_tiles = (N + bn - 1) / bn;
+    const int num_kb = (K + kBK - 1) / kBK;
+    int s = sm_count(dev) / n_tiles;
+    if (s > 8) s = 8;
+    while (s > 1 && (num_kb + s - 1) / s * (s - 1) >= num_kb) --s;  // every slice non-empty
+    if (s > 1 && static_cast<size_t>(s) * M * N * sizeof(float) <= ws_bytes &&
+        (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
+      args.k_splits = s;
+      args.ws = ws;
+    }
+  }
   if (M <= 0 || N <= 0 || K <= 0) {
     set_error("gemm: non-positive shape M=%d N=%d K=%d", M, N, K);
     return KVPR_EINVAL;

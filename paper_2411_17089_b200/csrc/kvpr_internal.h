@@ -27,12 +27,15 @@ struct GemmArgs {
   int scale_cols;
   int flags;
   int a_box_rows;  // rows of A per TMA box (128, or M rounded up to 8 for single-tile small-M GEMMs)
+  int k_splits;    // > 1: each CTA reduces a K slice into ws; a second kernel applies the epilogue
+  float* ws;       // split-K partials [k_splits][M][ws_ld] fp32
+  int ws_ld;
 };
 
 int sm_count(int device);
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
-             int bn, cudaStream_t stream);
+             int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0);
 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch,
                      int heads, int head_dim, int seq_len, float scale, cudaStream_t stream);

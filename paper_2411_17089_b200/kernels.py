@@ -49,19 +49,23 @@ def recompute_kv(x: torch.Tensor, w_kv: torch.Tensor, b_kv: torch.Tensor | None,
 
 
 def linear(a: torch.Tensor, w: torch.Tensor, epi: _lib.Epilogue, M: int | None = None, bn: int = 0,
-           stream=None, lda: int | None = None) -> None:
-    """out = epilogue(A[M,K] . W[N,K]^T + bias) via the tcgen05 GEMM."""
+           stream=None, lda: int | None = None, ws: torch.Tensor | None = None) -> None:
+    """out = epilogue(A[M,K] . W[N,K]^T + bias) via the tcgen05 GEMM (ws enables split-K for decode GEMMs)."""
     _need(a, torch.float16, "a")
     _need(w, torch.float16, "w")
     N, K = w.shape
     if M is None:
         M = a.shape[0]
     lda = K if lda is None else lda
-    _lib.call("kvpr_linear", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn, _stream(stream))
+    if ws is None:
+        _lib.call("kvpr_linear", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn, _stream(stream))
+    else:
+        _lib.call("kvpr_linear_ws", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn,
+                  ws.data_ptr(), ws.numel() * ws.element_size(), _stream(stream))
 
 
 def linear_simple(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, out: torch.Tensor,
-                  flags: int = 0, bn: int = 0, stream=None) -> torch.Tensor:
+                  flags: int = 0, bn: int = 0, stream=None, ws: torch.Tensor | None = None) -> torch.Tensor:
     """Row-major out[M, N] (fp16 or fp32 per flags) = epilogue(a . w^T + bias)."""
     N = w.shape[0]
     M = a.shape[0]
@@ -70,7 +74,7 @@ def linear_simple(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, o
     # one output segment covering all N columns, rows at out.stride(0)
     epi = _lib.make_epilogue([(out.data_ptr(), 0)], seg_width=((N + 31) // 32) * 32, ld=out.stride(0), row_group=M,
                              bias=bias.data_ptr() if bias is not None else None, flags=flags)
-    linear(a, w, epi, M=M, bn=bn, stream=stream)
+    linear(a, w, epi, M=M, bn=bn, stream=stream, ws=ws)
     return out
 
 

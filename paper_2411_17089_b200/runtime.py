@@ -225,7 +225,7 @@ class KVPRRuntime:
     def _mlp(self, attn: torch.Tensor, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
         """h += attn W_o^T + b_o;  h += relu(LN2(h) W_1^T + b_1) W_2^T + b_2  (OPT pre-LN block)."""
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
-        kernels.linear_simple(attn[:M], lw.wo, lw.bo, hres[:M], flags=acc, stream=stream)
+        kernels.linear_simple(attn[:M], lw.wo, lw.bo, hres[:M], flags=acc, stream=stream, ws=self.ws)
         self._k()
         self._ffn(M, lw, hres, ybuf, mid, stream)
 
@@ -233,15 +233,15 @@ class KVPRRuntime:
         cfg = self.cfg
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, ybuf, rows=M, eps=cfg.eps, stream=stream)
-        kernels.linear_simple(ybuf[:M], lw.w1, lw.b1, mid[:M], flags=_lib.EPI_RELU, stream=stream)
-        kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream)
+        kernels.linear_simple(ybuf[:M], lw.w1, lw.b1, mid[:M], flags=_lib.EPI_RELU, stream=stream, ws=self.ws)
+        kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream, ws=self.ws)
         self._k(3)
 
     def _head(self, hrows: torch.Tensor, stream) -> None:
         """Final LN, tied LM head (fp32 logits) and greedy argmax into self.tok."""
         cfg = self.cfg
         kernels.layernorm(hrows, self.w.lnf_g, self.w.lnf_b, self.zf, eps=cfg.eps, stream=stream)
-        kernels.linear_simple(self.zf, self.w.embed, None, self.logits, stream=stream)
+        kernels.linear_simple(self.zf, self.w.embed, None, self.logits, stream=stream, ws=self.ws)
         kernels.argmax(self.logits, self.tok, stream=stream)
         self._k(3)
 
@@ -336,7 +336,7 @@ class KVPRRuntime:
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
         self._k(2)
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
-        kernels.linear_simple(self.attn, lw.wo, lw.bo, self.hres, flags=acc, stream=cs)
+        kernels.linear_simple(self.attn, lw.wo, lw.bo, self.hres, flags=acc, stream=cs, ws=self.ws)
         self._k()
         if sp:
             tr.end(cs, sp)

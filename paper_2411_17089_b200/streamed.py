@@ -153,10 +153,10 @@ class StreamedRuntime:
                     _copy(st.kv[j].data_ptr(), pages.data_ptr(), S0 * 2 * b * h * 2, cs)
                     kernels.prefill_attention(q, pages, a, b, cfg.heads, cfg.head_dim, S0, stream=cs)
                     acc = _lib.EPI_F32 | _lib.EPI_ACCUM
-                    kernels.linear_simple(a, lw.wo, lw.bo, hb[k], flags=acc, stream=cs)
+                    kernels.linear_simple(a, lw.wo, lw.bo, hb[k], flags=acc, stream=cs, ws=self.ws)
                     kernels.layernorm(hb[k], lw.ln2_g, lw.ln2_b, x, eps=cfg.eps, stream=cs)
-                    kernels.linear_simple(x, lw.w1, lw.b1, mid, flags=_lib.EPI_RELU, stream=cs)
-                    kernels.linear_simple(mid, lw.w2, lw.b2, hb[k], flags=acc, stream=cs)
+                    kernels.linear_simple(x, lw.w1, lw.b1, mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
+                    kernels.linear_simple(mid, lw.w2, lw.b2, hb[k], flags=acc, stream=cs, ws=self.ws)
             for k in range(K):
                 self._head(hb[k][(S0 - 1) * b:], k)
         cs.synchronize()
@@ -175,7 +175,7 @@ class StreamedRuntime:
     def _head(self, hrows, k):
         cs = self.cs
         kernels.layernorm(hrows, self.lnf_g, self.lnf_b, self.zf, eps=self.cfg.eps, stream=cs)
-        kernels.linear_simple(self.zf, self.embed, None, self.logits, stream=cs)
+        kernels.linear_simple(self.zf, self.embed, None, self.logits, stream=cs, ws=self.ws)
         kernels.argmax(self.logits, self.tok[k], stream=cs)
 
     # ------------------------------------------------------------------ decode
@@ -270,10 +270,10 @@ class StreamedRuntime:
             cs.wait_event(ev["kv"][u])
             kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
             acc = _lib.EPI_F32 | _lib.EPI_ACCUM
-            kernels.linear_simple(self.attn, lw.wo, lw.bo, hres, flags=acc, stream=cs)
+            kernels.linear_simple(self.attn, lw.wo, lw.bo, hres, flags=acc, stream=cs, ws=self.ws)
             kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, self.y, eps=cfg.eps, stream=cs)
-            kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs)
-            kernels.linear_simple(self.mid, lw.w2, lw.b2, hres, flags=acc, stream=cs)
+            kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
+            kernels.linear_simple(self.mid, lw.w2, lw.b2, hres, flags=acc, stream=cs, ws=self.ws)
             self.launches += 12 + len(ev["x"][u])
             ev["done"][u] = E()
             ev["done"][u].record(cs)

@@ -188,7 +188,8 @@ class TPRuntime:
     def _rowpar(self, a, w, bias, out, M):
         """Row-parallel projection into the residual: rank 0 accumulates (+bias), others overwrite; then all-reduce."""
         flags = _lib.EPI_F32 | (_lib.EPI_ACCUM if self.rank == 0 else 0)
-        kernels.linear_simple(a[:M], w, bias if self.rank == 0 else None, out[:M], flags=flags, stream=self.cs)
+        kernels.linear_simple(a[:M], w, bias if self.rank == 0 else None, out[:M], flags=flags, stream=self.cs,
+                              ws=self.ws)
         self._allreduce_h(out[:M])
 
     def _qkv(self, x, M, lw, q_out, pages, stream):
@@ -233,7 +234,7 @@ class TPRuntime:
                 kernels.prefill_attention(q, pages, a, b, lay.heads_local, lay.head_dim, S0, stream=cs)
                 self._rowpar(a, lw.wo, lw.bo, hbuf, rows)
                 kernels.layernorm(hbuf, lw.ln2_g, lw.ln2_b, x, eps=cfg.eps, stream=cs)
-                kernels.linear_simple(x, lw.w1, lw.b1, mid, flags=_lib.EPI_RELU, stream=cs)
+                kernels.linear_simple(x, lw.w1, lw.b1, mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
                 self._rowpar(mid, lw.w2, lw.b2, hbuf, rows)
             self._head(hbuf[(S0 - 1) * b:])
         cs.synchronize()
@@ -243,7 +244,7 @@ class TPRuntime:
     def _head(self, hrows):
         cs = self.cs
         kernels.layernorm(hrows, self.lnf_g, self.lnf_b, self.zf, eps=self.cfg.eps, stream=cs)
-        kernels.linear_simple(self.zf, self.embed, None, self.logits, stream=cs)
+        kernels.linear_simple(self.zf, self.embed, None, self.logits, stream=cs, ws=self.ws)
         kernels.argmax(self.logits, self.tok, stream=cs)
 
     # ----------------------------------------------------------------- decode
@@ -324,7 +325,7 @@ class TPRuntime:
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, lay.heads_local, lay.head_dim, s, stream=cs)
         self._rowpar(self.attn, lw.wo, lw.bo, self.hres, b)
         kernels.layernorm(self.hres, lw.ln2_g, lw.ln2_b, self.y, eps=cfg.eps, stream=cs)
-        kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs)
+        kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
         self._rowpar(self.mid, lw.w2, lw.b2, self.hres, b)
         ev["done"][u] = torch.cuda.Event()
         ev["done"][u].record(cs)

@@ -262,3 +262,25 @@ def test_kv4_codec_bitwise_vs_oracle(dev, P, batch, hidden):
     assert np.array_equal(back[1:P + 1].cpu().numpy(), want_x)
     err = (back[1:P + 1].float() - pages[1:P + 1].float()).abs().max().item()
     assert err <= (x.float().max() - x.float().min()).item() / 15 / 2 + 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 4096, 16384), (32, 4096, 4096), (7, 768, 3072), (128, 1024, 8192)])
+def test_split_k_decode_gemm(dev, M, N, K):
+    """Single-row-block GEMMs with a workspace split K across CTAs; partials reduced in slice order:
+    fp32-reference accurate, run-to-run deterministic, all epilogues (bias, ReLU, fp32 residual add)."""
+    a = _rand(M, K, scale=0.5, seed=51)
+    w = _rand(N, K, scale=0.02, seed=52)
+    bias = _rand(N, scale=0.1, seed=53)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    ref = a.float() @ w.float().T + bias.float()
+    out = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, out, flags=_lib.EPI_RELU, ws=ws)
+    out2 = torch.empty_like(out)
+    kernels.linear_simple(a, w, bias, out2, flags=_lib.EPI_RELU, ws=ws)
+    resid = torch.randn(M, N, device=dev)
+    acc = resid.clone()
+    kernels.linear_simple(a, w, bias, acc, flags=_lib.EPI_ACCUM, ws=ws)
+    torch.cuda.synchronize()
+    _close(out, ref.clamp_min(0))
+    assert torch.equal(out, out2)
+    _close(acc, resid + ref, rtol=1e-5, atol=1e-4)
