@@ -221,6 +221,17 @@ def run_kvpr(args):
     plan = plan_generation(cfg.spec(), wl, prof, "column")
     splits = plan.splits
 
+    try:  # host stores are page-locked: warn early if the ranks of this node will not fit in DRAM
+        import psutil
+
+        need = cfg.layers * (args.prompt + total_steps + 1) * b * cfg.hidden * 2 * 3
+        local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        avail = psutil.virtual_memory().available
+        if need * local_ws > 0.9 * avail:
+            print(f"warning: {local_ws} ranks x {need / 2**30:.1f} GiB of pinned host stores vs "
+                  f"{avail / 2**30:.1f} GiB available", file=sys.stderr)
+    except ImportError:
+        pass
     w = OPTWeights.random(cfg, seed=0, device=dev)
     g = torch.Generator().manual_seed(1 + (0 if args.tp else rank))
     prompt = torch.randint(0, cfg.vocab, (b, args.prompt), generator=g)

@@ -555,7 +555,9 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
   args.k_splits = 1;
   args.ws = nullptr;
   args.ws_ld = N;
-  if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256) {
+  if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256 && K >= 8192) {
+    // only long k-loops gain: short ones are dominated by pipeline fill + the extra reduce launch
+    // (measured: fc2 32x4096x16384 75 -> 51 us; out-proj 32x4096x4096 23 -> 29 us)
     // one row block, weight-streaming: each CTA's k-loop is latency bound, so slice K until the
     // CTAs fill the SMs (deterministic: partials reduced in slice order by a second kernel)
     int dev = 0;
