@@ -27,7 +27,6 @@ KV[l:s'-1] are single contiguous byte ranges.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 
 import torch

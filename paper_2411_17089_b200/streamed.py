@@ -208,7 +208,7 @@ class StreamedRuntime:
             return g, k, i, j, s, min(splits[i], s - 1)
 
         def issue(u):
-            g, k, i, j, s, lp = unit(u)
+            g, k, _, j, s, lp = unit(u)
             buf = u % 2
             if u >= 2:
                 hs.wait_event(ev["done"][u - 2])

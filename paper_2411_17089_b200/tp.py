@@ -201,7 +201,7 @@ class TPRuntime:
 
     def _k1(self, xd, lw, kvd, p0, p1, stream):
         """K1 for the local heads: pages[p] = X[p] . W_kv_local^T + b (positions [p0, p1))."""
-        b, h, hs = self.batch, self.cfg.hidden, self.lay.hs
+        b, hs = self.batch, self.lay.hs
         if p1 <= p0:
             return
         page0 = kvd[p0].data_ptr()
@@ -292,10 +292,8 @@ class TPRuntime:
 
     def _compute(self, u, base, splits, ev):
         cfg, b, h, lay = self.cfg, self.batch, self.cfg.hidden, self.lay
-        L = cfg.layers
-        i, j = divmod(u, L)
-        s = base + i + 1
-        lp = min(splits[i], s - 1)
+        i, j = divmod(u, cfg.layers)
+        s = base + i + 1  # the rebuilt prefix length was fixed when the loads were issued (_works[u])
         buf = u % 2
         lw = self.layers[j]
         cs, ds = self.cs, self.ds

@@ -13,7 +13,6 @@ num_batches at 4 for fp16 KV at prompt 1024.
 import argparse
 import json
 import sys
-import time
 
 sys.path.insert(0, ".")
 import torch

@@ -17,7 +17,6 @@ import argparse
 import json
 import statistics
 import sys
-import time
 
 sys.path.insert(0, ".")
 
