@@ -257,11 +257,16 @@ def run_kvpr(args):
     tim = DecodeTiming()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
+    if hasattr(rt, "kernel_timing"):
+        rt.kernel_timing = []  # CUDA events around every K1 / K2 launch of the timed steps
     start.record(rt.cs)
     rt.decode(splits[args.warmup:], timing=tim)
     end.record(rt.cs)
     torch.cuda.synchronize(dev)
     launches = rt.launches - launches0
+    kstats = rt.kernel_stats() if hasattr(rt, "kernel_stats") else {}
+    if hasattr(rt, "kernel_timing"):
+        rt.kernel_timing = None
     elapsed = start.elapsed_time(end) / 1e3
     clk = clocks.stop(local) if clocks else None
     if ws > 1:
@@ -332,7 +337,7 @@ def run_kvpr(args):
         if lmid > 0:
             t_k1 = ev_time(lambda: kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, 0, lmid, stream=rt.cs))
             fl = recompute_flops(cfg.spec(), wl, lmid)
-            kern["k1_recompute_gemm"] = {"bound": "tensor", "achieved": fl / t_k1 / 1e12,
+            kern["k1_recompute_gemm_standalone"] = {"bound": "tensor", "achieved": fl / t_k1 / 1e12,
                                          "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                                          "frac": fl / t_k1 / 1e12 / peaks["bf16_tflops"], "traffic": None,
                                          "us": t_k1 * 1e6, "M": b * lmid, "N": 2 * cfg.hidden, "K": cfg.hidden}
@@ -340,7 +345,7 @@ def run_kvpr(args):
         t_k2 = ev_time(lambda: kernels.decode_attention(rt.q, kvd, rt.attn, rt.ws, b, cfg.heads, cfg.head_dim, s,
                                                         stream=rt.cs))
         by = 2 * b * s * cfg.hidden * 2
-        kern["k2_decode_attention"] = {"bound": "hbm", "achieved": by / t_k2 / 1e9, "peak": peaks["hbm_gbs"],
+        kern["k2_decode_attention_standalone"] = {"bound": "hbm", "achieved": by / t_k2 / 1e9, "peak": peaks["hbm_gbs"],
                                        "unit": "GB/s", "frac": by / t_k2 / 1e9 / peaks["hbm_gbs"], "traffic": None,
                                        "us": t_k2 * 1e6}
 
@@ -440,6 +445,27 @@ def run_kvpr(args):
                    "note": "KV cache stored and streamed as 4-bit groupwise pages (0.5625 B/elem, lossy); "
                            "reference solver with kv_bytes_per_element=0.5625; not the headline workload"}
 
+    # dominant kernel (K1) roofline from the launches inside the timed region (events on the compute stream)
+    k1_roof = None
+    if "k1" in kstats:
+        n, t, fl = kstats["k1"]
+        traffic = None
+        tp = ROOT / "profiles" / "r01_k1_chunk_ncu.json"
+        if tp.exists():  # dram read+write per launch from one ncu --set full capture of a chunk-sized K1
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        k1_roof = {"bound": "tensor", "kernel": "K1 recompute GEMM (tcgen05 cta_group::2, TMA, TMEM)",
+                   "achieved": fl / t / 1e12, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                   "frac": fl / t / 1e12 / peaks["bf16_tflops_sustained"], "traffic": traffic,
+                   "launches": n, "flops_per_launch": fl, "us_per_launch": t * 1e6,
+                   "algorithmic_bytes_per_launch": None,
+                   "peak_note": "sustained bf16 (kernel timed inside a long step); "
+                                f"burst {peaks['bf16_tflops']} TFLOP/s"}
+    if "k2" in kstats:
+        n, t, by = kstats["k2"]
+        kern["k2_decode_attention_in_step"] = {"bound": "hbm", "achieved": by / t / 1e9, "peak": peaks["hbm_gbs"],
+                                               "unit": "GB/s", "frac": by / t / 1e9 / peaks["hbm_gbs"],
+                                               "launches": n, "us_per_launch": t * 1e6}
+
     if rank == 0:
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
@@ -453,13 +479,14 @@ def run_kvpr(args):
                 "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
                 "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
             },
-            "roofline": {
+            "roofline": k1_roof,
+            "overlap_roofline": {
                 "bound": "pcie", "achieved": achieved_gbs, "peak": bw_peak / 1e9, "unit": "GB/s",
                 "frac": troof / elapsed, "traffic": None,
-                "note": "overlap roofline per layer max(H2D(X[:, :l]+KV[l:s'-1]) / measured pinned H2D peak, "
-                        "4bl h^2 / sustained bf16 peak); frac = T_roof / T_measured",
-                "kernels": kern,
+                "note": "north-star per-layer overlap roofline max(H2D(X[:, :l]+KV[l:s'-1]) / measured pinned H2D "
+                        "peak, 4bl h^2 / sustained bf16 peak); frac = T_roof / T_measured over the timed steps",
             },
+            "kernels": kern,
             "profile": {"gpu_flops": prof.gpu_flops, "h2d_bandwidth": prof.h2d_bandwidth,
                         "d2h_bandwidth": prof.d2h_bandwidth, "transfer_latency": prof.transfer_latency},
             "cpu_baseline": cpu,

@@ -158,10 +158,34 @@ class KVPRRuntime:
         self.ev_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
         self.launches = 0  # kernels issued (for bench's gpu_launches)
         self._trace = None
+        self.kernel_timing: list | None = None  # set to [] to time K1 / K2 launches with CUDA events
 
     # ------------------------------------------------------------------ utils
     def _k(self, n: int = 1) -> None:
         self.launches += n
+
+    def _ktimer(self, name: str, units: float, stream):
+        """With kernel_timing enabled, bracket one hot-kernel launch with CUDA events on its stream."""
+        if self.kernel_timing is None:
+            return None
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        return name, units, a
+
+    def _ktimer_end(self, kt, stream) -> None:
+        if kt is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.kernel_timing.append((kt[0], kt[1], kt[2], e))
+
+    def kernel_stats(self) -> dict:
+        """{name: (launches, mean seconds per launch, mean algorithmic units per launch)} of the timed launches."""
+        out = {}
+        for name, units, a, e in self.kernel_timing or []:
+            e.synchronize()
+            n, t, u = out.get(name, (0, 0.0, 0.0))
+            out[name] = (n + 1, t + a.elapsed_time(e) / 1e3, u + units)
+        return {k: (n, t / n, u / n) for k, (n, t, u) in out.items()}
 
     def reset(self, length: int) -> None:
         """Rewind the logical cache length (positions >= length are overwritten by later steps)."""
@@ -322,7 +346,9 @@ class KVPRRuntime:
             if not self.x_resident:
                 cs.wait_event(self.ev_x[r][c])
             sp = tr.begin(cs, "compute_recompute", I, J, f"c{c}") if tr else None
+            kt = self._ktimer("k1", 4 * b * (p1 - p0) * h * h, cs)
             kernels.recompute_kv(xd, lw.w_kv, lw.b_kv, kvd, b, p0, p1, stream=cs)
+            self._ktimer_end(kt, cs)
             if sp:
                 tr.end(cs, sp)
             self._k()
@@ -332,7 +358,9 @@ class KVPRRuntime:
             self._k()
         # K2 over the merged pages [0, s') in place, then W_O + residual
         sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
+        kt = self._ktimer("k2", 2 * b * s * h * 2, cs)
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
+        self._ktimer_end(kt, cs)
         self._k(2)
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.linear_simple(self.attn, lw.wo, lw.bo, self.hres, flags=acc, stream=cs, ws=self.ws)
