@@ -157,6 +157,40 @@ int kvpr_kv4_quantize(const void* pages, void* qpages, int batch, int hidden, in
 int kvpr_kv4_dequantize(const void* qpages, void* pages, int batch, int hidden, int pos_begin, int pos_end,
                         void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Native decode executor: the per-layer issue loop of the Python runtime
+ * (paper_2411_17089_b200/runtime.py, realising pipesim graph.py:232-347) in C,
+ * one call per decode run.  Same kernels, launch parameters and event DAG as the
+ * Python loop, hence identical results.  The caller owns every buffer; the handle
+ * holds descriptors and CUDA events only. */
+typedef struct kvpr_layer_desc {
+  const void *ln1_g, *ln1_b, *wqkv, *bqkv, *wo, *bo, *ln2_g, *ln2_b, *w1, *b1, *w2, *b2;
+  void* host_x;  /* pinned [capacity][batch][hidden] fp16 (unused when x_resident) */
+  void* host_kv; /* pinned [capacity][2][batch][hidden] fp16 */
+  void* dev_x;   /* x_resident: device [capacity][batch][hidden]; else NULL */
+} kvpr_layer_desc;
+
+typedef struct kvpr_decoder_desc {
+  int layers, batch, hidden, heads, ffn, vocab, capacity, chunks, nbuf, x_resident;
+  float eps;
+  const void *embed, *pos, *lnf_g, *lnf_b;
+  void* kv_dev; /* [nbuf][capacity][2][batch][hidden] fp16 */
+  void* x_dev;  /* [nbuf][capacity][batch][hidden] fp16 */
+  float* hres;  /* [batch][hidden] fp32 residual stream */
+  void *q, *attn, *y, *mid, *zf;
+  float* logits;
+  int* tok;     /* [batch] int32: input tokens of the first step, then each step's greedy output */
+  void* ws;
+  size_t ws_bytes;
+  void *compute_stream, *h2d_stream, *d2h_stream;
+} kvpr_decoder_desc;
+
+int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);
+int kvpr_decoder_destroy(void* handle);
+/* steps decode steps from cache length base_len with per-step splits; tokens of step i land in
+ * out_tokens[i][batch] (device, may be NULL), logits in out_logits[i][batch][vocab] (may be NULL). */
+int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, int* out_tokens, float* out_logits);
+
 #ifdef __cplusplus
 }
 #endif

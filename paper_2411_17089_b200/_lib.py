@@ -41,6 +41,9 @@ EXPORTS = (
     "kvpr_kv4_page_bytes",
     "kvpr_kv4_quantize",
     "kvpr_kv4_dequantize",
+    "kvpr_decoder_create",
+    "kvpr_decoder_destroy",
+    "kvpr_decoder_run",
 )
 
 
@@ -59,6 +62,21 @@ class Epilogue(ctypes.Structure):
         ("scale_cols", ctypes.c_int),
         ("flags", ctypes.c_int),
     ]
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2",
+        "host_x", "host_kv", "dev_x")]
+
+
+class DecoderDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "layers", "batch", "hidden", "heads", "ffn", "vocab", "capacity", "chunks", "nbuf", "x_resident")] + [
+        ("eps", ctypes.c_float)] + [(n, ctypes.c_void_p) for n in (
+            "embed", "pos", "lnf_g", "lnf_b", "kv_dev", "x_dev", "hres", "q", "attn", "y", "mid", "zf", "logits",
+            "tok", "ws")] + [("ws_bytes", ctypes.c_size_t)] + [(n, ctypes.c_void_p) for n in (
+                "compute_stream", "h2d_stream", "d2h_stream")]
 
 
 _lib: ctypes.CDLL | None = None
@@ -85,6 +103,9 @@ _SIGS = {
     "kvpr_kv4_page_bytes": ([_i, _i], _sz),
     "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
+    "kvpr_decoder_create": ([ctypes.POINTER(DecoderDesc), ctypes.POINTER(LayerDesc), ctypes.POINTER(_vp)], _i),
+    "kvpr_decoder_destroy": ([_vp], _i),
+    "kvpr_decoder_run": ([_vp, _i, ctypes.POINTER(_i), _i, _vp, _vp], _i),
 }
 
 

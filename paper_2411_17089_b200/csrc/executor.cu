@@ -1,0 +1,301 @@
+// Native decode executor: the per-layer issue loop of runtime.KVPRRuntime.decode in C++.
+//
+// Same DAG, same kernels, same launch parameters as the Python loop (so the two produce
+// identical bits, tests/test_executor_gpu.py), but one C call per decode run instead of
+// ~30 Python->C calls per layer — the loop costs ~microseconds per layer of host time, which
+// is what lets small models (BASELINE config 1) run at PCIe speed rather than at Python speed.
+//
+// Per unit u = (step i, layer j), buffer u % nbuf (graph.py:215-221 double buffering):
+//   H2D stream : [wait compute(u-nbuf), D2H(u-nbuf), D2H(u-L)] X chunks -> x_dev, KV tail -> kv_dev
+//   compute    : LN1 -> q,k,v (k,v into page s'-1) -> K1 per landed chunk -> [KV] K2 -> out-proj
+//                -> LN2 -> fc1 -> fc2 ; head on the last layer
+//   D2H stream : new X row, new K,V page -> host stores
+// The caller owns every buffer (the handle holds only descriptors and CUDA events).
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "kvpr_internal.h"
+
+namespace kvpr {
+
+namespace {
+
+struct Decoder {
+  kvpr_decoder_desc d;
+  std::vector<kvpr_layer_desc> layer;
+  int R = 0;
+  std::vector<cudaEvent_t> ev_x, ev_kv, ev_qkv, ev_d2h, ev_done;  // ring of R units (ev_x: R*chunks)
+};
+
+inline int ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
+#define KV_TRY(x)              \
+  do {                         \
+    int _rc = (x);             \
+    if (_rc) return _rc;       \
+  } while (0)
+
+// chunk_bounds() of runtime.py: <= chunks contiguous ranges of >= min_rows positions when possible
+inline int chunk_bounds(int n, int chunks, int (*out)[2], int min_rows = 64) {
+  if (n <= 0) return 0;
+  int c = n >= min_rows ? n / min_rows : 1;
+  if (c > chunks) c = chunks;
+  if (c < 1) c = 1;
+  const int base = n / c, rem = n % c;
+  int p = 0;
+  for (int i = 0; i < c; ++i) {
+    const int q = p + base + (i < rem ? 1 : 0);
+    out[i][0] = p;
+    out[i][1] = q;
+    p = q;
+  }
+  return c;
+}
+
+kvpr_epilogue simple_epi(void* out, long long ld, int M, int N, const void* bias, int flags) {
+  kvpr_epilogue e;
+  memset(&e, 0, sizeof(e));
+  e.bias = bias;
+  e.seg_width = ((N + 31) / 32) * 32;
+  e.row_group = M;
+  e.ld = ld;
+  e.seg[0].ptr = out;
+  e.scale = 1.f;
+  e.flags = flags;
+  return e;
+}
+
+struct Unit {
+  int i, j, s, lp, buf, r;
+};
+
+inline Unit unit_of(const Decoder& D, int u, int base, const int* splits) {
+  const int L = D.d.layers;
+  Unit x;
+  x.i = u / L;
+  x.j = u % L;
+  x.s = base + x.i + 1;
+  x.lp = splits[x.i] < x.s - 1 ? splits[x.i] : x.s - 1;
+  x.buf = u % D.d.nbuf;
+  x.r = u % D.R;
+  return x;
+}
+
+int issue_h2d(Decoder& D, int u, int base, const int* splits) {
+  const kvpr_decoder_desc& d = D.d;
+  const Unit x = unit_of(D, u, base, splits);
+  cudaStream_t hs = static_cast<cudaStream_t>(d.h2d_stream);
+  if (u >= d.nbuf) {
+    const int rp = (u - d.nbuf) % D.R;
+    KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_done[rp], 0), "wait compute"));
+    KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_d2h[rp], 0), "wait d2h"));
+  }
+  if (u >= d.layers) KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_d2h[(u - d.layers) % D.R], 0), "wait store"));
+  const size_t row = static_cast<size_t>(d.batch) * d.hidden * 2;
+  const kvpr_layer_desc& Lw = D.layer[x.j];
+  char* xd = static_cast<char*>(d.x_dev) + static_cast<size_t>(x.buf) * d.capacity * row;
+  char* kvd = static_cast<char*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * row;
+  if (!d.x_resident) {
+    int cb[16][2];
+    const int nc = chunk_bounds(x.lp, d.chunks, cb);
+    for (int c = 0; c < nc; ++c) {
+      KV_TRY(ck(cudaMemcpyAsync(xd + cb[c][0] * row, static_cast<const char*>(Lw.host_x) + cb[c][0] * row,
+                                (cb[c][1] - cb[c][0]) * row, cudaMemcpyDefault, hs),
+                "h2d X"));
+      KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks + c], hs), "record X"));
+    }
+  }
+  if (x.s - 1 > x.lp) {
+    KV_TRY(ck(cudaMemcpyAsync(kvd + x.lp * 2 * row, static_cast<const char*>(Lw.host_kv) + x.lp * 2 * row,
+                              (x.s - 1 - x.lp) * 2 * row, cudaMemcpyDefault, hs),
+              "h2d KV"));
+  }
+  return ck(cudaEventRecord(D.ev_kv[x.r], hs), "record KV");
+}
+
+int head(Decoder& D, cudaStream_t cs) {
+  const kvpr_decoder_desc& d = D.d;
+  KV_TRY(layernorm(d.hres, d.hidden, static_cast<const __half*>(d.lnf_g), static_cast<const __half*>(d.lnf_b),
+                   static_cast<__half*>(d.zf), d.hidden, d.batch, d.hidden, d.eps, cs));
+  kvpr_epilogue e = simple_epi(d.logits, d.vocab, d.batch, d.vocab, nullptr, KVPR_EPI_F32);
+  KV_TRY(kvpr_linear_ws(d.zf, d.hidden, d.embed, d.hidden, d.batch, d.vocab, d.hidden, &e, 0, d.ws, d.ws_bytes, cs));
+  return argmax_rows(d.logits, d.vocab, d.batch, d.vocab, d.tok, nullptr, cs);
+}
+
+int compute(Decoder& D, int u, int base, const int* splits) {
+  const kvpr_decoder_desc& d = D.d;
+  const Unit x = unit_of(D, u, base, splits);
+  const kvpr_layer_desc& Lw = D.layer[x.j];
+  cudaStream_t cs = static_cast<cudaStream_t>(d.compute_stream);
+  cudaStream_t ds = static_cast<cudaStream_t>(d.d2h_stream);
+  const int b = d.batch, h = d.hidden;
+  const long long bh = static_cast<long long>(b) * h;
+  const size_t row = static_cast<size_t>(bh) * 2;
+  __half* xd = d.x_resident ? static_cast<__half*>(Lw.dev_x)
+                            : static_cast<__half*>(d.x_dev) + static_cast<size_t>(x.buf) * d.capacity * bh;
+  __half* kvd = static_cast<__half*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * bh;
+  __half* x_slot = xd + static_cast<size_t>(x.s - 1) * bh;
+  __half* page = kvd + static_cast<size_t>(x.s - 1) * 2 * bh;
+  if (u >= d.nbuf) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_d2h[(u - d.nbuf) % D.R], 0), "wait d2h (slot reuse)"));
+  if (x.j == 0) {
+    KV_TRY(embed(d.tok, static_cast<const __half*>(d.embed), static_cast<const __half*>(d.pos), d.hres, b, b,
+                 x.s - 1, h, 2, cs));
+  }
+  // new token: LN1 into the X slot of position s'-1; q / k,v (k,v into page s'-1)
+  KV_TRY(layernorm(d.hres, h, static_cast<const __half*>(Lw.ln1_g), static_cast<const __half*>(Lw.ln1_b), x_slot, h,
+                   b, h, d.eps, cs));
+  {
+    kvpr_epilogue e;
+    memset(&e, 0, sizeof(e));
+    e.bias = Lw.bqkv;
+    e.seg_width = h;
+    e.row_group = b;
+    e.ld = h;
+    e.seg[0].ptr = d.q;
+    e.seg[0].group_stride = 0;
+    e.seg[1].ptr = page;
+    e.seg[1].group_stride = 2 * bh;
+    e.seg[2].ptr = page + bh;
+    e.seg[2].group_stride = 2 * bh;
+    e.scale = 1.f;
+    KV_TRY(kvpr_linear(x_slot, h, Lw.wqkv, h, b, 3 * h, h, &e, 0, cs));
+  }
+  KV_TRY(ck(cudaEventRecord(D.ev_qkv[x.r], cs), "record qkv"));
+  KV_TRY(ck(cudaStreamWaitEvent(ds, D.ev_qkv[x.r], 0), "d2h wait"));
+  if (!d.x_resident) {
+    KV_TRY(ck(cudaMemcpyAsync(static_cast<char*>(Lw.host_x) + static_cast<size_t>(x.s - 1) * row, x_slot, row,
+                              cudaMemcpyDefault, ds),
+              "d2h X"));
+  }
+  KV_TRY(ck(cudaMemcpyAsync(static_cast<char*>(Lw.host_kv) + static_cast<size_t>(x.s - 1) * 2 * row, page, 2 * row,
+                            cudaMemcpyDefault, ds),
+            "d2h KV"));
+  KV_TRY(ck(cudaEventRecord(D.ev_d2h[x.r], ds), "record d2h"));
+  // K1 per landed chunk (one launch when X is resident)
+  {
+    int cb[16][2];
+    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb);
+    const __half* wkv = static_cast<const __half*>(Lw.wqkv) + static_cast<size_t>(h) * h;
+    const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
+    for (int c = 0; c < nc; ++c) {
+      if (!d.x_resident) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_x[x.r * d.chunks + c], 0), "wait X chunk"));
+      KV_TRY(kvpr_recompute_kv(xd, wkv, bkv, kvd, b, cb[c][0], cb[c][1], h, cs));
+    }
+  }
+  KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_kv[x.r], 0), "wait KV"));
+  KV_TRY(decode_attention(static_cast<const __half*>(d.q), kvd, static_cast<__half*>(d.attn),
+                          static_cast<float*>(d.ws), d.ws_bytes, b, d.heads, h / d.heads, x.s,
+                          static_cast<float>(1.0 / sqrt(static_cast<double>(h / d.heads))), cs));
+  {
+    kvpr_epilogue e = simple_epi(d.hres, h, b, h, Lw.bo, KVPR_EPI_F32 | KVPR_EPI_ACCUM);
+    KV_TRY(kvpr_linear_ws(d.attn, h, Lw.wo, h, b, h, h, &e, 0, d.ws, d.ws_bytes, cs));
+  }
+  KV_TRY(layernorm(d.hres, h, static_cast<const __half*>(Lw.ln2_g), static_cast<const __half*>(Lw.ln2_b),
+                   static_cast<__half*>(d.y), h, b, h, d.eps, cs));
+  {
+    kvpr_epilogue e = simple_epi(d.mid, d.ffn, b, d.ffn, Lw.b1, KVPR_EPI_RELU);
+    KV_TRY(kvpr_linear_ws(d.y, h, Lw.w1, h, b, d.ffn, h, &e, 0, d.ws, d.ws_bytes, cs));
+  }
+  {
+    kvpr_epilogue e = simple_epi(d.hres, h, b, h, Lw.b2, KVPR_EPI_F32 | KVPR_EPI_ACCUM);
+    KV_TRY(kvpr_linear_ws(d.mid, d.ffn, Lw.w2, d.ffn, b, h, d.ffn, &e, 0, d.ws, d.ws_bytes, cs));
+  }
+  return ck(cudaEventRecord(D.ev_done[x.r], cs), "record done");
+}
+
+}  // namespace
+
+}  // namespace kvpr
+
+using namespace kvpr;
+
+extern "C" {
+
+int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle) {
+  if (desc == nullptr || layers == nullptr || handle == nullptr || desc->layers <= 0 || desc->batch <= 0 ||
+      desc->hidden <= 0 || desc->heads <= 0 || desc->nbuf < 2 || desc->chunks < 1 || desc->chunks > 16) {
+    set_error("decoder_create: invalid descriptor (need layers, batch, hidden, heads > 0, nbuf >= 2, 1 <= chunks <= 16)");
+    return KVPR_EINVAL;
+  }
+  Decoder* D = new Decoder();
+  D->d = *desc;
+  D->layer.assign(layers, layers + desc->layers);
+  D->R = desc->layers + desc->nbuf + 2;
+  auto mk = [](std::vector<cudaEvent_t>& v, int n) {
+    v.resize(n);
+    for (auto& e : v)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return false;
+    return true;
+  };
+  if (!mk(D->ev_x, D->R * desc->chunks) || !mk(D->ev_kv, D->R) || !mk(D->ev_qkv, D->R) || !mk(D->ev_d2h, D->R) ||
+      !mk(D->ev_done, D->R)) {
+    set_error("decoder_create: cudaEventCreate failed");
+    delete D;
+    return KVPR_ECUDA;
+  }
+  *handle = D;
+  return KVPR_OK;
+}
+
+int kvpr_decoder_destroy(void* handle) {
+  Decoder* D = static_cast<Decoder*>(handle);
+  if (D == nullptr) return KVPR_OK;
+  for (auto* v : {&D->ev_x, &D->ev_kv, &D->ev_qkv, &D->ev_d2h, &D->ev_done})
+    for (auto e : *v) cudaEventDestroy(e);
+  delete D;
+  return KVPR_OK;
+}
+
+int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, int* out_tokens, float* out_logits) {
+  clear_error();
+  Decoder* D = static_cast<Decoder*>(handle);
+  if (D == nullptr || splits == nullptr || steps <= 0) {
+    set_error("decoder_run: null handle/splits or steps <= 0");
+    return KVPR_EINVAL;
+  }
+  const kvpr_decoder_desc& d = D->d;
+  if (base_len < 1 || base_len + steps > d.capacity) {
+    set_error("cache capacity %d exceeded (%d + %d steps)", d.capacity, base_len, steps);
+    return KVPR_EINVAL;
+  }
+  for (int i = 0; i < steps; ++i) {
+    if (splits[i] < 0 || splits[i] > base_len + i + 1) {
+      set_error("step %d: split %d out of range [0, %d]", i + 1, splits[i], base_len + i + 1);
+      return KVPR_EINVAL;
+    }
+  }
+  cudaStream_t cs = static_cast<cudaStream_t>(d.compute_stream);
+  const int n = steps * d.layers;
+  KV_TRY(issue_h2d(*D, 0, base_len, splits));
+  for (int u = 0; u < n; ++u) {
+    if (u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
+    KV_TRY(compute(*D, u, base_len, splits));
+    if (u % d.layers == d.layers - 1) {
+      const int i = u / d.layers;
+      KV_TRY(head(*D, cs));
+      if (out_tokens)
+        KV_TRY(ck(cudaMemcpyAsync(out_tokens + static_cast<size_t>(i) * d.batch, d.tok, d.batch * sizeof(int),
+                                  cudaMemcpyDeviceToDevice, cs),
+                  "tokens"));
+      if (out_logits)
+        KV_TRY(ck(cudaMemcpyAsync(out_logits + static_cast<size_t>(i) * d.batch * d.vocab, d.logits,
+                                  static_cast<size_t>(d.batch) * d.vocab * sizeof(float), cudaMemcpyDeviceToDevice,
+                                  cs),
+                  "logits"));
+    }
+  }
+  return KVPR_OK;
+}
+
+}  // extern "C"

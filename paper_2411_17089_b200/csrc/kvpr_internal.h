@@ -33,6 +33,7 @@ struct GemmArgs {
 };
 
 int sm_count(int device);
+void clear_error();
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0);

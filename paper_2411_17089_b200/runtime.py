@@ -373,9 +373,50 @@ class KVPRRuntime:
             tr.end(cs, sp)
         self.ev_done[r].record(cs)
 
+    # ------------------------------------------------------- native executor
+    def _native_handle(self):
+        """Descriptor of this runtime's buffers for the C executor (csrc/executor.cu), built once."""
+        if getattr(self, "_native", None) is not None:
+            return self._native
+        import ctypes
+
+        cfg, ptr = self.cfg, (lambda t: t.data_ptr() if t is not None else None)  # noqa: E731
+        layers = (_lib.LayerDesc * cfg.layers)()
+        for j, lw in enumerate(self.w.layers):
+            L = layers[j]
+            for name in ("ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2"):
+                setattr(L, name, getattr(lw, name).data_ptr())
+            L.host_x = self.stores.x[j].data_ptr() if not self.x_resident else None
+            L.host_kv = self.stores.kv[j].data_ptr()
+            L.dev_x = self.x_store[j].data_ptr() if self.x_resident else None
+        d = _lib.DecoderDesc()
+        d.layers, d.batch, d.hidden, d.heads, d.ffn = cfg.layers, self.batch, cfg.hidden, cfg.heads, cfg.ffn
+        d.vocab, d.capacity, d.chunks, d.nbuf, d.x_resident = cfg.vocab, self.capacity, self.chunks, self.nbuf, int(
+            self.x_resident)
+        d.eps = cfg.eps
+        d.embed, d.pos, d.lnf_g, d.lnf_b = ptr(self.w.embed), ptr(self.w.pos), ptr(self.w.lnf_g), ptr(self.w.lnf_b)
+        d.kv_dev, d.x_dev, d.hres = ptr(self.kv_dev), ptr(self.x_dev), ptr(self.hres)
+        d.q, d.attn, d.y, d.mid, d.zf = ptr(self.q), ptr(self.attn), ptr(self.y), ptr(self.mid), ptr(self.zf)
+        d.logits, d.tok, d.ws, d.ws_bytes = ptr(self.logits), ptr(self.tok), ptr(self.ws), self.ws.numel()
+        d.compute_stream, d.h2d_stream, d.d2h_stream = self.cs.cuda_stream, self.hs.cuda_stream, self.ds.cuda_stream
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
+        self._native_keep = (d, layers)
+        self._native = h
+        return h
+
+    def _decode_native(self, splits: list[int], out_tokens: torch.Tensor, logits: torch.Tensor | None) -> None:
+        import ctypes
+
+        arr = (ctypes.c_int * len(splits))(*splits)
+        _lib.check(_lib.load().kvpr_decoder_run(self._native_handle(), self.len, arr, len(splits),
+                                                out_tokens.data_ptr(), logits.data_ptr() if logits is not None else None),
+                   "kvpr_decoder_run")
+        self.launches += len(splits) * (self.cfg.layers * 12 + 3)
+
     def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
                timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None,
-               trace=None) -> torch.Tensor:
+               trace=None, native: bool | None = None) -> torch.Tensor:
         """Enqueue len(splits) decode steps (no host sync); returns device int32 [steps, batch] tokens.
 
         Step i attends over s' = len + i + 1 positions, rebuilding [0, min(l_i, s'-1)) with K1.
@@ -398,6 +439,16 @@ class KVPRRuntime:
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         cs.wait_stream(torch.cuda.current_stream(self.dev))
         self.hs.wait_stream(torch.cuda.current_stream(self.dev))
+        if native is None:  # the C executor covers the plain path; tracing / timing / 4-bit KV stay in Python
+            native = trace is None and timing is None and self.kv_bits is None and self.kernel_timing is None
+        if native:
+            self._decode_native(splits, out_tokens, logits)
+            self.len = base + steps
+            cur = torch.cuda.current_stream(self.dev)
+            cur.wait_stream(cs)
+            cur.wait_stream(self.ds)
+            self._last_logits = logits
+            return out_tokens
         n_units = steps * L
         t_start = torch.cuda.Event(enable_timing=True) if timing is not None else None
         step_marks, layer_marks = [], []
@@ -453,6 +504,9 @@ class KVPRRuntime:
         return getattr(self, "_last_logits", None)
 
     def close(self) -> None:
+        if getattr(self, "_native", None) is not None:
+            _lib.load().kvpr_decoder_destroy(self._native)
+            self._native = None
         self.stores.close()
 
 
