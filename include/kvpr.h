@@ -191,6 +191,14 @@ int kvpr_decoder_destroy(void* handle);
  * out_tokens[i][batch] (device, may be NULL), logits in out_logits[i][batch][vocab] (may be NULL). */
 int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, int* out_tokens, float* out_logits);
 
+/* Bracket every K1 (kind 0) / K2 (kind 1) launch of subsequent runs with CUDA timing events
+ * (enable=0 clears them); stats: launches, mean seconds per launch, mean algorithmic units
+ * (FLOPs for K1, bytes for K2) per launch.  Synchronises on the recorded events. */
+int kvpr_decoder_set_timing(void* handle, int enable);
+int kvpr_decoder_kernel_stats(void* handle, int kind, int* launches, double* mean_seconds, double* mean_units);
+/* Kernel launches (ABI-level) the executor has issued so far. */
+long long kvpr_decoder_launches(void* handle);
+
 #ifdef __cplusplus
 }
 #endif

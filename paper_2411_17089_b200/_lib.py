@@ -44,6 +44,9 @@ EXPORTS = (
     "kvpr_decoder_create",
     "kvpr_decoder_destroy",
     "kvpr_decoder_run",
+    "kvpr_decoder_set_timing",
+    "kvpr_decoder_kernel_stats",
+    "kvpr_decoder_launches",
 )
 
 
@@ -106,6 +109,10 @@ _SIGS = {
     "kvpr_decoder_create": ([ctypes.POINTER(DecoderDesc), ctypes.POINTER(LayerDesc), ctypes.POINTER(_vp)], _i),
     "kvpr_decoder_destroy": ([_vp], _i),
     "kvpr_decoder_run": ([_vp, _i, ctypes.POINTER(_i), _i, _vp, _vp], _i),
+    "kvpr_decoder_set_timing": ([_vp, _i], _i),
+    "kvpr_decoder_kernel_stats": ([_vp, _i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_double)], _i),
+    "kvpr_decoder_launches": ([_vp], _ll),
 }
 
 

@@ -25,12 +25,39 @@ namespace kvpr {
 
 namespace {
 
+struct KTime {
+  int kind;  // 0 = K1 recompute GEMM, 1 = K2 decode attention
+  double units;
+  cudaEvent_t a, b;
+};
+
 struct Decoder {
   kvpr_decoder_desc d;
   std::vector<kvpr_layer_desc> layer;
   int R = 0;
   std::vector<cudaEvent_t> ev_x, ev_kv, ev_qkv, ev_d2h, ev_done;  // ring of R units (ev_x: R*chunks)
+  bool timing = false;  // bracket K1 / K2 launches with timing events (kvpr_decoder_kernel_stats)
+  std::vector<KTime> kt;
+  long long launches = 0;
 };
+
+inline int kt_begin(Decoder& D, int kind, double units, cudaStream_t s, KTime* out) {
+  if (!D.timing) return KVPR_OK;
+  out->kind = kind;
+  out->units = units;
+  if (cudaEventCreate(&out->a) != cudaSuccess || cudaEventCreate(&out->b) != cudaSuccess) {
+    set_error("timing event create failed");
+    return KVPR_ECUDA;
+  }
+  return cudaEventRecord(out->a, s) == cudaSuccess ? KVPR_OK : KVPR_ECUDA;
+}
+
+inline int kt_end(Decoder& D, KTime* t, cudaStream_t s) {
+  if (!D.timing) return KVPR_OK;
+  if (cudaEventRecord(t->b, s) != cudaSuccess) return KVPR_ECUDA;
+  D.kt.push_back(*t);
+  return KVPR_OK;
+}
 
 inline int ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -190,13 +217,21 @@ int compute(Decoder& D, int u, int base, const int* splits) {
     const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
     for (int c = 0; c < nc; ++c) {
       if (!d.x_resident) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_x[x.r * d.chunks + c], 0), "wait X chunk"));
+      KTime t;
+      KV_TRY(kt_begin(D, 0, 4.0 * b * (cb[c][1] - cb[c][0]) * static_cast<double>(h) * h, cs, &t));
       KV_TRY(kvpr_recompute_kv(xd, wkv, bkv, kvd, b, cb[c][0], cb[c][1], h, cs));
+      KV_TRY(kt_end(D, &t, cs));
+      ++D.launches;
     }
   }
   KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_kv[x.r], 0), "wait KV"));
+  KTime t2;
+  KV_TRY(kt_begin(D, 1, 2.0 * b * x.s * static_cast<double>(h) * 2, cs, &t2));
   KV_TRY(decode_attention(static_cast<const __half*>(d.q), kvd, static_cast<__half*>(d.attn),
                           static_cast<float*>(d.ws), d.ws_bytes, b, d.heads, h / d.heads, x.s,
                           static_cast<float>(1.0 / sqrt(static_cast<double>(h / d.heads))), cs));
+  KV_TRY(kt_end(D, &t2, cs));
+  D.launches += 10;  // LN1, qkv, K2 (+ combine), out-proj, LN2, fc1, fc2 (+ split-K reduce)
   {
     kvpr_epilogue e = simple_epi(d.hres, h, b, h, Lw.bo, KVPR_EPI_F32 | KVPR_EPI_ACCUM);
     KV_TRY(kvpr_linear_ws(d.attn, h, Lw.wo, h, b, h, h, &e, 0, d.ws, d.ws_bytes, cs));
@@ -248,9 +283,49 @@ int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* la
   return KVPR_OK;
 }
 
+int kvpr_decoder_set_timing(void* handle, int enable) {
+  Decoder* D = static_cast<Decoder*>(handle);
+  if (D == nullptr) return KVPR_EINVAL;
+  for (auto& t : D->kt) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  D->kt.clear();
+  D->timing = enable != 0;
+  return KVPR_OK;
+}
+
+int kvpr_decoder_kernel_stats(void* handle, int kind, int* launches, double* mean_seconds, double* mean_units) {
+  Decoder* D = static_cast<Decoder*>(handle);
+  if (D == nullptr || launches == nullptr || mean_seconds == nullptr || mean_units == nullptr) return KVPR_EINVAL;
+  int n = 0;
+  double t = 0.0, u = 0.0;
+  for (auto& k : D->kt) {
+    if (k.kind != kind) continue;
+    float ms = 0.f;
+    if (cudaEventSynchronize(k.b) != cudaSuccess || cudaEventElapsedTime(&ms, k.a, k.b) != cudaSuccess) {
+      set_error("kernel_stats: event query failed");
+      return KVPR_ECUDA;
+    }
+    ++n;
+    t += ms * 1e-3;
+    u += k.units;
+  }
+  *launches = n;
+  *mean_seconds = n ? t / n : 0.0;
+  *mean_units = n ? u / n : 0.0;
+  return KVPR_OK;
+}
+
+long long kvpr_decoder_launches(void* handle) {
+  Decoder* D = static_cast<Decoder*>(handle);
+  return D ? D->launches : 0;
+}
+
 int kvpr_decoder_destroy(void* handle) {
   Decoder* D = static_cast<Decoder*>(handle);
   if (D == nullptr) return KVPR_OK;
+  kvpr_decoder_set_timing(handle, 0);
   for (auto* v : {&D->ev_x, &D->ev_kv, &D->ev_qkv, &D->ev_d2h, &D->ev_done})
     for (auto e : *v) cudaEventDestroy(e);
   delete D;
@@ -284,6 +359,7 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
     if (u % d.layers == d.layers - 1) {
       const int i = u / d.layers;
       KV_TRY(head(*D, cs));
+      D->launches += 3;
       if (out_tokens)
         KV_TRY(ck(cudaMemcpyAsync(out_tokens + static_cast<size_t>(i) * d.batch, d.tok, d.batch * sizeof(int),
                                   cudaMemcpyDeviceToDevice, cs),

@@ -180,6 +180,18 @@ class KVPRRuntime:
 
     def kernel_stats(self) -> dict:
         """{name: (launches, mean seconds per launch, mean algorithmic units per launch)} of the timed launches."""
+        if getattr(self, "_native", None) is not None and not self.kernel_timing:
+            import ctypes
+
+            res = {}
+            for kind, name in ((0, "k1"), (1, "k2")):
+                n, t, u = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+                _lib.check(_lib.load().kvpr_decoder_kernel_stats(self._native, kind, ctypes.byref(n), ctypes.byref(t),
+                                                                 ctypes.byref(u)), "kvpr_decoder_kernel_stats")
+                if n.value:
+                    res[name] = (n.value, t.value, u.value)
+            if res:
+                return res
         out = {}
         for name, units, a, e in self.kernel_timing or []:
             e.synchronize()
@@ -409,10 +421,12 @@ class KVPRRuntime:
         import ctypes
 
         arr = (ctypes.c_int * len(splits))(*splits)
-        _lib.check(_lib.load().kvpr_decoder_run(self._native_handle(), self.len, arr, len(splits),
-                                                out_tokens.data_ptr(), logits.data_ptr() if logits is not None else None),
-                   "kvpr_decoder_run")
-        self.launches += len(splits) * (self.cfg.layers * 12 + 3)
+        lib, h = _lib.load(), self._native_handle()
+        before = lib.kvpr_decoder_launches(h)
+        _lib.check(lib.kvpr_decoder_set_timing(h, int(self.kernel_timing is not None)), "kvpr_decoder_set_timing")
+        _lib.check(lib.kvpr_decoder_run(h, self.len, arr, len(splits), out_tokens.data_ptr(),
+                                        logits.data_ptr() if logits is not None else None), "kvpr_decoder_run")
+        self.launches += lib.kvpr_decoder_launches(h) - before
 
     def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
                timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None,
@@ -439,8 +453,8 @@ class KVPRRuntime:
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         cs.wait_stream(torch.cuda.current_stream(self.dev))
         self.hs.wait_stream(torch.cuda.current_stream(self.dev))
-        if native is None:  # the C executor covers the plain path; tracing / timing / 4-bit KV stay in Python
-            native = trace is None and timing is None and self.kv_bits is None and self.kernel_timing is None
+        if native is None:  # the C executor covers the plain path; tracing / per-layer timing / 4-bit KV stay in Python
+            native = trace is None and timing is None and self.kv_bits is None
         if native:
             self._decode_native(splits, out_tokens, logits)
             self.len = base + steps

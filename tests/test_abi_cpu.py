@@ -20,7 +20,7 @@ HEADER = ROOT / "include" / "kvpr.h"
 
 def _declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(kvpr_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^[A-Za-z_][\w \t*]*?\b(kvpr_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol(lib):
