@@ -449,15 +449,17 @@ def run_kvpr(args):
     k1_roof = None
     if "k1" in kstats:
         n, t, fl = kstats["k1"]
-        traffic = None
+        traffic, alg_bytes = None, None
         tp = ROOT / "profiles" / "r01_k1_chunk_ncu.json"
         if tp.exists():  # dram read+write per launch from one ncu --set full capture of a chunk-sized K1
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            rec = json.loads(tp.read_text())
+            traffic, alg_bytes = rec.get("dram_bytes_per_launch"), rec.get("algorithmic_bytes_per_launch")
         k1_roof = {"bound": "tensor", "kernel": "K1 recompute GEMM (tcgen05 cta_group::2, TMA, TMEM)",
                    "achieved": fl / t / 1e12, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                    "frac": fl / t / 1e12 / peaks["bf16_tflops_sustained"], "traffic": traffic,
                    "launches": n, "flops_per_launch": fl, "us_per_launch": t * 1e6,
-                   "algorithmic_bytes_per_launch": None,
+                   "algorithmic_bytes_per_launch": alg_bytes,
+                   "traffic_note": "ncu dram read+write of one chunk-sized launch (profiles/r01_k1_chunk_ncu.json)",
                    "peak_note": "sustained bf16 (kernel timed inside a long step); "
                                 f"burst {peaks['bf16_tflops']} TFLOP/s"}
     if "k2" in kstats:
