@@ -21,6 +21,12 @@
 #include "common.cuh"
 #include "kvpr_internal.h"
 
+#define KV_TRY(x)        \
+  do {                   \
+    int _rc = (x);       \
+    if (_rc) return _rc; \
+  } while (0)
+
 namespace kvpr {
 
 namespace {
@@ -38,17 +44,32 @@ struct Decoder {
   std::vector<cudaEvent_t> ev_x, ev_kv, ev_qkv, ev_d2h, ev_done;  // ring of R units (ev_x: R*chunks)
   bool timing = false;  // bracket K1 / K2 launches with timing events (kvpr_decoder_kernel_stats)
   std::vector<KTime> kt;
+  std::vector<cudaEvent_t> pool;  // timing events, created once and reused across runs
+  size_t pool_used = 0;
   long long launches = 0;
 };
+
+inline int pool_take(Decoder& D, cudaEvent_t* e) {
+  if (D.pool_used == D.pool.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t x;
+      if (cudaEventCreate(&x) != cudaSuccess) {
+        set_error("timing event create failed");
+        return KVPR_ECUDA;
+      }
+      D.pool.push_back(x);
+    }
+  }
+  *e = D.pool[D.pool_used++];
+  return KVPR_OK;
+}
 
 inline int kt_begin(Decoder& D, int kind, double units, cudaStream_t s, KTime* out) {
   if (!D.timing) return KVPR_OK;
   out->kind = kind;
   out->units = units;
-  if (cudaEventCreate(&out->a) != cudaSuccess || cudaEventCreate(&out->b) != cudaSuccess) {
-    set_error("timing event create failed");
-    return KVPR_ECUDA;
-  }
+  KV_TRY(pool_take(D, &out->a));
+  KV_TRY(pool_take(D, &out->b));
   return cudaEventRecord(out->a, s) == cudaSuccess ? KVPR_OK : KVPR_ECUDA;
 }
 
@@ -67,11 +88,6 @@ inline int ck(cudaError_t e, const char* what) {
   return KVPR_OK;
 }
 
-#define KV_TRY(x)              \
-  do {                         \
-    int _rc = (x);             \
-    if (_rc) return _rc;       \
-  } while (0)
 
 // chunk_bounds() of runtime.py: <= chunks contiguous ranges of >= min_rows positions when possible
 inline int chunk_bounds(int n, int chunks, int (*out)[2], int min_rows = 64) {
@@ -286,11 +302,8 @@ int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* la
 int kvpr_decoder_set_timing(void* handle, int enable) {
   Decoder* D = static_cast<Decoder*>(handle);
   if (D == nullptr) return KVPR_EINVAL;
-  for (auto& t : D->kt) {
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
-  }
-  D->kt.clear();
+  D->kt.clear();  // pooled events are reused by the next timed run
+  D->pool_used = 0;
   D->timing = enable != 0;
   return KVPR_OK;
 }
@@ -326,6 +339,7 @@ int kvpr_decoder_destroy(void* handle) {
   Decoder* D = static_cast<Decoder*>(handle);
   if (D == nullptr) return KVPR_OK;
   kvpr_decoder_set_timing(handle, 0);
+  for (auto e : D->pool) cudaEventDestroy(e);
   for (auto* v : {&D->ev_x, &D->ev_kv, &D->ev_qkv, &D->ev_d2h, &D->ev_done})
     for (auto e : *v) cudaEventDestroy(e);
   delete D;
