@@ -157,6 +157,15 @@ int kvpr_kv4_quantize(const void* pages, void* qpages, int batch, int hidden, in
 int kvpr_kv4_dequantize(const void* qpages, void* pages, int batch, int hidden, int pos_begin, int pos_end,
                         void* stream);
 
+/* K2 over a mixed cache ("dequant fused into the staging read in K2"):
+ * as kvpr_decode_attention, but positions [q_lo, q_hi) are read from 4-bit compressed pages
+ * `qpages` (layout above, indexed from position 0) and dequantised in registers with the exact
+ * arithmetic of kvpr_kv4_dequantize — identical bits to dequantize-then-K2, without writing the
+ * fp16 tail to HBM and reading it back.  Other positions come from the fp16 pages. */
+int kvpr_decode_attention_kv4(const void* q, const void* kv_pages, const void* qpages, int q_lo, int q_hi, void* out,
+                              void* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
+                              void* stream);
+
 /* ---------------------------------------------------------------------------
  * Native decode executor: the per-layer issue loop of the Python runtime
  * (paper_2411_17089_b200/runtime.py, realising pipesim graph.py:232-347) in C,
@@ -183,6 +192,7 @@ typedef struct kvpr_decoder_desc {
   void* ws;
   size_t ws_bytes;
   void *compute_stream, *h2d_stream, *d2h_stream;
+  int chunk_rows; /* minimum positions per X chunk / K1 launch (runtime.KVPRRuntime.chunk_rows) */
 } kvpr_decoder_desc;
 
 int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);
@@ -196,6 +206,11 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
  * (FLOPs for K1, bytes for K2) per launch.  Synchronises on the recorded events. */
 int kvpr_decoder_set_timing(void* handle, int enable);
 int kvpr_decoder_kernel_stats(void* handle, int kind, int* launches, double* mean_seconds, double* mean_units);
+/* Timeline of the last timed run, in runtime.DecodeTiming's convention: layer_ms[i*layers+j] =
+ * compute-stream time from the previous layer end (or step i's start) to the end of layer j of
+ * step i; step_ms[i] = time from the previous step's end (or the run start) to the end of step
+ * i's head.  Returns the number of steps (0 if the last run was untimed), or -KVPR_E* on error. */
+int kvpr_decoder_timeline(void* handle, float* layer_ms, int layer_cap, float* step_ms, int step_cap);
 /* Kernel launches (ABI-level) the executor has issued so far. */
 long long kvpr_decoder_launches(void* handle);
 

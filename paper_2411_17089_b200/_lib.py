@@ -41,11 +41,13 @@ EXPORTS = (
     "kvpr_kv4_page_bytes",
     "kvpr_kv4_quantize",
     "kvpr_kv4_dequantize",
+    "kvpr_decode_attention_kv4",
     "kvpr_decoder_create",
     "kvpr_decoder_destroy",
     "kvpr_decoder_run",
     "kvpr_decoder_set_timing",
     "kvpr_decoder_kernel_stats",
+    "kvpr_decoder_timeline",
     "kvpr_decoder_launches",
 )
 
@@ -79,7 +81,7 @@ class DecoderDesc(ctypes.Structure):
         ("eps", ctypes.c_float)] + [(n, ctypes.c_void_p) for n in (
             "embed", "pos", "lnf_g", "lnf_b", "kv_dev", "x_dev", "hres", "q", "attn", "y", "mid", "zf", "logits",
             "tok", "ws")] + [("ws_bytes", ctypes.c_size_t)] + [(n, ctypes.c_void_p) for n in (
-                "compute_stream", "h2d_stream", "d2h_stream")]
+                "compute_stream", "h2d_stream", "d2h_stream")] + [("chunk_rows", ctypes.c_int)]
 
 
 _lib: ctypes.CDLL | None = None
@@ -106,12 +108,14 @@ _SIGS = {
     "kvpr_kv4_page_bytes": ([_i, _i], _sz),
     "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
+    "kvpr_decode_attention_kv4": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
     "kvpr_decoder_create": ([ctypes.POINTER(DecoderDesc), ctypes.POINTER(LayerDesc), ctypes.POINTER(_vp)], _i),
     "kvpr_decoder_destroy": ([_vp], _i),
     "kvpr_decoder_run": ([_vp, _i, ctypes.POINTER(_i), _i, _vp, _vp], _i),
     "kvpr_decoder_set_timing": ([_vp, _i], _i),
     "kvpr_decoder_kernel_stats": ([_vp, _i, ctypes.POINTER(_i), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_double)], _i),
+    "kvpr_decoder_timeline": ([_vp, ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(ctypes.c_float), _i], _i),
     "kvpr_decoder_launches": ([_vp], _ll),
 }
 

@@ -149,6 +149,16 @@ int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* 
                           seq_len, scale, static_cast<cudaStream_t>(stream));
 }
 
+int kvpr_decode_attention_kv4(const void* q, const void* kv_pages, const void* qpages, int q_lo, int q_hi, void* out,
+                              void* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
+                              void* stream) {
+  g_err[0] = 0;
+  return decode_attention_q4(static_cast<const __half*>(q), static_cast<const __half*>(kv_pages),
+                             static_cast<const uint8_t*>(qpages), q_lo, q_hi, static_cast<__half*>(out),
+                             static_cast<float*>(ws), ws_bytes, batch, heads, head_dim, seq_len, scale,
+                             static_cast<cudaStream_t>(stream));
+}
+
 int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,
                            int seq_len, float scale, void* stream) {
   g_err[0] = 0;

@@ -74,10 +74,43 @@ struct Softmax8 {
 // scale*log2e so scores come out in the exp2 domain.
 // `first` must be warp-uniform (the shuffles below need the whole warp in every
 // trip); lane group `grp` owns positions first + grp + u*step + trip*U*step.
-template <int D, int U>
+// Positions [lo, hi) of the sweep read 4-bit compressed pages (kvquant.cu layout) instead of the
+// fp16 page buffer: the transferred tail of the kv_bits=4 path, dequantised in registers with the
+// exact arithmetic of kv4_dequantize_kernel (x^ = half(min + q*scale), no FMA), so K2 sees the
+// same fp16 values as after a separate dequantize pass — without writing and re-reading them.
+struct Q4Src {
+  const uint8_t* base;  // compressed page of position 0
+  long long page_bytes;
+  long long ck, cv, pk, pv;  // this lane's K/V code and (min, scale) byte offsets within a page
+  int lo, hi;
+};
+
+__device__ __forceinline__ uint32_t ld_stream32(const uint8_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 deq8(uint32_t codes, uint32_t prm) {
+  __half2 mp = *reinterpret_cast<const __half2*>(&prm);
+  const float2 f = __half22float2(mp);
+  uint4 out;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t byte = (codes >> (8 * i)) & 0xffu;
+    const float a = __fadd_rn(f.x, __fmul_rn(static_cast<float>(byte & 15u), f.y));
+    const float b = __fadd_rn(f.x, __fmul_rn(static_cast<float>(byte >> 4), f.y));
+    __half2 h = __floats2half2_rn(a, b);
+    o[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return out;
+}
+
+template <int D, int U, bool Q4 = false>
 __device__ __forceinline__ void sweep(const __half* __restrict__ kbase, long long page_stride, long long v_off,
                                       int first, int end, int step, int grp, const float (&q8)[8], int glane,
-                                      Softmax8& st) {
+                                      Softmax8& st, const Q4Src* qs = nullptr) {
   constexpr int LPP = D / 8;
   for (int pb = first; pb < end; pb += step * U) {
     const int p0 = pb + grp;
@@ -88,9 +121,15 @@ __device__ __forceinline__ void sweep(const __half* __restrict__ kbase, long lon
       kr[u] = make_uint4(0, 0, 0, 0);
       vr[u] = make_uint4(0, 0, 0, 0);
       if (p < end) {
-        const __half* kp = kbase + (long long)p * page_stride + glane * 8;
-        kr[u] = ld_stream(kp);
-        vr[u] = ld_stream(kp + v_off);
+        if (Q4 && p >= qs->lo && p < qs->hi) {
+          const uint8_t* pg = qs->base + (long long)p * qs->page_bytes;
+          kr[u] = deq8(ld_stream32(pg + qs->ck), __ldg(reinterpret_cast<const unsigned int*>(pg + qs->pk)));
+          vr[u] = deq8(ld_stream32(pg + qs->cv), __ldg(reinterpret_cast<const unsigned int*>(pg + qs->pv)));
+        } else {
+          const __half* kp = kbase + (long long)p * page_stride + glane * 8;
+          kr[u] = ld_stream(kp);
+          vr[u] = ld_stream(kp + v_off);
+        }
       }
     }
     float s[U];
@@ -148,11 +187,12 @@ __device__ __forceinline__ void merge_in_warp(Softmax8& st) {
   }
 }
 
-// grid: (batch*heads, splits), block: 128 threads.
-template <int D>
+// grid: (batch*heads, splits), block: 128 threads.  Q4: positions [q4.lo, q4.hi) come from
+// compressed pages (the caller passes base/page_bytes/lo/hi; per-lane offsets are set here).
+template <int D, bool Q4>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
                                                           __half* __restrict__ out, float* __restrict__ ws, int batch,
-                                                          int heads, int seq_len, int chunk, float qscale) {
+                                                          int heads, int seq_len, int chunk, float qscale, Q4Src q4) {
   constexpr int LPP = D / 8;
   constexpr int PPW = 32 / LPP;  // positions per warp step
   constexpr int NW = 4;
@@ -175,7 +215,15 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
   const __half* kbase = kv + (long long)b * hidden + hd * D;
   Softmax8 st;
   st.init();
-  sweep<D, 4>(kbase, page_stride, (long long)batch * hidden, p_lo + warp * PPW, p_hi, NW * PPW, grp, q8, glane, st);
+  if constexpr (Q4) {
+    const long long e = (long long)b * hidden + hd * D + glane * 8;  // element index of this lane's K slice
+    q4.ck = e / 2;
+    q4.cv = q4.ck + (long long)batch * hidden / 2;
+    q4.pk = (long long)batch * hidden + (e / 64) * 4;  // params follow the 2*batch*hidden/2 code bytes
+    q4.pv = q4.pk + ((long long)batch * hidden / 64) * 4;
+  }
+  sweep<D, 4, Q4>(kbase, page_stride, (long long)batch * hidden, p_lo + warp * PPW, p_hi, NW * PPW, grp, q8, glane, st,
+                  &q4);
   merge_in_warp<LPP>(st);
 
   __shared__ float sm_m[NW], sm_l[NW];
@@ -269,6 +317,19 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(const __half* __restr
 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch, int heads,
                      int head_dim, int seq_len, float scale, cudaStream_t stream) {
+  return decode_attention_q4(q, kv, nullptr, 0, 0, out, ws, ws_bytes, batch, heads, head_dim, seq_len, scale, stream);
+}
+
+int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages, int q_lo, int q_hi, __half* out,
+                        float* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
+                        cudaStream_t stream) {
+  const bool use_q4 = q_hi > q_lo;
+  if (use_q4 && (qpages == nullptr || q_lo < 0 || q_hi > seq_len || (heads * head_dim) % 64 != 0 ||
+                 (reinterpret_cast<uintptr_t>(qpages) & 3))) {
+    set_error("decode_attention_kv4: need 4-byte aligned qpages, 0 <= q_lo <= q_hi <= seq_len, hidden %% 64 == 0 "
+              "(got [%d,%d) of %d)", q_lo, q_hi, seq_len);
+    return KVPR_EINVAL;
+  }
   if (seq_len <= 0) {
     set_error("cannot attend over an empty cache (seq_len=%d)", seq_len);
     return KVPR_EINVAL;
@@ -297,10 +358,24 @@ int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, 
   splits = (seq_len + chunk - 1) / chunk;
   const float qscale = scale * kLog2e;
   dim3 grid(bh, splits);
-  if (head_dim == 128)
-    decode_attn_kernel<128><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale);
-  else
-    decode_attn_kernel<64><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale);
+  Q4Src q4{};
+  if (use_q4) {
+    q4.base = qpages;
+    q4.page_bytes = (long long)kv4_page_bytes(batch, heads * head_dim);
+    q4.lo = q_lo;
+    q4.hi = q_hi;
+  }
+  if (head_dim == 128) {
+    if (use_q4)
+      decode_attn_kernel<128, true><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+    else
+      decode_attn_kernel<128, false><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+  } else {
+    if (use_q4)
+      decode_attn_kernel<64, true><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+    else
+      decode_attn_kernel<64, false><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+  }
   int rc = check_launch("decode_attention");
   if (rc || splits == 1) return rc;
   if (head_dim == 128)

@@ -46,6 +46,9 @@ struct Decoder {
   std::vector<KTime> kt;
   std::vector<cudaEvent_t> pool;  // timing events, created once and reused across runs
   size_t pool_used = 0;
+  cudaEvent_t t0 = nullptr;                          // run start (timing only)
+  std::vector<cudaEvent_t> layer_marks, step_marks;  // after each layer / after each step's head
+
   long long launches = 0;
 };
 
@@ -80,6 +83,16 @@ inline int kt_end(Decoder& D, KTime* t, cudaStream_t s) {
   return KVPR_OK;
 }
 
+// timing only: one event on the compute stream, appended to `marks`
+inline int mark(Decoder& D, std::vector<cudaEvent_t>& marks, cudaStream_t s) {
+  if (!D.timing) return KVPR_OK;
+  cudaEvent_t e;
+  KV_TRY(pool_take(D, &e));
+  if (cudaEventRecord(e, s) != cudaSuccess) return KVPR_ECUDA;
+  marks.push_back(e);
+  return KVPR_OK;
+}
+
 inline int ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     set_error("%s: %s", what, cudaGetErrorString(e));
@@ -105,6 +118,8 @@ inline int chunk_bounds(int n, int chunks, int (*out)[2], int min_rows = 64) {
   }
   return c;
 }
+
+inline int chunk_rows(const kvpr_decoder_desc& d) { return d.chunk_rows > 0 ? d.chunk_rows : 64; }
 
 kvpr_epilogue simple_epi(void* out, long long ld, int M, int N, const void* bias, int flags) {
   kvpr_epilogue e;
@@ -151,7 +166,7 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   char* kvd = static_cast<char*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * row;
   if (!d.x_resident) {
     int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.chunks, cb);
+    const int nc = chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d));
     for (int c = 0; c < nc; ++c) {
       KV_TRY(ck(cudaMemcpyAsync(xd + cb[c][0] * row, static_cast<const char*>(Lw.host_x) + cb[c][0] * row,
                                 (cb[c][1] - cb[c][0]) * row, cudaMemcpyDefault, hs),
@@ -228,7 +243,7 @@ int compute(Decoder& D, int u, int base, const int* splits) {
   // K1 per landed chunk (one launch when X is resident)
   {
     int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb);
+    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb, chunk_rows(d));
     const __half* wkv = static_cast<const __half*>(Lw.wqkv) + static_cast<size_t>(h) * h;
     const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
     for (int c = 0; c < nc; ++c) {
@@ -303,6 +318,9 @@ int kvpr_decoder_set_timing(void* handle, int enable) {
   Decoder* D = static_cast<Decoder*>(handle);
   if (D == nullptr) return KVPR_EINVAL;
   D->kt.clear();  // pooled events are reused by the next timed run
+  D->layer_marks.clear();
+  D->step_marks.clear();
+  D->t0 = nullptr;
   D->pool_used = 0;
   D->timing = enable != 0;
   return KVPR_OK;
@@ -328,6 +346,41 @@ int kvpr_decoder_kernel_stats(void* handle, int kind, int* launches, double* mea
   *mean_seconds = n ? t / n : 0.0;
   *mean_units = n ? u / n : 0.0;
   return KVPR_OK;
+}
+
+int kvpr_decoder_timeline(void* handle, float* layer_ms, int layer_cap, float* step_ms, int step_cap) {
+  Decoder* D = static_cast<Decoder*>(handle);
+  if (D == nullptr || (layer_cap > 0 && layer_ms == nullptr) || (step_cap > 0 && step_ms == nullptr)) {
+    set_error("decoder_timeline: null handle or output");
+    return -KVPR_EINVAL;
+  }
+  if (D->t0 == nullptr) return 0;
+  const int L = D->d.layers;
+  const int steps = static_cast<int>(D->step_marks.size());
+  if (static_cast<int>(D->layer_marks.size()) != steps * L || layer_cap < steps * L || step_cap < steps) {
+    set_error("decoder_timeline: %d steps x %d layers do not fit (caps %d, %d)", steps, L, layer_cap, step_cap);
+    return -KVPR_EINVAL;
+  }
+  auto el = [](cudaEvent_t a, cudaEvent_t b, float* out) {
+    return cudaEventSynchronize(b) == cudaSuccess && cudaEventElapsedTime(out, a, b) == cudaSuccess;
+  };
+  cudaEvent_t prev = D->t0;  // same convention as runtime.KVPRRuntime.decode(timing=...)
+  for (int i = 0; i < steps; ++i) {
+    if (!el(prev, D->step_marks[i], &step_ms[i])) goto fail;
+    prev = D->step_marks[i];
+  }
+  prev = D->t0;
+  for (int i = 0; i < steps; ++i) {
+    for (int j = 0; j < L; ++j) {
+      if (!el(prev, D->layer_marks[i * L + j], &layer_ms[i * L + j])) goto fail;
+      prev = D->layer_marks[i * L + j];
+    }
+    prev = D->step_marks[i];
+  }
+  return steps;
+fail:
+  set_error("decoder_timeline: event query failed");
+  return -KVPR_ECUDA;
 }
 
 long long kvpr_decoder_launches(void* handle) {
@@ -366,10 +419,17 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
   }
   cudaStream_t cs = static_cast<cudaStream_t>(d.compute_stream);
   const int n = steps * d.layers;
+  if (D->timing) {
+    D->layer_marks.clear();
+    D->step_marks.clear();
+    KV_TRY(pool_take(*D, &D->t0));
+    KV_TRY(ck(cudaEventRecord(D->t0, cs), "record start"));
+  }
   KV_TRY(issue_h2d(*D, 0, base_len, splits));
   for (int u = 0; u < n; ++u) {
     if (u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
     KV_TRY(compute(*D, u, base_len, splits));
+    KV_TRY(mark(*D, D->layer_marks, cs));
     if (u % d.layers == d.layers - 1) {
       const int i = u / d.layers;
       KV_TRY(head(*D, cs));
@@ -383,6 +443,7 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
                                   static_cast<size_t>(d.batch) * d.vocab * sizeof(float), cudaMemcpyDeviceToDevice,
                                   cs),
                   "logits"));
+      KV_TRY(mark(*D, D->step_marks, cs));
     }
   }
   return KVPR_OK;

@@ -41,6 +41,10 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch,
                      int heads, int head_dim, int seq_len, float scale, cudaStream_t stream);
 
+int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages, int q_lo, int q_hi, __half* out,
+                        float* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
+                        cudaStream_t stream);
+
 int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim,
                       int seq_len, float scale, cudaStream_t stream);
 

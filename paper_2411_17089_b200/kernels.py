@@ -96,6 +96,26 @@ def decode_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor,
     return out
 
 
+def decode_attention_kv4(q: torch.Tensor, kv_pages: torch.Tensor, qpages: torch.Tensor, q_lo: int, q_hi: int,
+                         out: torch.Tensor, ws: torch.Tensor | None, batch: int, heads: int, head_dim: int,
+                         seq_len: int, scale: float | None = None, stream=None) -> torch.Tensor:
+    """K2 with positions [q_lo, q_hi) read from 4-bit compressed pages (dequantised in registers,
+    same bits as kv4_dequantize followed by decode_attention)."""
+    _need(q, torch.float16, "q")
+    _need(kv_pages, torch.float16, "kv_pages")
+    _need(qpages, torch.uint8, "qpages")
+    _need(out, torch.float16, "out")
+    if scale is None:
+        scale = 1.0 / math.sqrt(head_dim)
+    ws_ptr, ws_bytes = (ws.data_ptr(), ws.numel() * ws.element_size()) if ws is not None else (None, 0)
+    _lib.call(
+        "kvpr_decode_attention_kv4",
+        q.data_ptr(), kv_pages.data_ptr(), qpages.data_ptr(), q_lo, q_hi, out.data_ptr(), ws_ptr, ws_bytes,
+        batch, heads, head_dim, seq_len, float(scale), _stream(stream),
+    )
+    return out
+
+
 def prefill_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor, batch: int, heads: int,
                       head_dim: int, seq_len: int, scale: float | None = None, stream=None) -> torch.Tensor:
     if scale is None:

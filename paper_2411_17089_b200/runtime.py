@@ -106,7 +106,7 @@ class KVPRRuntime:
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
                  chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None,
-                 x_resident: bool = False):
+                 x_resident: bool = False, chunk_rows: int | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
 
         x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
@@ -121,6 +121,9 @@ class KVPRRuntime:
         self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
         self.dev = torch.device(device) if device is not None else weights.embed.device
         self.chunks, self.nbuf = chunks, nbuf
+        # a K1 chunk carries >= 4 MiB of X (>= 64 positions): small models issue one X copy + one K1
+        # per layer instead of paying per-call latency `chunks` times (tests lower it to cover chunking)
+        self.chunk_rows = chunk_rows or max(64, -(-(4 << 20) // (batch * cfg.hidden * 2)))
         _lib.load()
         h, b = cfg.hidden, batch
         with torch.cuda.device(self.dev):
@@ -303,7 +306,7 @@ class KVPRRuntime:
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         row = b * h * 2
         tr = self._trace
-        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks)):
+        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows)):
             sp = tr.begin(hs, "load_activation_recompute", i + 1, j + 1, f"c{c}") if tr else None
             _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
             if sp:
@@ -354,7 +357,7 @@ class KVPRRuntime:
             tr.end(ds, sp)
         self.ev_d2h[r].record(ds)
         # K1: rebuild K,V[0:l) chunk by chunk as X lands (one launch when X is resident)
-        for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks)):
+        for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks, self.chunk_rows)):
             if not self.x_resident:
                 cs.wait_event(self.ev_x[r][c])
             sp = tr.begin(cs, "compute_recompute", I, J, f"c{c}") if tr else None
@@ -365,13 +368,15 @@ class KVPRRuntime:
                 tr.end(cs, sp)
             self._k()
         cs.wait_event(self.ev_kv[r])
-        if self.kv_bits == 4 and s - 1 > lp:  # expand the transferred 4-bit tail into fp16 pages
-            kernels.kv4_dequantize(self.kvq_dev[buf], kvd, b, lp, s - 1, stream=cs)
-            self._k()
-        # K2 over the merged pages [0, s') in place, then W_O + residual
+        # K2 over the merged pages [0, s') in place (4-bit tail [lp, s'-1) dequantised inside K2), then W_O
         sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
-        kt = self._ktimer("k2", 2 * b * s * h * 2, cs)
-        kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
+        if self.kv_bits == 4 and s - 1 > lp:
+            kt = self._ktimer("k2", 2 * b * (lp + 1) * h * 2 + (s - 1 - lp) * self.qbytes, cs)
+            kernels.decode_attention_kv4(self.q, kvd, self.kvq_dev[buf], lp, s - 1, self.attn, self.ws, b,
+                                         cfg.heads, cfg.head_dim, s, stream=cs)
+        else:
+            kt = self._ktimer("k2", 2 * b * s * h * 2, cs)
+            kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
         self._ktimer_end(kt, cs)
         self._k(2)
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
@@ -411,22 +416,33 @@ class KVPRRuntime:
         d.q, d.attn, d.y, d.mid, d.zf = ptr(self.q), ptr(self.attn), ptr(self.y), ptr(self.mid), ptr(self.zf)
         d.logits, d.tok, d.ws, d.ws_bytes = ptr(self.logits), ptr(self.tok), ptr(self.ws), self.ws.numel()
         d.compute_stream, d.h2d_stream, d.d2h_stream = self.cs.cuda_stream, self.hs.cuda_stream, self.ds.cuda_stream
+        d.chunk_rows = self.chunk_rows
         h = ctypes.c_void_p()
         _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
         self._native_keep = (d, layers)
         self._native = h
         return h
 
-    def _decode_native(self, splits: list[int], out_tokens: torch.Tensor, logits: torch.Tensor | None) -> None:
+    def _decode_native(self, splits: list[int], out_tokens: torch.Tensor, logits: torch.Tensor | None,
+                       timing: DecodeTiming | None = None) -> None:
         import ctypes
 
         arr = (ctypes.c_int * len(splits))(*splits)
         lib, h = _lib.load(), self._native_handle()
         before = lib.kvpr_decoder_launches(h)
-        _lib.check(lib.kvpr_decoder_set_timing(h, int(self.kernel_timing is not None)), "kvpr_decoder_set_timing")
+        timed = self.kernel_timing is not None or timing is not None
+        _lib.check(lib.kvpr_decoder_set_timing(h, int(timed)), "kvpr_decoder_set_timing")
         _lib.check(lib.kvpr_decoder_run(h, self.len, arr, len(splits), out_tokens.data_ptr(),
                                         logits.data_ptr() if logits is not None else None), "kvpr_decoder_run")
         self.launches += lib.kvpr_decoder_launches(h) - before
+        if timing is not None:
+            L, n = self.cfg.layers, len(splits)
+            lay, stp = (ctypes.c_float * (n * L))(), (ctypes.c_float * n)()
+            got = lib.kvpr_decoder_timeline(h, lay, n * L, stp, n)
+            if got < 0:
+                _lib.check(-got, "kvpr_decoder_timeline")
+            timing.step_ms.extend(stp[:got])
+            timing.layer_ms.extend([list(lay[i * L:(i + 1) * L]) for i in range(got)])
 
     def decode(self, splits: list[int], tokens: torch.Tensor | None = None, keep_logits: bool = False,
                timing: DecodeTiming | None = None, out_tokens: torch.Tensor | None = None,
@@ -453,10 +469,10 @@ class KVPRRuntime:
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         cs.wait_stream(torch.cuda.current_stream(self.dev))
         self.hs.wait_stream(torch.cuda.current_stream(self.dev))
-        if native is None:  # the C executor covers the plain path; tracing / per-layer timing / 4-bit KV stay in Python
-            native = trace is None and timing is None and self.kv_bits is None
+        if native is None:  # the C executor covers the plain path (timed or not); tracing / 4-bit KV stay in Python
+            native = trace is None and self.kv_bits is None
         if native:
-            self._decode_native(splits, out_tokens, logits)
+            self._decode_native(splits, out_tokens, logits, timing)
             self.len = base + steps
             cur = torch.cuda.current_stream(self.dev)
             cur.wait_stream(cs)

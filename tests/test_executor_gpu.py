@@ -23,7 +23,7 @@ def test_native_equals_python_loop_bitwise(x_resident):
     prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(32))
     outs = []
     for native in (False, True):
-        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident)
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, chunk_rows=64)
         first = rt.prefill(prompt)
         toks = rt.decode(splits, tokens=first, keep_logits=True, native=native)
         torch.cuda.synchronize()
@@ -53,3 +53,29 @@ def test_native_loop_cuts_host_time():
         t[native] = time.perf_counter() - t0
     rt.close()
     assert t[True] < t[False], t
+
+
+def test_native_timeline_matches_python_convention():
+    """decode(timing=...) runs through the executor and fills DecodeTiming with the Python loop's
+    shape (steps x layers), positive times whose per-step sums track the step times."""
+    from paper_2411_17089_b200.runtime import DecodeTiming
+
+    cfg = OPTConfig(hidden=512, layers=3, heads=8, ffn=2048, vocab=2048, max_pos=512)
+    b, S0, splits = 2, 100, [50, 0, 102, 7]
+    w = OPTWeights.random(cfg, seed=5, device="cuda", std=0.1, emb_std=0.1)
+    prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(6))
+    rt = KVPRRuntime(w, b, S0 + len(splits) + 1)
+    first = rt.prefill(prompt)
+    tims, toks = [], []
+    for native in (False, True):
+        rt.reset(S0)
+        tim = DecodeTiming()
+        toks.append(rt.decode(splits, tokens=first, timing=tim, native=native).cpu())
+        tims.append(tim)
+    rt.close()
+    assert torch.equal(toks[0], toks[1])
+    nat = tims[1]
+    assert len(nat.step_ms) == len(splits) and [len(r) for r in nat.layer_ms] == [cfg.layers] * len(splits)
+    assert all(x > 0 for r in nat.layer_ms for x in r)
+    for row, st in zip(nat.layer_ms, nat.step_ms):
+        assert sum(row) <= st + 1e-3  # the head closes each step after its last layer

@@ -264,6 +264,33 @@ def test_kv4_codec_bitwise_vs_oracle(dev, P, batch, hidden):
     assert err <= (x.float().max() - x.float().min()).item() / 15 / 2 + 1e-2
 
 
+@pytest.mark.parametrize("batch,heads,d,seq,lo,hi", [
+    (4, 12, 64, 257, 200, 256), (32, 32, 128, 1025, 0, 1024), (3, 8, 128, 300, 17, 299), (2, 4, 64, 70, 5, 5),
+    (1, 2, 128, 9, 0, 9)])
+def test_decode_attention_kv4_fused_bitwise(dev, batch, heads, d, seq, lo, hi):
+    """K2 reading [lo, hi) from 4-bit pages == kv4_dequantize into the fp16 pages, then K2 — bit for bit
+    (the fused read uses the dequantize kernel's arithmetic)."""
+    h = heads * d
+    g = torch.Generator().manual_seed(seq + lo)
+    pages = (torch.randn(seq + 1, 2, batch, h, generator=g)).half().to(dev)
+    q = torch.randn(batch, h, generator=g).half().to(dev)
+    qp = torch.zeros(seq + 1, kernels.kv4_page_bytes(batch, h), dtype=torch.uint8, device=dev)
+    kernels.kv4_quantize(pages, qp, batch, 0, seq)
+    ws = torch.empty(8 << 20, dtype=torch.uint8, device=dev)
+    mixed = pages.clone()
+    mixed[lo:hi] = float("nan")  # the fused path must not read the fp16 tail
+    fused = torch.empty(batch, h, dtype=torch.float16, device=dev)
+    kernels.decode_attention_kv4(q, mixed, qp, lo, hi, fused, ws, batch, heads, d, seq)
+    ref_pages = pages.clone()
+    kernels.kv4_dequantize(qp, ref_pages, batch, lo, hi)
+    ref = torch.empty_like(fused)
+    kernels.decode_attention(q, ref_pages, ref, ws, batch, heads, d, seq)
+    torch.cuda.synchronize()
+    assert torch.equal(fused, ref)
+    with pytest.raises(ValueError):
+        kernels.decode_attention_kv4(q, mixed, qp, 0, seq + 1, fused, ws, batch, heads, d, seq)
+
+
 @pytest.mark.parametrize("M,N,K", [(32, 4096, 16384), (32, 4096, 4096), (7, 768, 3072), (128, 1024, 8192)])
 def test_split_k_decode_gemm(dev, M, N, K):
     """Single-row-block GEMMs with a workspace split K across CTAs; partials reduced in slice order:

@@ -54,3 +54,44 @@ for _ in range(10):  # GPU kept busy (a long GEMM) right before K2
 res["after_busy_gemm_us"] = sorted(spin)[5]
 res["bytes"] = 2 * b * s * h * 2
 print(json.dumps(res))
+
+# K2 while a copy engine streams into / out of HBM on another stream (as the next layer's
+# X chunks and KV tail do in the step).
+big = torch.empty(1 << 30, dtype=torch.uint8)
+torch.cuda.cudart().cudaHostRegister(big.data_ptr(), big.numel(), 0)
+dst = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+side = torch.cuda.Stream()
+for name, d2h in (("concurrent_h2d_us", False), ("concurrent_d2h_us", True)):
+    conc = []
+    for _ in range(10):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            if d2h:
+                big.copy_(dst, non_blocking=True)
+            else:
+                dst.copy_(big, non_blocking=True)
+        time.sleep(0.002)
+        conc.append(timed(k2))
+    torch.cuda.synchronize()
+    res[name] = sorted(conc)[5]
+print(json.dumps(res))
+
+# Is the slowdown K2's access pattern or any HBM-streaming kernel?  A 512 MiB device-to-device
+# copy by SM threads (torch copy kernel), alone and with the same concurrent H2D.
+src2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+dst2 = torch.empty_like(src2)
+smcopy = lambda: dst2.copy_(src2)  # noqa: E731
+for _ in range(3):
+    smcopy()
+res["sm_copy_alone_us"] = sorted(timed(smcopy) for _ in range(10))[5]
+conc = []
+for _ in range(10):
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        dst.copy_(big, non_blocking=True)
+    time.sleep(0.002)
+    conc.append(timed(smcopy))
+torch.cuda.synchronize()
+res["sm_copy_concurrent_h2d_us"] = sorted(conc)[5]
+res["sm_copy_bytes"] = 2 * src2.numel()
+print(json.dumps(res))
