@@ -21,8 +21,12 @@ roofline  the per-layer overlap roofline of the north star,
           T_roof(l) = max(H2D bytes / BW_h2d_measured, recompute FLOPs / F_peak):
           achieved = algorithmic H2D bytes per layer / measured layer time.
           Kernel rooflines (K1 tensor, K2 HBM) are measured in the same run.
-Multi-GPU (torchrun): batch-partitioned replicas, one per GPU, each with its
-own host stores and PCIe link; no data-path collective (scaling "weak").
+Multi-GPU (torchrun): the global batch (--batch, default 32) is partitioned
+over the ranks (BASELINE config 3: b/G sequences per GPU), each rank with its
+own host stores, PCIe link, profile and plan; no data-path collective.  Total
+work is fixed as N grows (scaling "strong"), so the pinned host stores of all
+ranks together stay at one batch's size however many GPUs run; the decode is
+PCIe-bound, so tok/s per GPU is nearly independent of the slice size.
 --impl reference: the reference's CPU path (split_merge_kv + decode_attention,
 fp64 NumPy, restated in oracle/numerics_ref.py) timed on this host's cores.
 """
@@ -129,7 +133,7 @@ def run_reference(args):
     line = {
         "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "impl": "reference",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV offloaded to host",
                    "mode": "column", "profile": "b200-guess (1391.2e12 FLOP/s, 55e9 B/s) for the split"},
         "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample,
@@ -204,7 +208,11 @@ def run_kvpr(args):
     peaks = load_peaks()
     cfg = preset(args.model)
     cfg = cfg.with_positions(args.prompt + args.warmup + args.steps + 8)
-    b = args.batch
+    from paper_2411_17089_b200.multigpu import partition
+
+    gb = args.batch  # global batch: TP runs all of it on every rank, batch partition a b/G slice per rank
+    sl = partition(gb, 1 if args.tp else ws)[0 if args.tp else rank]
+    b = sl.count
     total_steps = args.warmup + args.steps
     wl = WorkloadSpec(batch_size=b, prompt_len=args.prompt, gen_len=total_steps)
 
@@ -232,8 +240,8 @@ def run_kvpr(args):
     except ImportError:
         pass
     w = OPTWeights.random(cfg, seed=0, device=dev)
-    g = torch.Generator().manual_seed(1 + (0 if args.tp else rank))
-    prompt = torch.randint(0, cfg.vocab, (b, args.prompt), generator=g)
+    g = torch.Generator().manual_seed(1)
+    prompt = torch.randint(0, cfg.vocab, (gb, args.prompt), generator=g)[sl.start:sl.start + b]  # this rank's rows
     if args.tp:
         from paper_2411_17089_b200.tp import TPRuntime
 
@@ -273,8 +281,7 @@ def run_kvpr(args):
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    jobs = 1 if args.tp else ws  # TP: one batch across all GPUs; batch partition: one batch per GPU
-    value = jobs * b * args.steps / elapsed
+    value = gb * args.steps / elapsed  # every rank's slice, over the slowest rank's time
 
     # per-layer latency and overlap roofline over the timed steps
     L = cfg.layers
@@ -309,7 +316,7 @@ def run_kvpr(args):
             t = torch.tensor([alt_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             alt_s = float(t.item())
-        alt = {"value": ws * b * args.steps / alt_s, "unit": "tok/s", "splits": alt_splits,
+        alt = {"value": gb * args.steps / alt_s, "unit": "tok/s", "splits": alt_splits,
                "ms_per_step": alt_s / args.steps * 1e3,
                "note": "extension objective max(t_act + t_kv, t_rec) of the chunked pipeline "
                        "(scheduler.solve_split_overlap); l differs from the reference's column solver, "
@@ -382,9 +389,13 @@ def run_kvpr(args):
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = jobs * b * e2e_steps / e2e_s
+    e2e_value = gb * e2e_steps / e2e_s
     h2d_step = h2d_alg / args.steps + b * 4
     d2h_step = (3 * b * cfg.hidden * 2) * L + b * 4
+    if ws > 1 and not args.tp:  # whole-job bytes
+        t = torch.tensor([h2d_step, d2h_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        h2d_step, d2h_step = float(t[0]), float(t[1])
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -424,7 +435,7 @@ def run_kvpr(args):
         for d in plan_r.decisions[args.warmup:]:
             troof_r += max(kv_remainder_bytes(cfg.spec(), wl, d.seq_len, d.recompute_len) / bw_peak,
                            recompute_flops(cfg.spec(), wl, d.recompute_len) / f_peak) * L
-        alt_row = {"value": jobs * b * args.steps / row_s, "unit": "tok/s", "splits": plan_r.splits[args.warmup:],
+        alt_row = {"value": gb * args.steps / row_s, "unit": "tok/s", "splits": plan_r.splits[args.warmup:],
                    "ms_per_step": row_s / args.steps * 1e3, "roofline_frac": troof_r / row_s,
                    "note": "row schedule: layer inputs X resident in HBM (8.9 GB), only KV[l:s'] over PCIe; "
                            "reference solver in mode 'row' (t_act = 0); roofline max(KV bytes/BW, FLOPs/F_sust)"}
@@ -455,7 +466,7 @@ def run_kvpr(args):
             kv4_s = float(t.item())
         troof4 = sum(overlap_roofline(cfg.spec(), wl4, d.seq_len, d.recompute_len, bw_peak, f_peak) * L
                      for d in plan4.decisions[args.warmup:])
-        alt_kv4 = {"value": jobs * b * args.steps / kv4_s, "unit": "tok/s", "splits": plan4.splits[args.warmup:],
+        alt_kv4 = {"value": gb * args.steps / kv4_s, "unit": "tok/s", "splits": plan4.splits[args.warmup:],
                    "ms_per_step": kv4_s / args.steps * 1e3, "roofline_frac": troof4 / kv4_s,
                    "note": "KV cache stored and streamed as 4-bit groupwise pages (0.5625 B/elem, lossy); "
                            "reference solver with kv_bytes_per_element=0.5625; not the headline workload"}
@@ -492,10 +503,10 @@ def run_kvpr(args):
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong" if args.tp else "weak", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
             "config": {
                 "workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV+X offloaded to pinned host",
-                "model": args.model, "global_batch": b * jobs, "seq_len": args.prompt,
+                "model": args.model, "global_batch": gb, "batch_per_gpu": b, "seq_len": args.prompt,
                 "parallelism": f"tp{ws} (head-sharded, NCCL)" if args.tp else f"batch-partition x{ws}",
                 "mode": "column", "splits_timed": splits[args.warmup:],
                 "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
