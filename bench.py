@@ -59,6 +59,21 @@ def load_peaks():
     return d
 
 
+COMM_DEV = "cpu"  # where the timing reductions live: the rank's GPU under NCCL, host under gloo
+
+
+def allreduce(vals, op="max"):
+    """Max (or sum) of a few floats over the ranks; identity at world size 1."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(vals)
+    t = torch.tensor(list(vals), dtype=torch.float64, device=COMM_DEV)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -199,11 +214,23 @@ def run_kvpr(args):
     from paper_2411_17089_b200.scheduler import overlap_roofline, plan_generation
     from paper_2411_17089_b200.weights import OPTWeights, preset
 
+    global COMM_DEV
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # KVPR_BENCH_SHARE_GPU=1: test mode for the multi-rank path on a 1-GPU box (ranks share cuda:0,
+    # reductions over gloo, since NCCL refuses two ranks on one device)
+    share = os.environ.get("KVPR_BENCH_SHARE_GPU") == "1"
+    gpu = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    from paper_2411_17089_b200.multigpu import bind_to_gpu_numa
+
+    numa = bind_to_gpu_numa(gpu)  # before any pinned allocation: this rank's host stores on its GPU's socket
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            COMM_DEV = dev
         args.no_alt = True  # alt lines are single-GPU context; N ranks x their host stores would crowd host DRAM
     peaks = load_peaks()
     cfg = preset(args.model)
@@ -276,11 +303,8 @@ def run_kvpr(args):
     if hasattr(rt, "kernel_timing"):
         rt.kernel_timing = None
     elapsed = start.elapsed_time(end) / 1e3
-    clk = clocks.stop(local) if clocks else None
-    if ws > 1:
-        t = torch.tensor([elapsed], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    clk = clocks.stop(gpu) if clocks else None
+    elapsed = allreduce([elapsed])[0]
     value = gb * args.steps / elapsed  # every rank's slice, over the slowest rank's time
 
     # per-layer latency and overlap roofline over the timed steps
@@ -312,10 +336,7 @@ def run_kvpr(args):
         a1.record(rt.cs)
         torch.cuda.synchronize(dev)
         alt_s = a0.elapsed_time(a1) / 1e3
-        if ws > 1:
-            t = torch.tensor([alt_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            alt_s = float(t.item())
+        alt_s = allreduce([alt_s])[0]
         alt = {"value": gb * args.steps / alt_s, "unit": "tok/s", "splits": alt_splits,
                "ms_per_step": alt_s / args.steps * 1e3,
                "note": "extension objective max(t_act + t_kv, t_rec) of the chunked pipeline "
@@ -385,17 +406,12 @@ def run_kvpr(args):
         tok_host.copy_(out[0], non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
     e2e_s = time.perf_counter() - te0
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = allreduce([e2e_s])[0]
     e2e_value = gb * e2e_steps / e2e_s
     h2d_step = h2d_alg / args.steps + b * 4
     d2h_step = (3 * b * cfg.hidden * 2) * L + b * 4
     if ws > 1 and not args.tp:  # whole-job bytes
-        t = torch.tensor([h2d_step, d2h_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        h2d_step, d2h_step = float(t[0]), float(t[1])
+        h2d_step, d2h_step = allreduce([h2d_step, d2h_step], op="sum")
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -427,10 +443,7 @@ def run_kvpr(args):
         r1.record(rt.cs)
         torch.cuda.synchronize(dev)
         row_s = r0.elapsed_time(r1) / 1e3
-        if ws > 1:
-            t = torch.tensor([row_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            row_s = float(t.item())
+        row_s = allreduce([row_s])[0]
         troof_r = 0.0
         for d in plan_r.decisions[args.warmup:]:
             troof_r += max(kv_remainder_bytes(cfg.spec(), wl, d.seq_len, d.recompute_len) / bw_peak,
@@ -460,10 +473,7 @@ def run_kvpr(args):
         k1.record(rt.cs)
         torch.cuda.synchronize(dev)
         kv4_s = k0.elapsed_time(k1) / 1e3
-        if ws > 1:
-            t = torch.tensor([kv4_s], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            kv4_s = float(t.item())
+        kv4_s = allreduce([kv4_s])[0]
         troof4 = sum(overlap_roofline(cfg.spec(), wl4, d.seq_len, d.recompute_len, bw_peak, f_peak) * L
                      for d in plan4.decisions[args.warmup:])
         alt_kv4 = {"value": gb * args.steps / kv4_s, "unit": "tok/s", "splits": plan4.splits[args.warmup:],
@@ -511,6 +521,7 @@ def run_kvpr(args):
                 "mode": "column", "splits_timed": splits[args.warmup:],
                 "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
                 "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
+                "numa": numa,
             },
             "roofline": k1_roof,
             "overlap_roofline": {

@@ -76,3 +76,61 @@ def gather_tokens(local: torch.Tensor, global_batch: int, device: torch.device |
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad)
     return torch.cat([bufs[s.rank][:, : s.count] for s in slices], dim=1)
+
+
+# ---------------------------------------------------------------------------
+# NUMA placement of a rank's host stores
+#
+# Every rank streams X[:, :l] and KV[l:] from its own page-locked stores over its own PCIe link;
+# on a two-socket host those pages must sit on the socket the GPU's root port hangs off, or every
+# H2D crosses the inter-socket link (and all ranks share it).  Pinning faults pages in on the
+# calling thread, so restricting the rank to the GPU's local CPUs before the stores are allocated
+# places them locally (first touch).
+
+def parse_cpulist(text: str) -> list[int]:
+    """'0-3,8,10-11' -> [0, 1, 2, 3, 8, 10, 11] (the kernel's cpulist format)."""
+    out: list[int] = []
+    for part in text.strip().split(","):
+        part = part.strip()
+        if not part:
+            continue
+        if "-" in part:
+            lo, hi = part.split("-", 1)
+            if int(hi) < int(lo):
+                raise ValueError(f"bad cpulist range {part!r}")
+            out.extend(range(int(lo), int(hi) + 1))
+        else:
+            out.append(int(part))
+    return sorted(set(out))
+
+
+def pci_address(device_index: int) -> str:
+    p = torch.cuda.get_device_properties(device_index)
+    return f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+
+
+def bind_to_gpu_numa(device_index: int, sysfs: str = "/sys/bus/pci/devices") -> dict:
+    """Restrict this process to the CPUs local to GPU `device_index` (no-op on one-node hosts).
+
+    Returns what was done: {"pci", "numa_node", "cpus", "bound"}.
+    """
+    import os
+    from pathlib import Path
+
+    info: dict = {"pci": None, "numa_node": None, "cpus": None, "bound": False}
+    try:
+        addr = pci_address(device_index)
+        info["pci"] = addr
+        d = Path(sysfs) / addr
+        node = int((d / "numa_node").read_text().strip()) if (d / "numa_node").exists() else -1
+        info["numa_node"] = node
+        cpus = parse_cpulist((d / "local_cpulist").read_text()) if (d / "local_cpulist").exists() else []
+        allowed = sorted(os.sched_getaffinity(0))
+        local = [c for c in cpus if c in set(allowed)]
+        info["cpus"] = len(local)
+        if local and len(local) < len(allowed):
+            os.sched_setaffinity(0, local)
+            info["bound"] = True
+    except (OSError, ValueError, RuntimeError, AttributeError) as e:
+        info["error"] = str(e)
+    return info

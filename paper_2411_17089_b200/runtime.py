@@ -243,9 +243,10 @@ class KVPRRuntime:
                 self._mlp(a, rows, lw, hbuf, x, mid, stream=cs)
             last = hbuf[(S0 - 1) * b:]
             self._head(last, stream=cs)
+            first = self.tok.clone()
         cs.synchronize()
         self.len = S0
-        return self.tok.clone()
+        return first
 
     # ------------------------------------------------------------ layer pieces
     def _qkv(self, x: torch.Tensor, M: int, lw, q_out: torch.Tensor, pages: torch.Tensor, q_group: int, stream):
@@ -461,14 +462,15 @@ class KVPRRuntime:
                 raise ValueError(f"step {i + 1}: split {l} out of range [0, {base + i + 1}]")
         cs = self.cs
         self._trace = trace
-        if tokens is not None:
-            with torch.cuda.stream(cs):
-                self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
         if out_tokens is None:
             out_tokens = torch.empty(steps, b, dtype=torch.int32, device=self.dev)
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
+        # everything the caller enqueued (e.g. the H2D of `tokens`) precedes this run on both engines
         cs.wait_stream(torch.cuda.current_stream(self.dev))
         self.hs.wait_stream(torch.cuda.current_stream(self.dev))
+        if tokens is not None:
+            with torch.cuda.stream(cs):
+                self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
         if native is None:  # the C executor covers the plain path (timed or not); tracing / 4-bit KV stay in Python
             native = trace is None and self.kv_bits is None
         if native:

@@ -159,9 +159,11 @@ class StreamedRuntime:
                     kernels.linear_simple(mid, lw.w2, lw.b2, hb[k], flags=acc, stream=cs, ws=self.ws)
             for k in range(K):
                 self._head(hb[k][(S0 - 1) * b:], k)
+        with torch.cuda.stream(cs):
+            first = self.tok.clone()
         cs.synchronize()
         self.len = S0
-        return self.tok.clone()
+        return first
 
     # ---------------------------------------------------------- layer pieces
     def _qkv(self, x, M, lw, q_out, pages, q_group, stream):
@@ -189,12 +191,12 @@ class StreamedRuntime:
             if not 0 <= l <= base + i + 1:
                 raise ValueError(f"step {i + 1}: split {l} out of range [0, {base + i + 1}]")
         cs, hs, ds = self.cs, self.hs, self.ds
+        cur = torch.cuda.current_stream(self.dev)
+        cs.wait_stream(cur)  # the caller's work (e.g. the H2D of `tokens`) precedes this run
+        hs.wait_stream(cur)
         if tokens is not None:
             with torch.cuda.stream(cs):
                 self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
-        cur = torch.cuda.current_stream(self.dev)
-        cs.wait_stream(cur)
-        hs.wait_stream(cur)
         out = torch.empty(steps, K, b, dtype=torch.int32, device=self.dev)
         logits = torch.empty(steps, K, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         ev = {k: {} for k in ("x", "kv", "wkv", "wrest", "done", "d2h", "layer_done")}

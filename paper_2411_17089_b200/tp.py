@@ -237,9 +237,11 @@ class TPRuntime:
                 kernels.linear_simple(x, lw.w1, lw.b1, mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
                 self._rowpar(mid, lw.w2, lw.b2, hbuf, rows)
             self._head(hbuf[(S0 - 1) * b:])
+        with torch.cuda.stream(cs):
+            first = self.tok.clone()
         cs.synchronize()
         self.len = S0
-        return self.tok.clone()
+        return first
 
     def _head(self, hrows):
         cs = self.cs
@@ -342,11 +344,11 @@ class TPRuntime:
             if not 0 <= l <= base + i + 1:
                 raise ValueError(f"step {i + 1}: split {l} out of range [0, {base + i + 1}]")
         cs = self.cs
+        cs.wait_stream(torch.cuda.current_stream(self.dev))  # the caller's work (e.g. H2D of `tokens`) first
+        self.hs_.wait_stream(torch.cuda.current_stream(self.dev))
         if tokens is not None:
             with torch.cuda.stream(cs):
                 self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
-        cs.wait_stream(torch.cuda.current_stream(self.dev))
-        self.hs_.wait_stream(torch.cuda.current_stream(self.dev))
         out = torch.empty(steps, b, dtype=torch.int32, device=self.dev)
         logits = torch.empty(steps, b, cfg.vocab, dtype=F32, device=self.dev) if keep_logits else None
         ev = {"done": {}, "d2h": {}}

@@ -115,3 +115,11 @@ def test_streamed_weight_regions_tile_the_layer(h, f):
     assert all(off % 16 == 0 for off, _ in covered)  # DMA / TMA friendly alignment
     with pytest.raises(ValueError):
         weight_regions(h, f, "ffn")
+
+
+def test_parse_cpulist():
+    assert multigpu.parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert multigpu.parse_cpulist("5") == [5]
+    assert multigpu.parse_cpulist("") == []
+    with pytest.raises(ValueError):
+        multigpu.parse_cpulist("4-2")

@@ -219,3 +219,28 @@ def test_row_schedule_x_resident_equals_column_bitwise():
         rt.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_decode_orders_after_callers_token_copy():
+    """decode(tokens=t) must read t only after the caller's stream has produced it.
+
+    Regression: the token copy used to be enqueued on the compute stream before the
+    compute stream waited on the caller's stream, so a `tokens` tensor still being written
+    on the current stream (e.g. the e2e loop's H2D of the next ids) was read stale; with two
+    ranks sharing a GPU the stale ids indexed past the embedding table.
+    """
+    cfg = OPTConfig(hidden=256, layers=2, heads=4, ffn=1024, vocab=1024, max_pos=128)
+    batch, S0 = 4, 40
+    w, prompt = _setup(cfg, batch, S0)
+    rt = KVPRRuntime(w, batch, S0 + 4)
+    first = rt.prefill(prompt)
+    other = (first + 7) % cfg.vocab
+    ref = rt.decode([3], tokens=other).cpu()
+    rt.reset(S0)
+    t = first.clone()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(int(5e7))  # the caller's stream is busy ...
+    t.copy_(other)               # ... and only then produces the ids
+    got = rt.decode([3], tokens=t).cpu()
+    rt.close()
+    assert torch.equal(got, ref)
