@@ -96,8 +96,9 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
  * Used for the decode-token q/k/v (K3), out-proj + residual (K4), fc1+ReLU and
  * fc2 + residual (K6), LM head (K8), and the prefill that fills the host stores.
  * bn selects the tile: 32 / 64 / 128 / 256 = 128 x bn tile on one CTA; 512 = 256 x 256 tile on a
- * CTA pair (tcgen05 cta_group::2); 0 = auto.  All variants accumulate K in the same order, so
- * they produce identical bits. */
+ * CTA pair (tcgen05 cta_group::2); -1 = weight-streaming decode GEMM with the operands swapped
+ * (128 weight rows x all M <= 64 activation rows per tile); 0 = auto (-1 for M <= 64).  All
+ * variants accumulate K in the same order, so without a K split they produce identical bits. */
 int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                 const kvpr_epilogue* epi, int bn, void* stream);
 

@@ -6,6 +6,7 @@
 
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -31,6 +32,15 @@ int check_launch(const char* what) {
     return KVPR_ECUDA;
   }
   return KVPR_OK;
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KVPR_PDL");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int sm_count(int device) {
@@ -101,8 +111,24 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
   a.flags = 0;
   const __half* a_ptr = static_cast<const __half*>(x) + (long long)pos_begin * bh;
   const int M = (pos_end - pos_begin) * batch;
-  // CTA-pair 256x256 tiles once there are rows for a pair tile; 1-CTA 128x256 below that
-  const int bn = M >= 256 ? 512 : 256;
+  // CTA-pair 256x256 tiles when they fill the SM pairs; below that (small models, short chunks)
+  // the widest 1-CTA tile that still gives >= sms/2 tiles (every shape accumulates K in the same
+  // order, so the choice never changes a bit; measured: tools/decode_gemm_bench.py --k1-only)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sm_count(dev);
+  const long long N = 2LL * hidden;
+  int bn = 512;
+  if (((M + 255) / 256) * ((N + 255) / 256) < sms / 2) {
+    const long long m_blk = (M + 127) / 128;
+    bn = 32;
+    for (int c = 256; c >= 32; c /= 2) {
+      if (m_blk * ((N + c - 1) / c) >= sms / 2) {
+        bn = c;
+        break;
+      }
+    }
+  }
   return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, bn, static_cast<cudaStream_t>(stream));
 }
 
@@ -125,10 +151,13 @@ int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, i
     cudaGetDevice(&dev);
     const int sms = sm_count(dev);
     const long long m_blk = (M + 127) / 128;
-    if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {
+    if (M <= 64) {
+      // decode (M = batch): weight streaming with the operands swapped (gemm_swapab_kernel)
+      bn = -1;
+    } else if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {
       bn = 512;
     } else if (m_blk == 1) {
-      // one row block (decode): weight-streaming; per-CTA k-loop throughput, not CTA count, limits
+      // one row block: weight-streaming; per-CTA k-loop throughput, not CTA count, limits
       // it, so wide N tiles win (measured: tools/gemm_bench.py, profiles/r01_gemm_variants.jsonl)
       bn = 128;
     } else {

@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
   constexpr int LPP = D / 8;
   constexpr int PPW = 32 / LPP;  // positions per warp step
   constexpr int NW = 4;
+  pdl_trigger();
+  pdl_wait();  // q (qkv GEMM), pages [0, l) (K1) come from the preceding kernels
   const int bh = blockIdx.x;
   const int b = bh / heads;
   const int hd = bh % heads;
@@ -266,6 +268,8 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
 template <int D>
 __global__ void decode_attn_combine_kernel(const float* __restrict__ ws, __half* __restrict__ out, int heads,
                                            int splits) {
+  pdl_trigger();
+  pdl_wait();
   const int bh = blockIdx.x;
   const int b = bh / heads, hd = bh % heads;
   const int dd = threadIdx.x;
@@ -365,24 +369,26 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
     q4.lo = q_lo;
     q4.hi = q_hi;
   }
+  int rc;
   if (head_dim == 128) {
     if (use_q4)
-      decode_attn_kernel<128, true><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<128, true>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
+                  seq_len, chunk, qscale, q4);
     else
-      decode_attn_kernel<128, false><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<128, false>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
+                  seq_len, chunk, qscale, q4);
   } else {
     if (use_q4)
-      decode_attn_kernel<64, true><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<64, true>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
+                  seq_len, chunk, qscale, q4);
     else
-      decode_attn_kernel<64, false><<<grid, 128, 0, stream>>>(q, kv, out, ws, batch, heads, seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<64, false>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
+                  seq_len, chunk, qscale, q4);
   }
-  int rc = check_launch("decode_attention");
   if (rc || splits == 1) return rc;
   if (head_dim == 128)
-    decode_attn_combine_kernel<128><<<bh, 128, 0, stream>>>(ws, out, heads, splits);
-  else
-    decode_attn_combine_kernel<64><<<bh, 64, 0, stream>>>(ws, out, heads, splits);
-  return check_launch("decode_attention_combine");
+    return launch("decode_attention_combine", decode_attn_combine_kernel<128>, bh, 128, 0, stream, ws, out, heads, splits);
+  return launch("decode_attention_combine", decode_attn_combine_kernel<64>, bh, 64, 0, stream, ws, out, heads, splits);
 }
 
 int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim, int seq_len,

@@ -190,6 +190,44 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16_f32(uint32_t M, uint32_t N
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL)
+//
+// Every kernel of the decode chain is launched with programmatic stream serialization
+// (launch() below), so kernel N+1's CTAs are scheduled while kernel N drains: its prologue
+// (barrier init, TMEM alloc, descriptor prefetch) and, for the GEMMs, the weight stream run
+// under kernel N's tail.  Contract for every kernel launched this way: pdl_wait() before the
+// first read of data an earlier kernel produces and before the first global write.  The wait
+// returns once the preceding grid has completed and its writes are visible (a no-op when the
+// kernel was launched without the attribute).
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // KVPR_PDL=0 in the environment turns the attribute off (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline int launch(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                  Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return check_launch(what);
+}
+
+// ---------------------------------------------------------------------------
 // fp16 packing
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {

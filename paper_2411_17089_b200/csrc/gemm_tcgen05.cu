@@ -24,16 +24,33 @@ namespace kvpr {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
+constexpr int kBnSwapAB = -1;  // gemm_f16 tile code of the swapped-operand decode GEMM
+
+// The 1-CTA ring is sized at launch: stage = A box (a_box_rows x 128 B: 16 KB, or only the live
+// rows of a small-M decode GEMM) + B box (BN x 128 B), as many stages as fit in shared memory
+// (<= kMaxStages).  A decode GEMM (M = batch) is weight streaming: its per-CTA rate is the
+// weight bytes in flight / the TMA round trip, so the ring holds only live A rows and spends the
+// rest of the 227 KB on B.  The MMA still reads a 128-row A operand; rows past a_box_rows fall on
+// the next stages' bytes (inside the allocation), which only feed accumulator rows >= M that the
+// epilogue never stores.
+constexpr int kMaxStages = 48;
+constexpr uint32_t kSmemBudget = 227 * 1024;
+constexpr uint32_t kBarrierBytes = 1024;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : (BN >= 64 ? 8 : 10));
-  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;  // full 128-row A box
   static constexpr uint32_t kBBytes = BN * kBK * 2;
-  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr uint32_t kSmemBytes = kSmemBudget;
 };
+
+// stages that fit: 1024 B alignment slack + barriers + stages x (A + B), and the last A stage's
+// 128-row MMA read (16 KB) stays inside the allocation
+__host__ __device__ inline int ring_stages(uint32_t a_stage, uint32_t b_stage) {
+  int s = static_cast<int>((kSmemBudget - 1024 - kBarrierBytes) / (a_stage + b_stage));
+  return s < kMaxStages ? s : kMaxStages;
+}
 
 
 // Epilogue for one thread: 32 fp32 accumulators of row (r_in, r_grp) at columns [n0, n0+32):
@@ -114,6 +131,8 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& p, const uint32_t (&
 
 // Deterministic split-K reduction: partials summed in slice order, then the GEMM epilogue.
 __global__ void split_k_reduce_kernel(const GemmArgs p) {
+  pdl_trigger();
+  pdl_wait();
   const int chunks = p.N / 32;
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(p.M) * chunks) return;
@@ -154,19 +173,21 @@ __global__ void __launch_bounds__(256, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const GemmArgs p) {
   using Cfg = GemmCfg<BN>;
-  constexpr int STAGES = Cfg::kStages;
+  const uint32_t a_stage = static_cast<uint32_t>(p.a_box_rows) * kBK * 2;
+  const int STAGES = ring_stages(a_stage, Cfg::kBBytes);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * Cfg::kABytes;
+  uint8_t* sB = smem + STAGES * a_stage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::kBBytes);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -196,23 +217,46 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
+      // The weights (B) never depend on an earlier kernel: the first ring's worth of B boxes is
+      // issued before the PDL wait, so the weight stream starts under the previous kernel's tail;
+      // A (activations) and everything after follow the wait.
+      // small-M GEMMs load only the live rows of A; the rest of the 128-row operand is stale smem
+      // that only produces accumulator rows the epilogue never stores
       uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int m_blk, n_blk;
-        tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
-        const int kb0 = (tile % splits) * kb_per;
-        const int kb1 = min(p.num_k_blk, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          // small-M GEMMs load only the live rows of A; the rest of the 128-row operand is stale smem
-          // that only produces accumulator rows the epilogue never stores
-          mbar_arrive_expect_tx(&full[stage], p.a_box_rows * kBK * 2 + Cfg::kBBytes);
-          tma_load_2d(sA + stage * Cfg::kABytes, &tmap_a, &full[stage], kb * kBK, m_blk * kBM);
-          tma_load_2d(sB + stage * Cfg::kBBytes, &tmap_b, &full[stage], kb * kBK, n_blk * BN);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      int it = 0, pre = 0;
+      for (int pass = 0; pass < 3; ++pass) {  // 0: B prefetch, 1: A of the prefetched, 2: the rest
+        if (pass == 1) pdl_wait();
+        it = 0;
+        stage = 0;
+        phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          int m_blk, n_blk;
+          tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+          const int kb0 = (tile % splits) * kb_per;
+          const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            if (pass == 0 && it == STAGES) break;
+            if (pass == 1 && it == pre) break;
+            if (pass == 2 && it < pre) {
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
+            if (pass != 1) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_arrive_expect_tx(&full[stage], a_stage + Cfg::kBBytes);
+              tma_load_2d(sB + stage * Cfg::kBBytes, &tmap_b, &full[stage], kb * kBK, n_blk * BN);
+            }
+            if (pass != 0) tma_load_2d(sA + stage * a_stage, &tmap_a, &full[stage], kb * kBK, m_blk * kBM);
+            if (pass == 0) ++pre;
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          if ((pass == 0 && it == STAGES) || (pass == 1 && it == pre)) break;
         }
       }
     }
@@ -232,7 +276,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
+          const uint32_t a_addr = smem_u32(sA + stage * a_stage);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
@@ -251,6 +295,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> regs -> global ----------------
+    pdl_wait();  // the residual (ACCUM) and every output buffer belong to the preceding kernels
     const uint32_t q = warp & 3;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -327,6 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -357,21 +403,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
+      // same PDL split as the 1-CTA producer: first ring of W_kv boxes before the wait
       uint32_t stage = 0, phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        int m_blk, n_blk;
-        tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
-        const int a_row = m_blk * 2 * kBM + rank * kBM;
-        const int b_row = n_blk * k2BN + rank * (k2BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
-          tma_load_2d_2sm(sA + stage * k2ABytes, &tmap_a, &full[stage], kb * kBK, a_row);
-          tma_load_2d_2sm(sB + stage * k2BBytes, &tmap_b, &full[stage], kb * kBK, b_row);
-          if (++stage == k2Stages) {
-            stage = 0;
-            phase ^= 1;
+      int it = 0, pre = 0;
+      for (int pass = 0; pass < 3; ++pass) {  // 0: B prefetch, 1: A of the prefetched, 2: the rest
+        if (pass == 1) pdl_wait();
+        it = 0;
+        stage = 0;
+        phase = 0;
+        for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+          int m_blk, n_blk;
+          tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+          const int a_row = m_blk * 2 * kBM + rank * kBM;
+          const int b_row = n_blk * k2BN + rank * (k2BN / 2);
+          for (int kb = 0; kb < num_kb; ++kb, ++it) {
+            if (pass == 0 && it == k2Stages) break;
+            if (pass == 1 && it == pre) break;
+            if (pass == 2 && it < pre) {
+              if (++stage == k2Stages) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
+            if (pass != 1) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * k2StageBytes);
+              tma_load_2d_2sm(sB + stage * k2BBytes, &tmap_b, &full[stage], kb * kBK, b_row);
+            }
+            if (pass != 0) tma_load_2d_2sm(sA + stage * k2ABytes, &tmap_a, &full[stage], kb * kBK, a_row);
+            if (pass == 0) ++pre;
+            if (++stage == k2Stages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          if ((pass == 0 && it == k2Stages) || (pass == 1 && it == pre)) break;
         }
       }
     }
@@ -407,6 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
+    pdl_wait();
     const uint32_t q = warp & 3;
     uint32_t local = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
@@ -446,6 +514,239 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_2sm<512>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Weight-streaming decode GEMM (M = batch rows <= 64): operands swapped.
+//
+//   D^T[n, m] = sum_k W[n, k] * A[m, k]
+//
+// A decode GEMM has a handful of live activation rows against megabytes of weights.  In the
+// regular kernel the activations are the MMA's M operand, padded to 128 rows, and the weights
+// the N operand: a k-block then costs a full 128 x BN MMA for 4..32 useful rows, and one CTA's
+// chain of dependent MMAs, not HBM, sets the pace (~0.25 us per 64-wide k-block whatever BN).
+// Here the weight tile is the 128-row M operand and the activation rows the N operand (MP = M
+// rounded up to 16; TMA zero-fills rows >= M), so every k-block of the same MMA chain moves 16 KB
+// of weights and the tensor core does no padded work on the weight side.  The accumulator is
+// 128 TMEM lanes (weight rows) x MP columns (activation rows); the epilogue thread owning lane
+// n writes column n of every output row m (coalesced across the warp for each m).
+//
+// The k order per output element is the regular kernel's (k-blocks ascending, 16-wide MMA K
+// steps), so an unsplit launch reproduces it bit for bit (tested against K1: the decode-time
+// k, v of the new token must equal the K1 rebuild).  k_splits > 1 (only with a workspace, never
+// for the q/k/v projection) writes raw fp32 partials that split_k_reduce_kernel sums in slice
+// order.
+
+constexpr uint32_t kSwWBytes = kBM * kBK * 2;  // 16 KB: 128 weight rows x 64 k
+
+template <int MP>
+struct SwapCfg {
+  static constexpr uint32_t kXBytes = MP * kBK * 2;
+  static constexpr uint32_t kStageBytes = kSwWBytes + kXBytes;
+  static constexpr int kStages = static_cast<int>((kSmemBudget - 1024 - kBarrierBytes) / kStageBytes) < kMaxStages
+                                     ? static_cast<int>((kSmemBudget - 1024 - kBarrierBytes) / kStageBytes)
+                                     : kMaxStages;
+  static constexpr uint32_t kTmemCols = (2 * MP <= 32) ? 32 : (2 * MP <= 64 ? 64 : 128);
+};
+
+template <int MP>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[MP]);
+
+template <>
+__device__ __forceinline__ void tmem_ld_cols<16>(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+template <>
+__device__ __forceinline__ void tmem_ld_cols<32>(uint32_t taddr, uint32_t (&r)[32]) {
+  tmem_ld_32x32b_x32(taddr, r);
+}
+
+template <>
+__device__ __forceinline__ void tmem_ld_cols<64>(uint32_t taddr, uint32_t (&r)[64]) {
+  tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+  tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+}
+
+template <int MP>
+__global__ void __launch_bounds__(256, 1)
+    gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+                       const GemmArgs p) {
+  using Cfg = SwapCfg<MP>;
+  constexpr int STAGES = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + STAGES * kSwWBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + STAGES * Cfg::kXBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  pdl_trigger();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int splits = p.k_splits > 1 ? p.k_splits : 1;
+  const int num_tiles = p.num_n_blk * splits;  // tile = (n block, k slice), slices of a block adjacent
+  const int kb_per = (p.num_k_blk + splits - 1) / splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: weights before the PDL wait, activations after ----------------
+      uint32_t stage = 0, phase = 0;
+      int it = 0, pre = 0;
+      for (int pass = 0; pass < 3; ++pass) {
+        if (pass == 1) pdl_wait();
+        it = 0;
+        stage = 0;
+        phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          const int n_blk = tile / splits;
+          const int kb0 = (tile % splits) * kb_per;
+          const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            if (pass == 0 && it == STAGES) break;
+            if (pass == 1 && it == pre) break;
+            if (pass == 2 && it < pre) {
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
+            if (pass != 1) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+              tma_load_2d(sW + stage * kSwWBytes, &tmap_w, &full[stage], kb * kBK, n_blk * kBM);
+            }
+            if (pass != 0) tma_load_2d(sX + stage * Cfg::kXBytes, &tmap_x, &full[stage], kb * kBK, 0);
+            if (pass == 0) ++pre;
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          if ((pass == 0 && it == STAGES) || (pass == 1 && it == pre)) break;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer: M = 128 weight rows, N = MP activation rows ----------------
+      constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, MP);
+      uint32_t stage = 0, phase = 0, local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * MP;
+        const int kb0 = (tile % splits) * kb_per;
+        const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t w_addr = smem_u32(sW + stage * kSwWBytes);
+          const uint32_t x_addr = smem_u32(sX + stage * Cfg::kXBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_f16(d_tmem, umma_desc_k_sw128(w_addr + k * 32), umma_desc_k_sw128(x_addr + k * 32), idesc,
+                     (kb != kb0) || (k != 0));
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: lane n of the tile, every activation row m ----------------
+    pdl_wait();
+    const uint32_t q = warp & 3;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int n_blk = tile / splits;
+      const int ks = tile % splits;
+      const uint32_t acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      uint32_t r[MP];
+      tmem_ld_cols<MP>(tmem_base + ((q * 32u) << 16) + acc * MP, r);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained into registers
+      const int n = n_blk * kBM + q * 32 + lane;
+      if (n < p.N) {
+        if (splits > 1) {
+          float* o = p.ws + static_cast<long long>(ks) * p.M * p.ws_ld + n;
+#pragma unroll
+          for (int m = 0; m < MP; ++m)
+            if (m < p.M) o[static_cast<long long>(m) * p.ws_ld] = __uint_as_float(r[m]);
+        } else {
+          const float bias = p.bias != nullptr ? __half2float(p.bias[n]) : 0.f;
+          const bool scaled = n < p.scale_cols;
+          const int seg = n / p.seg_width;
+          const int col = n - seg * p.seg_width;
+          char* sp = static_cast<char*>(seg == 0 ? p.seg_ptr[0] : (seg == 1 ? p.seg_ptr[1] : p.seg_ptr[2]));
+          const long long gs = seg == 0 ? p.seg_group_stride[0] : (seg == 1 ? p.seg_group_stride[1] : p.seg_group_stride[2]);
+#pragma unroll
+          for (int m = 0; m < MP; ++m) {
+            if (m >= p.M) continue;
+            float v = __uint_as_float(r[m]) + bias;
+            if (scaled) v *= p.scale;
+            if (p.flags & KVPR_EPI_RELU) v = fmaxf(v, 0.f);
+            const long long off = (m % p.row_group) * p.ld + (m / p.row_group) * gs + col;
+            if (p.flags & KVPR_EPI_F32) {
+              float* o = reinterpret_cast<float*>(sp) + off;
+              *o = (p.flags & KVPR_EPI_ACCUM) ? *o + v : v;
+            } else {
+              reinterpret_cast<__half*>(sp)[off] = __float2half_rn(v);
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -514,14 +815,44 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
     attr_done[dev] = 1;
   }
   const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
-  gemm_tcgen05_kernel<BN><<<grid, 256, Cfg::kSmemBytes, stream>>>(ta, tb, args);
-  int rc2 = check_launch("gemm_tcgen05");
+  int rc2 = launch("gemm_tcgen05", gemm_tcgen05_kernel<BN>, grid, 256, Cfg::kSmemBytes, stream, ta, tb, args);
   if (rc2 || splits == 1) return rc2;
   const long long work = static_cast<long long>(args.M) * (args.N / 32);
-  split_k_reduce_kernel<<<static_cast<unsigned>((work + 127) / 128), 128, 0, stream>>>(args);
-  return check_launch("split_k_reduce");
+  return launch("split_k_reduce", split_k_reduce_kernel, static_cast<unsigned>((work + 127) / 128), 128, 0, stream,
+                args);
 }
 
+
+template <int MP>
+static int launch_swapab(const void* a, long long lda, const void* w, long long ldw, GemmArgs args,
+                         cudaStream_t stream) {
+  using Cfg = SwapCfg<MP>;
+  CUtensorMap tw, tx;
+  int rc = make_tmap(&tw, w, args.N, args.K, ldw, kBM);
+  if (rc) return rc;
+  rc = make_tmap(&tx, a, args.M, args.K, lda, MP);  // rows >= M of the box are zero-filled
+  if (rc) return rc;
+  args.num_m_blk = 1;
+  args.num_n_blk = (args.N + kBM - 1) / kBM;
+  args.num_k_blk = (args.K + kBK - 1) / kBK;
+  args.a_box_rows = MP;
+  const int splits = args.k_splits > 1 ? args.k_splits : 1;
+  const int tiles = args.num_n_blk * splits;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  constexpr uint32_t smem = 1024 + Cfg::kStages * Cfg::kStageBytes + kBarrierBytes;
+  static int attr_done[64] = {0};
+  if (dev < 64 && !attr_done[dev]) {
+    cudaFuncSetAttribute(gemm_swapab_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_done[dev] = 1;
+  }
+  const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
+  rc = launch("gemm_swapab", gemm_swapab_kernel<MP>, grid, 256, smem, stream, tw, tx, args);
+  if (rc || splits == 1) return rc;
+  const long long work = static_cast<long long>(args.M) * (args.N / 32);
+  return launch("split_k_reduce", split_k_reduce_kernel, static_cast<unsigned>((work + 127) / 128), 128, 0, stream,
+                args);
+}
 
 static int launch_2sm(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
   CUtensorMap ta, tb;
@@ -542,8 +873,7 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
   }
   const int pairs = sm_count(dev) / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  gemm_tcgen05_2sm_kernel<<<grid, 256, k2SmemBytes, stream>>>(ta, tb, args);
-  return check_launch("gemm_tcgen05_2sm");
+  return launch("gemm_tcgen05_2sm", gemm_tcgen05_2sm_kernel, grid, 256, k2SmemBytes, stream, ta, tb, args);
 }
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
@@ -555,7 +885,26 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
   args.k_splits = 1;
   args.ws = nullptr;
   args.ws_ld = N;
-  if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256 && K >= 8192) {
+  if (bn == kBnSwapAB && ws != nullptr) {
+    // weight-streaming decode GEMM: an SM streams ~46 GB/s, so HBM needs every SM: slice K until
+    // the 128-row weight tiles fill them (deterministic: slices summed in order by
+    // split_k_reduce_kernel).  The reduce is one more dependent launch, so only weights of
+    // >= 16 MB split, into slices of >= 16 k-blocks (measured: tools/decode_gemm_bench.py)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int n_tiles = (N + kBM - 1) / kBM;
+    const int num_kb = (K + kBK - 1) / kBK;
+    int s = sm_count(dev) / n_tiles;
+    if (s > 8) s = 8;
+    if (s > num_kb / 16) s = num_kb / 16;
+    if (static_cast<long long>(N) * K * 2 < (16ll << 20)) s = 1;
+    while (s > 1 && (num_kb + s - 1) / s * (s - 1) >= num_kb) --s;  // every slice non-empty
+    if (s > 1 && static_cast<size_t>(s) * M * N * sizeof(float) <= ws_bytes &&
+        (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
+      args.k_splits = s;
+      args.ws = ws;
+    }
+  } else if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256 && K >= 8192) {
     // only long k-loops gain: short ones are dominated by pipeline fill + the extra reduce launch
     // (measured: fc2 32x4096x16384 75 -> 51 us; out-proj 32x4096x4096 23 -> 29 us)
     // one row block, weight-streaming: each CTA's k-loop is latency bound, so slice K until the
@@ -605,6 +954,14 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
     return KVPR_EINVAL;
   }
   switch (bn) {
+    case kBnSwapAB:  // weight-streaming decode GEMM, M <= 64
+      if (M > 64) {
+        set_error("gemm: swap-AB decode GEMM needs M <= 64 (M=%d)", M);
+        return KVPR_EINVAL;
+      }
+      if (M <= 16) return launch_swapab<16>(a, lda, w, ldw, args, stream);
+      if (M <= 32) return launch_swapab<32>(a, lda, w, ldw, args, stream);
+      return launch_swapab<64>(a, lda, w, ldw, args, stream);
     case 512:  // 256 x 256 pair tile on a CTA pair (cta_group::2)
       return launch_2sm(a, lda, w, ldw, args, stream);
     case 256:

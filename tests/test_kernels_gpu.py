@@ -49,7 +49,12 @@ def _rand(*shape, scale=1.0, dev="cuda", seed=None, dtype=torch.float16):
         (100, 768, 768, 512),  # M < 128: the peer CTA's rows are all out of range
         (4096, 2304, 768, 512),  # N tail within the pair tile (2304 = 9 x 256)
         (32, 4096, 16384, 32),  # decode fc2 shape on narrow 128x32 tiles
-        (32, 4096, 4096, 0),  # decode out-proj, auto BN
+        (32, 4096, 4096, 0),  # decode out-proj, auto BN (swap-AB)
+        (4, 2304, 768, -1),  # swap-AB decode GEMM, config-1 q/k/v
+        (32, 12288, 4096, -1),  # swap-AB, config-2 q/k/v
+        (50, 1024, 512, -1),  # swap-AB with 64 padded activation rows
+        (1, 50272, 768, -1),  # swap-AB, LM-head N tail, persistent tiles
+        (17, 640, 1000, -1),  # swap-AB, K tail and an N tail inside a tile
     ],
 )
 def test_linear_matches_fp32(dev, M, N, K, bn):
@@ -74,6 +79,59 @@ def test_pair_tile_bitwise_equals_single_cta(dev):
     kernels.linear_simple(a, w, None, o2, bn=512)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("M", [1, 4, 16, 32, 33, 64])
+def test_swapab_bitwise_equals_regular(dev, M):
+    """The swapped-operand decode GEMM keeps the regular kernel's k order: identical bits unsplit
+    (so the decode-time k, v of a new token equal what K1 rebuilds later)."""
+    N, K = 768, 2048
+    a = _rand(M, K, scale=0.5, seed=51)
+    w = _rand(N, K, scale=0.05, seed=52)
+    bias = _rand(N, scale=0.1, seed=53)
+    o1 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    o2 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, o1, bn=-1)
+    kernels.linear_simple(a, w, bias, o2, bn=128)
+    r1 = torch.randn(M, N, device=dev)
+    r2 = r1.clone()
+    kernels.linear_simple(a, w, bias, r1, bn=-1, flags=_lib.EPI_ACCUM)
+    kernels.linear_simple(a, w, bias, r2, bn=128, flags=_lib.EPI_ACCUM)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    assert torch.equal(r1, r2)
+
+
+def test_swapab_qkv_equals_k1_rebuild(dev):
+    """Decode q/k/v via the swap-AB GEMM vs K1 recomputing the same position: k, v bit-identical."""
+    b, h = 32, 1024
+    x = _rand(1, b, h, scale=1.0, seed=61)
+    wqkv = _rand(3 * h, h, scale=0.03, seed=62)
+    bqkv = _rand(3 * h, scale=0.1, seed=63)
+    q = torch.empty(b, h, dtype=torch.float16, device=dev)
+    page_dec = torch.zeros(1, 2, b, h, dtype=torch.float16, device=dev)
+    bh = b * h
+    kp = page_dec.data_ptr()
+    epi = _lib.make_epilogue([(q.data_ptr(), 0), (kp, 2 * bh), (kp + bh * 2, 2 * bh)], seg_width=h, ld=h,
+                             row_group=b, bias=bqkv.data_ptr())
+    kernels.linear(x.view(b, h), wqkv, epi, M=b, bn=-1)
+    page_k1 = torch.zeros(1, 2, b, h, dtype=torch.float16, device=dev)
+    kernels.recompute_kv(x, wqkv[h:], bqkv[h:], page_k1, b, 0, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(page_dec, page_k1)
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 4096, 16384), (32, 4096, 4096), (4, 768, 3072), (4, 50272, 768)])
+def test_swapab_splitk_matches_fp32(dev, M, N, K):
+    a = _rand(M, K, scale=0.5, seed=71)
+    w = _rand(N, K, scale=0.05, seed=72)
+    bias = _rand(N, scale=0.1, seed=73)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    out = torch.randn(M, N, device=dev)
+    ref = out.clone() + (a.float() @ w.float().T + bias.float())
+    kernels.linear_simple(a, w, bias, out, flags=_lib.EPI_ACCUM, ws=ws)
+    torch.cuda.synchronize()
+    _close(out, ref, rtol=1e-4, atol=2e-3)
 
 
 def test_linear_epilogues(dev):

@@ -36,22 +36,30 @@ def main():
     ap.add_argument("--prompt", type=int, default=256)
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--graph", type=int, default=-1, help="force executor graph mode (0/1); -1 = runtime default")
+    ap.add_argument("--x-resident", action="store_true", help="row schedule: X resident in HBM (no X H2D)")
+    ap.add_argument("--split", type=int, default=-2, help=">= 0: constant split l; -1: l = s' (all recompute)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     cfg = preset(args.model).with_positions(args.prompt + 4 * args.steps + 8)
     wl = WorkloadSpec(args.batch, args.prompt, 4 * args.steps)
     prof = HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=55e9)
-    splits = plan_generation(cfg.spec(), wl, prof, "column").splits
+    splits = plan_generation(cfg.spec(), wl, prof, "row" if args.x_resident else "column").splits
+    if args.split >= 0:
+        splits = [min(args.split, args.prompt + i + 1) for i in range(len(splits))]
+    elif args.split == -1:
+        splits = [args.prompt + i + 1 for i in range(len(splits))]
     w = OPTWeights.random(cfg, seed=0, device=dev)
     prompt = torch.randint(0, cfg.vocab, (args.batch, args.prompt), generator=torch.Generator().manual_seed(1))
-    rt = KVPRRuntime(w, args.batch, args.prompt + 4 * args.steps + 1, device=dev)
+    rt = KVPRRuntime(w, args.batch, args.prompt + 4 * args.steps + 1, device=dev, x_resident=args.x_resident)
     if args.graph >= 0 and hasattr(rt, "graph"):
         rt.graph = bool(args.graph)
     first = rt.prefill(prompt)
     K = args.steps
     rt.decode(splits[:K], tokens=first)  # warm-up
     torch.cuda.synchronize()
-    out = {"model": args.model, "batch": args.batch, "prompt": args.prompt, "steps": K, "layers": cfg.layers}
+    out = {"model": args.model, "batch": args.batch, "prompt": args.prompt, "steps": K, "layers": cfg.layers,
+           "x_resident": args.x_resident, "split": args.split, "pdl": os.environ.get("KVPR_PDL", "1"),
+           "splits": splits[K:2 * K]}
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     cur = torch.cuda.current_stream()
