@@ -17,6 +17,8 @@
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM owner,
 // w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes [32*(w%4), +32)).
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kvpr_internal.h"
 
@@ -25,6 +27,8 @@ namespace kvpr {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
 constexpr int kBnSwapAB = -1;  // gemm_f16 tile code of the swapped-operand decode GEMM
+constexpr long long kABandBytes = 32ll << 20;
+constexpr int kSwapKBoxDefault = 1;  // L2-resident A band of one rasterization group
 
 // The 1-CTA ring is sized at launch: stage = A box (a_box_rows x 128 B: 16 KB, or only the live
 // rows of a small-M decode GEMM) + B box (BN x 128 B), as many stages as fit in shared memory
@@ -155,17 +159,19 @@ __global__ void split_k_reduce_kernel(const GemmArgs p) {
   store_chunk_f(p, v, n0, row % p.row_group, row / p.row_group);
 }
 
-// Tile order: groups of kGroupM m-blocks, n-major inside a group, so the CTAs in flight share
-// a small band of A (reused across n from L2) and a few B column blocks.
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
-  constexpr int kGroupM = 16;
-  const int per_group = kGroupM * num_n;
+// Tile order: groups of `group` m-blocks, n-major inside a group, so the CTAs in flight share a
+// band of A (reused across n from L2) and stream each B column block once per group.  Odd groups
+// sweep n backwards, so a group starts on the B blocks the previous one just left in L2.  The
+// band (kABandBytes) is sized to stay L2-resident: at K1's config-2 chunk, 16 pair m-blocks
+// (32 MB of A) measured best; 24 or all 28 thrash (DRAM reads 208 -> 326 MB, profiles/).
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group, int& m_blk, int& n_blk) {
+  const int per_group = group * num_n;
   const int g = tile / per_group;
-  const int first_m = g * kGroupM;
-  const int gm = min(kGroupM, num_m - first_m);
+  const int first_m = g * group;
+  const int gm = min(group, num_m - first_m);
   const int local = tile - g * per_group;
   m_blk = first_m + local % gm;
-  n_blk = local / gm;
+  n_blk = (g & 1) ? num_n - 1 - local / gm : local / gm;
 }
 
 template <int BN>
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(256, 1)
         phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           int m_blk, n_blk;
-          tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+          tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, p.group_m, m_blk, n_blk);
           const int kb0 = (tile % splits) * kb_per;
           const int kb1 = min(p.num_k_blk, kb0 + kb_per);
           for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       int m_blk, n_blk;
-      tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+      tile_coords(tile / splits, p.num_m_blk, p.num_n_blk, p.group_m, m_blk, n_blk);
       const int ks = tile % splits;
       const uint32_t acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -413,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         phase = 0;
         for (int tile = cluster; tile < num_tiles; tile += nclusters) {
           int m_blk, n_blk;
-          tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+          tile_coords(tile, p.num_m_blk, p.num_n_blk, p.group_m, m_blk, n_blk);
           const int a_row = m_blk * 2 * kBM + rank * kBM;
           const int b_row = n_blk * k2BN + rank * (k2BN / 2);
           for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -479,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint32_t local = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
       int m_blk, n_blk;
-      tile_coords(tile, p.num_m_blk, p.num_n_blk, m_blk, n_blk);
+      tile_coords(tile, p.num_m_blk, p.num_n_blk, p.group_m, m_blk, n_blk);
       const uint32_t acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -540,10 +546,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
 constexpr uint32_t kSwWBytes = kBM * kBK * 2;  // 16 KB: 128 weight rows x 64 k
 
-template <int MP>
+// KB 64-wide k-boxes per ring stage: a stage reads KB x 128 B contiguous from each of its 128
+// weight rows (one DRAM page visit instead of KB), at the cost of fewer, larger stages.
+template <int MP, int KB>
 struct SwapCfg {
-  static constexpr uint32_t kXBytes = MP * kBK * 2;
-  static constexpr uint32_t kStageBytes = kSwWBytes + kXBytes;
+  static constexpr uint32_t kXBox = MP * kBK * 2;
+  static constexpr uint32_t kWStage = KB * kSwWBytes;
+  static constexpr uint32_t kXStage = KB * kXBox;
+  static constexpr uint32_t kStageBytes = kWStage + kXStage;
   static constexpr int kStages = static_cast<int>((kSmemBudget - 1024 - kBarrierBytes) / kStageBytes) < kMaxStages
                                      ? static_cast<int>((kSmemBudget - 1024 - kBarrierBytes) / kStageBytes)
                                      : kMaxStages;
@@ -574,17 +584,17 @@ __device__ __forceinline__ void tmem_ld_cols<64>(uint32_t taddr, uint32_t (&r)[6
   tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
 }
 
-template <int MP>
+template <int MP, int KB>
 __global__ void __launch_bounds__(256, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                        const GemmArgs p) {
-  using Cfg = SwapCfg<MP>;
+  using Cfg = SwapCfg<MP, KB>;
   constexpr int STAGES = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  uint8_t* sX = smem + STAGES * kSwWBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + STAGES * Cfg::kXBytes);
+  uint8_t* sX = smem + STAGES * Cfg::kWStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + STAGES * Cfg::kXStage);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
@@ -633,7 +643,7 @@ __global__ void __launch_bounds__(256, 1)
           const int n_blk = tile / splits;
           const int kb0 = (tile % splits) * kb_per;
           const int kb1 = min(p.num_k_blk, kb0 + kb_per);
-          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          for (int kb = kb0; kb < kb1; kb += KB, ++it) {
             if (pass == 0 && it == STAGES) break;
             if (pass == 1 && it == pre) break;
             if (pass == 2 && it < pre) {
@@ -643,12 +653,18 @@ __global__ void __launch_bounds__(256, 1)
               }
               continue;
             }
+            const int nbox = min(KB, kb1 - kb);
             if (pass != 1) {
               mbar_wait(&empty[stage], phase ^ 1);
-              mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-              tma_load_2d(sW + stage * kSwWBytes, &tmap_w, &full[stage], kb * kBK, n_blk * kBM);
+              mbar_arrive_expect_tx(&full[stage], nbox * (kSwWBytes + Cfg::kXBox));
+              for (int j = 0; j < nbox; ++j)
+                tma_load_2d(sW + stage * Cfg::kWStage + j * kSwWBytes, &tmap_w, &full[stage], (kb + j) * kBK,
+                            n_blk * kBM);
             }
-            if (pass != 0) tma_load_2d(sX + stage * Cfg::kXBytes, &tmap_x, &full[stage], kb * kBK, 0);
+            if (pass != 0) {
+              for (int j = 0; j < nbox; ++j)
+                tma_load_2d(sX + stage * Cfg::kXStage + j * Cfg::kXBox, &tmap_x, &full[stage], (kb + j) * kBK, 0);
+            }
             if (pass == 0) ++pre;
             if (++stage == STAGES) {
               stage = 0;
@@ -672,15 +688,18 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t d_tmem = tmem_base + acc * MP;
         const int kb0 = (tile % splits) * kb_per;
         const int kb1 = min(p.num_k_blk, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += KB) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t w_addr = smem_u32(sW + stage * kSwWBytes);
-          const uint32_t x_addr = smem_u32(sX + stage * Cfg::kXBytes);
+          const int nbox = min(KB, kb1 - kb);
+          for (int j = 0; j < nbox; ++j) {
+            const uint32_t w_addr = smem_u32(sW + stage * Cfg::kWStage + j * kSwWBytes);
+            const uint32_t x_addr = smem_u32(sX + stage * Cfg::kXStage + j * Cfg::kXBox);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            umma_f16(d_tmem, umma_desc_k_sw128(w_addr + k * 32), umma_desc_k_sw128(x_addr + k * 32), idesc,
-                     (kb != kb0) || (k != 0));
+            for (int k = 0; k < kBK / 16; ++k) {
+              umma_f16(d_tmem, umma_desc_k_sw128(w_addr + k * 32), umma_desc_k_sw128(x_addr + k * 32), idesc,
+                       (kb != kb0) || (j != 0) || (k != 0));
+            }
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -793,6 +812,26 @@ static int make_tmap(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t 
   return KVPR_OK;
 }
 
+// 64-wide k-boxes per ring stage of the swap-AB decode GEMM: KVPR_SWAP_KBOX = 1, 2 or 4 overrides
+// the shape-based default (0)
+static int swap_kbox() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KVPR_SWAP_KBOX");
+    v = (e != nullptr && (atoi(e) == 1 || atoi(e) == 2 || atoi(e) == 4)) ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// m-blocks per rasterization group: the A band of a group stays in L2 while B streams past it
+static int band_group(int num_m_blk, long long band_bytes_per_m_blk) {
+  const char* e = getenv("KVPR_GEMM_GROUP_M");  // experiment override
+  if (e != nullptr && atoi(e) > 0) return atoi(e) < num_m_blk ? atoi(e) : num_m_blk;
+  long long g = kABandBytes / (band_bytes_per_m_blk > 0 ? band_bytes_per_m_blk : 1);
+  if (g < 1) g = 1;
+  return static_cast<int>(g < num_m_blk ? g : num_m_blk);
+}
+
 template <int BN>
 static int launch_bn(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
@@ -805,6 +844,7 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
   args.num_m_blk = (args.M + kBM - 1) / kBM;
   args.num_n_blk = (args.N + BN - 1) / BN;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
+  args.group_m = band_group(args.num_m_blk, static_cast<long long>(kBM) * args.K * 2);
   const int splits = args.k_splits > 1 ? args.k_splits : 1;
   const int tiles = args.num_m_blk * args.num_n_blk * splits;
   int dev = 0;
@@ -823,10 +863,10 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
 }
 
 
-template <int MP>
+template <int MP, int KB>
 static int launch_swapab(const void* a, long long lda, const void* w, long long ldw, GemmArgs args,
                          cudaStream_t stream) {
-  using Cfg = SwapCfg<MP>;
+  using Cfg = SwapCfg<MP, KB>;
   CUtensorMap tw, tx;
   int rc = make_tmap(&tw, w, args.N, args.K, ldw, kBM);
   if (rc) return rc;
@@ -843,11 +883,11 @@ static int launch_swapab(const void* a, long long lda, const void* w, long long 
   constexpr uint32_t smem = 1024 + Cfg::kStages * Cfg::kStageBytes + kBarrierBytes;
   static int attr_done[64] = {0};
   if (dev < 64 && !attr_done[dev]) {
-    cudaFuncSetAttribute(gemm_swapab_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gemm_swapab_kernel<MP, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_done[dev] = 1;
   }
   const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
-  rc = launch("gemm_swapab", gemm_swapab_kernel<MP>, grid, 256, smem, stream, tw, tx, args);
+  rc = launch("gemm_swapab", gemm_swapab_kernel<MP, KB>, grid, 256, smem, stream, tw, tx, args);
   if (rc || splits == 1) return rc;
   const long long work = static_cast<long long>(args.M) * (args.N / 32);
   return launch("split_k_reduce", split_k_reduce_kernel, static_cast<unsigned>((work + 127) / 128), 128, 0, stream,
@@ -863,6 +903,7 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
   args.num_m_blk = (args.M + 2 * kBM - 1) / (2 * kBM);
   args.num_n_blk = (args.N + k2BN - 1) / k2BN;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
+  args.group_m = band_group(args.num_m_blk, static_cast<long long>(2 * kBM) * args.K * 2);
   const int tiles = args.num_m_blk * args.num_n_blk;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -959,9 +1000,20 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
         set_error("gemm: swap-AB decode GEMM needs M <= 64 (M=%d)", M);
         return KVPR_EINVAL;
       }
-      if (M <= 16) return launch_swapab<16>(a, lda, w, ldw, args, stream);
-      if (M <= 32) return launch_swapab<32>(a, lda, w, ldw, args, stream);
-      return launch_swapab<64>(a, lda, w, ldw, args, stream);
+      {
+        // measured (tools/decode_gemm_bench.py --swap-only, KVPR_SWAP_KBOX): 4 boxes per stage at
+        // M <= 16, 2 above (larger stages, fewer of them, once the activation box grows)
+        const int kb = swap_kbox() > 0 ? swap_kbox() : (M <= 16 ? 4 : 2);
+        if (M <= 16) return kb == 4 ? launch_swapab<16, 4>(a, lda, w, ldw, args, stream)
+                                    : (kb == 2 ? launch_swapab<16, 2>(a, lda, w, ldw, args, stream)
+                                               : launch_swapab<16, 1>(a, lda, w, ldw, args, stream));
+        if (M <= 32) return kb == 4 ? launch_swapab<32, 4>(a, lda, w, ldw, args, stream)
+                                    : (kb == 2 ? launch_swapab<32, 2>(a, lda, w, ldw, args, stream)
+                                               : launch_swapab<32, 1>(a, lda, w, ldw, args, stream));
+        return kb == 4 ? launch_swapab<64, 4>(a, lda, w, ldw, args, stream)
+                       : (kb == 2 ? launch_swapab<64, 2>(a, lda, w, ldw, args, stream)
+                                  : launch_swapab<64, 1>(a, lda, w, ldw, args, stream));
+      }
     case 512:  // 256 x 256 pair tile on a CTA pair (cta_group::2)
       return launch_2sm(a, lda, w, ldw, args, stream);
     case 256:

@@ -54,7 +54,8 @@ def main():
     ]
     # K1 at small models: M = b * l rows (config 1: b4, l ~ 250), N = 2h, K = h; every tile shape
     # accumulates K in the same order (bit-identical), so the choice is free
-    for M, N, K in ((1000, 1536, 768), (4 * 64, 1536, 768), (32 * 250, 1536, 768), (4 * 880, 8192, 4096)):
+    for M, N, K in (() if "--swap-only" in sys.argv else
+                    ((1000, 1536, 768), (4 * 64, 1536, 768), (32 * 250, 1536, 768), (4 * 880, 8192, 4096))):
         for bn in (512, 256, 128, 64, 32):
             t = run(M, N, K, bn)
             print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "k1": True, "us": round(t * 1e6, 2),
@@ -62,10 +63,11 @@ def main():
     if "--k1-only" in sys.argv:
         return
     for M, N, K in shapes:
-        for bn in (-1, 32, 128, 0):
+        for bn in ((-1,) if "--swap-only" in sys.argv else (-1, 32, 128, 0)):
             for split in (False, True):
                 t = run(M, N, K, bn, ws=wsb if split else None)
                 print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "split_ws": split, "us": round(t * 1e6, 2),
+                                  "kbox": os.environ.get("KVPR_SWAP_KBOX", "default"),
                                   "weight_gbs": round(N * K * 2 / t / 1e9, 1)}), flush=True)
 
 

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--graph", type=int, default=-1, help="force executor graph mode (0/1); -1 = runtime default")
     ap.add_argument("--x-resident", action="store_true", help="row schedule: X resident in HBM (no X H2D)")
+    ap.add_argument("--nbuf", type=int, default=2, help="device staging buffers per category")
     ap.add_argument("--split", type=int, default=-2, help=">= 0: constant split l; -1: l = s' (all recompute)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -50,7 +51,8 @@ def main():
         splits = [args.prompt + i + 1 for i in range(len(splits))]
     w = OPTWeights.random(cfg, seed=0, device=dev)
     prompt = torch.randint(0, cfg.vocab, (args.batch, args.prompt), generator=torch.Generator().manual_seed(1))
-    rt = KVPRRuntime(w, args.batch, args.prompt + 4 * args.steps + 1, device=dev, x_resident=args.x_resident)
+    rt = KVPRRuntime(w, args.batch, args.prompt + 4 * args.steps + 1, device=dev, x_resident=args.x_resident,
+                     nbuf=args.nbuf)
     if args.graph >= 0 and hasattr(rt, "graph"):
         rt.graph = bool(args.graph)
     first = rt.prefill(prompt)
@@ -58,7 +60,7 @@ def main():
     rt.decode(splits[:K], tokens=first)  # warm-up
     torch.cuda.synchronize()
     out = {"model": args.model, "batch": args.batch, "prompt": args.prompt, "steps": K, "layers": cfg.layers,
-           "x_resident": args.x_resident, "split": args.split, "pdl": os.environ.get("KVPR_PDL", "1"),
+           "x_resident": args.x_resident, "split": args.split, "nbuf": args.nbuf, "pdl": os.environ.get("KVPR_PDL", "1"),
            "splits": splits[K:2 * K]}
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -28,12 +28,13 @@ if which in ("k2", "all"):
     ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
     for _ in range(2):
         kernels.decode_attention(q, pages, out, ws, b, 32, 128, s)
-if which in ("dec", "all"):
-    for n, k in ((3 * h, h), (h, h), (4 * h, h), (h, 4 * h)):
+if which in ("dec", "all"):  # decode projections as the executor issues them (swap-AB; split-K with ws)
+    wsb = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    for n, k, use_ws in ((3 * h, h, False), (h, h, True), (4 * h, h, True), (h, 4 * h, True)):
         a = torch.randn(b, k, device=dev).half()
         wt = (torch.randn(n, k, device=dev) * 0.02).half()
         o = torch.empty(b, n, device=dev).half()
         for _ in range(2):
-            kernels.linear_simple(a, wt, None, o)
+            kernels.linear_simple(a, wt, None, o, ws=wsb if use_ws else None)
 torch.cuda.synchronize()
 print("ok")
