@@ -194,6 +194,7 @@ typedef struct kvpr_decoder_desc {
   size_t ws_bytes;
   void *compute_stream, *h2d_stream, *d2h_stream;
   int chunk_rows; /* minimum positions per X chunk / K1 launch (runtime.KVPRRuntime.chunk_rows) */
+  int chunk_wave; /* > 0: X chunks are multiples of this many positions (whole K1 tile waves) */
 } kvpr_decoder_desc;
 
 int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);

@@ -102,9 +102,26 @@ inline int ck(cudaError_t e, const char* what) {
 }
 
 
-// chunk_bounds() of runtime.py: <= chunks contiguous ranges of >= min_rows positions when possible
-inline int chunk_bounds(int n, int chunks, int (*out)[2], int min_rows = 64) {
+// chunk_bounds() of runtime.py: <= chunks contiguous ranges of >= min_rows positions when possible;
+// with wave > 0 (and n >= wave) every range but the last is a multiple of wave positions
+inline int chunk_bounds(int n, int chunks, int (*out)[2], int min_rows = 64, int wave = 0) {
   if (n <= 0) return 0;
+  if (wave > 0 && n >= wave) {
+    const int waves = (n + wave - 1) / wave;
+    int per = wave * ((waves + chunks - 1) / chunks);
+    const int min_per = wave * ((min_rows + wave - 1) / wave);
+    if (per < min_per) per = min_per;
+    int c = 0;
+    for (int p = 0; p < n; p += per, ++c) {
+      out[c][0] = p;
+      out[c][1] = p + per < n ? p + per : n;
+    }
+    if (c > 1 && out[c - 1][1] - out[c - 1][0] < per / 2) {  // a short tail rides on the last chunk
+      out[c - 2][1] = n;
+      --c;
+    }
+    return c;
+  }
   int c = n >= min_rows ? n / min_rows : 1;
   if (c > chunks) c = chunks;
   if (c < 1) c = 1;
@@ -166,7 +183,7 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   char* kvd = static_cast<char*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * row;
   if (!d.x_resident) {
     int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d));
+    const int nc = chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d), d.chunk_wave);
     for (int c = 0; c < nc; ++c) {
       KV_TRY(ck(cudaMemcpyAsync(xd + cb[c][0] * row, static_cast<const char*>(Lw.host_x) + cb[c][0] * row,
                                 (cb[c][1] - cb[c][0]) * row, cudaMemcpyDefault, hs),
@@ -243,7 +260,7 @@ int compute(Decoder& D, int u, int base, const int* splits) {
   // K1 per landed chunk (one launch when X is resident)
   {
     int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb, chunk_rows(d));
+    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb, chunk_rows(d), d.x_resident ? 0 : d.chunk_wave);
     const __half* wkv = static_cast<const __half*>(Lw.wqkv) + static_cast<size_t>(h) * h;
     const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
     for (int c = 0; c < nc; ++c) {

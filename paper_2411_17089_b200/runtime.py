@@ -87,10 +87,20 @@ class DecodeTiming:
     layer_ms: list[list[float]] = field(default_factory=list)  # per step, per layer (consecutive layer ends)
 
 
-def chunk_bounds(n: int, chunks: int, min_rows: int = 64) -> list[tuple[int, int]]:
-    """Split [0, n) into <= chunks contiguous position ranges (>= min_rows each when possible)."""
+def chunk_bounds(n: int, chunks: int, min_rows: int = 64, wave: int = 0) -> list[tuple[int, int]]:
+    """Split [0, n) into <= chunks contiguous position ranges (>= min_rows each when possible).
+
+    wave > 0 (and n >= wave): every range but the last is a multiple of `wave` positions, so the
+    K1 launch of each full chunk is a whole number of tile waves (wave_positions())."""
     if n <= 0:
         return []
+    if wave > 0 and n >= wave:
+        per = wave * -(-(-(-n // wave)) // chunks)  # wave x ceil(ceil(n / wave) / chunks)
+        per = max(per, wave * -(-min_rows // wave))
+        out = [(p, min(n, p + per)) for p in range(0, n, per)]
+        if len(out) > 1 and out[-1][1] - out[-1][0] < per // 2:  # a short tail rides on the last chunk
+            out[-2:] = [(out[-2][0], n)]
+        return out
     c = max(1, min(chunks, n // min_rows if n >= min_rows else 1))
     base, rem = divmod(n, c)
     out, p = [], 0
@@ -101,12 +111,26 @@ def chunk_bounds(n: int, chunks: int, min_rows: int = 64) -> list[tuple[int, int
     return out
 
 
+def wave_positions(batch: int, hidden: int, sms: int, max_positions: int = 1024) -> int:
+    """Smallest position count whose K1 launch is whole waves of the CTA-pair kernel, else 0.
+
+    K1 over P positions is ceil(P*batch/256) x ceil(2h/256) tiles of 256 x 256 on sms/2 CTA pairs
+    (csrc/gemm_tcgen05.cu).  At OPT-6.7B b32 that is P = 296 (37 m-blocks x 32 n-blocks = 16 waves
+    of 74 pairs) instead of the 12.1 waves of an even 4-way split of l = 888, whose last wave runs
+    ~10% full."""
+    pairs, n_blk = sms // 2, -(-2 * hidden // 256)
+    for p in range(1, max_positions + 1):
+        if (p * batch) % 256 == 0 and ((p * batch // 256) * n_blk) % pairs == 0:
+            return p
+    return 0
+
+
 class KVPRRuntime:
     """One decoder replica on one GPU (the unit the batch-partitioned multi-GPU mode replicates)."""
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
                  chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None,
-                 x_resident: bool = False, chunk_rows: int | None = None):
+                 x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
 
         x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
@@ -124,6 +148,11 @@ class KVPRRuntime:
         # a K1 chunk carries >= 4 MiB of X (>= 64 positions): small models issue one X copy + one K1
         # per layer instead of paying per-call latency `chunks` times (tests lower it to cover chunking)
         self.chunk_rows = chunk_rows or max(64, -(-(4 << 20) // (batch * cfg.hidden * 2)))
+        # X chunks in whole K1 waves when the wave is short enough to still pipeline (<= l / 2)
+        if chunk_wave is None:
+            chunk_wave = 0 if chunk_rows else wave_positions(
+                batch, cfg.hidden, torch.cuda.get_device_properties(self.dev).multi_processor_count)
+        self.chunk_wave = chunk_wave
         _lib.load()
         h, b = cfg.hidden, batch
         with torch.cuda.device(self.dev):
@@ -307,7 +336,8 @@ class KVPRRuntime:
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         row = b * h * 2
         tr = self._trace
-        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows)):
+        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows,
+                                                  self.chunk_wave)):
             sp = tr.begin(hs, "load_activation_recompute", i + 1, j + 1, f"c{c}") if tr else None
             _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
             if sp:
@@ -358,7 +388,8 @@ class KVPRRuntime:
             tr.end(ds, sp)
         self.ev_d2h[r].record(ds)
         # K1: rebuild K,V[0:l) chunk by chunk as X lands (one launch when X is resident)
-        for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks, self.chunk_rows)):
+        for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks, self.chunk_rows,
+                                                  0 if self.x_resident else self.chunk_wave)):
             if not self.x_resident:
                 cs.wait_event(self.ev_x[r][c])
             sp = tr.begin(cs, "compute_recompute", I, J, f"c{c}") if tr else None
@@ -418,6 +449,7 @@ class KVPRRuntime:
         d.logits, d.tok, d.ws, d.ws_bytes = ptr(self.logits), ptr(self.tok), ptr(self.ws), self.ws.numel()
         d.compute_stream, d.h2d_stream, d.d2h_stream = self.cs.cuda_stream, self.hs.cuda_stream, self.ds.cuda_stream
         d.chunk_rows = self.chunk_rows
+        d.chunk_wave = self.chunk_wave
         h = ctypes.c_void_p()
         _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
         self._native_keep = (d, layers)

@@ -52,7 +52,8 @@ def test_ctypes_struct_layout_matches_c(tmp_path):
         'printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(kvpr_decoder_desc), offsetof(kvpr_decoder_desc, eps),'
         " offsetof(kvpr_decoder_desc, embed), offsetof(kvpr_decoder_desc, ws_bytes),"
         " offsetof(kvpr_decoder_desc, d2h_stream), sizeof(kvpr_layer_desc));"
-        ' printf("%zu\\n", offsetof(kvpr_decoder_desc, chunk_rows)); return 0;}'))
+        ' printf("%zu %zu\\n", offsetof(kvpr_decoder_desc, chunk_rows), offsetof(kvpr_decoder_desc, chunk_wave));'
+        ' return 0;}'))
     exe = tmp_path / "layout"
     subprocess.run([gcc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
@@ -60,7 +61,7 @@ def test_ctypes_struct_layout_matches_c(tmp_path):
     want = [ctypes.sizeof(E), E.seg_width.offset, E.ld.offset, E.seg.offset, E.scale.offset, E.scale_cols.offset,
             E.flags.offset, ctypes.sizeof(_lib.OutSeg),
             ctypes.sizeof(D), D.eps.offset, D.embed.offset, D.ws_bytes.offset, D.d2h_stream.offset,
-            ctypes.sizeof(_lib.LayerDesc), D.chunk_rows.offset]
+            ctypes.sizeof(_lib.LayerDesc), D.chunk_rows.offset, D.chunk_wave.offset]
     assert got == want
 
 

@@ -14,8 +14,8 @@ from paper_2411_17089_b200.weights import OPTConfig, OPTWeights
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("x_resident", [False, True])
-def test_native_equals_python_loop_bitwise(x_resident):
+@pytest.mark.parametrize("x_resident,wave", [(False, 0), (True, 0), (False, 24)])
+def test_native_equals_python_loop_bitwise(x_resident, wave):
     cfg = OPTConfig(hidden=512, layers=4, heads=8, ffn=2048, vocab=2048, max_pos=512)
     b, S0 = 3, 150
     splits = [75, 0, 152, 1, 154, 100, 3]
@@ -23,7 +23,7 @@ def test_native_equals_python_loop_bitwise(x_resident):
     prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(32))
     outs = []
     for native in (False, True):
-        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, chunk_rows=64)
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, chunk_rows=64, chunk_wave=wave)
         first = rt.prefill(prompt)
         toks = rt.decode(splits, tokens=first, keep_logits=True, native=native)
         torch.cuda.synchronize()

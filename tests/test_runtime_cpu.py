@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 from paper_2411_17089_b200 import multigpu
 from paper_2411_17089_b200.costmodel import WorkloadSpec, opt_preset
 from paper_2411_17089_b200.hwprofile import HardwareProfile
-from paper_2411_17089_b200.runtime import chunk_bounds
+from paper_2411_17089_b200.runtime import chunk_bounds, wave_positions
 from paper_2411_17089_b200.scheduler import solve_split
 
 
@@ -123,3 +123,19 @@ def test_parse_cpulist():
     assert multigpu.parse_cpulist("") == []
     with pytest.raises(ValueError):
         multigpu.parse_cpulist("4-2")
+
+
+def test_wave_positions_and_wave_chunks():
+    # OPT-6.7B b32 on 148 SMs: 296 positions = 37 pair m-blocks x 32 n-blocks = 16 waves of 74 pairs
+    assert wave_positions(32, 4096, 148) == 296
+    assert wave_positions(32, 5120, 148) == 296  # 13B: 40 n-blocks, still 37 m-blocks
+    assert wave_positions(4, 768, 148) == 0      # config 1: no whole-wave chunk under 1024 positions
+    for n, chunks in ((888, 4), (1000, 4), (1500, 4), (296, 4), (300, 2), (5000, 4)):
+        b = chunk_bounds(n, chunks, 64, wave=296)
+        assert b[0][0] == 0 and b[-1][1] == n and len(b) <= chunks
+        assert all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
+        assert all((p1 - p0) % 296 == 0 for p0, p1 in b[:-1])
+    assert chunk_bounds(888, 4, 64, wave=296) == [(0, 296), (296, 592), (592, 888)]
+    assert chunk_bounds(895, 4, 64, wave=296) == [(0, 296), (296, 592), (592, 895)]  # short tail merged
+    assert chunk_bounds(1100, 4, 64, wave=296) == [(0, 296), (296, 592), (592, 888), (888, 1100)]
+    assert chunk_bounds(200, 4, 64, wave=296) == chunk_bounds(200, 4, 64)  # shorter than a wave: even split
