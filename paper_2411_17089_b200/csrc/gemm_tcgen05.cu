@@ -159,19 +159,31 @@ __global__ void split_k_reduce_kernel(const GemmArgs p) {
   store_chunk_f(p, v, n0, row % p.row_group, row / p.row_group);
 }
 
-// Tile order: groups of `group` m-blocks, n-major inside a group, so the CTAs in flight share a
-// band of A (reused across n from L2) and stream each B column block once per group.  Odd groups
-// sweep n backwards, so a group starts on the B blocks the previous one just left in L2.  The
-// band (kABandBytes) is sized to stay L2-resident: at K1's config-2 chunk, 16 pair m-blocks
-// (32 MB of A) measured best; 24 or all 28 thrash (DRAM reads 208 -> 326 MB, profiles/).
+// Tile order.  group > 0: bands of `group` m-blocks, n-major inside a band, so the CTAs in flight
+// share the band's A (reused across n from L2) while B streams past once per band.  group < 0:
+// bands of -group n-blocks, m-major inside, so the band's B stays in L2 while A streams once per
+// band.  The host picks the orientation with fewer DRAM reads and sizes the band to stay
+// L2-resident (kABandBytes: 16 pair blocks = 32 MB at K = 4096 measured best; 24 or all thrash).
+// Odd bands sweep backwards, so a band starts on the blocks the previous one just left in L2.
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group, int& m_blk, int& n_blk) {
-  const int per_group = group * num_n;
-  const int g = tile / per_group;
-  const int first_m = g * group;
-  const int gm = min(group, num_m - first_m);
-  const int local = tile - g * per_group;
-  m_blk = first_m + local % gm;
-  n_blk = (g & 1) ? num_n - 1 - local / gm : local / gm;
+  if (group > 0) {
+    const int per_group = group * num_n;
+    const int g = tile / per_group;
+    const int first_m = g * group;
+    const int gm = min(group, num_m - first_m);
+    const int local = tile - g * per_group;
+    m_blk = first_m + local % gm;
+    n_blk = (g & 1) ? num_n - 1 - local / gm : local / gm;
+  } else {
+    const int gsz = -group;
+    const int per_group = gsz * num_m;
+    const int g = tile / per_group;
+    const int first_n = g * gsz;
+    const int gn = min(gsz, num_n - first_n);
+    const int local = tile - g * per_group;
+    n_blk = first_n + local % gn;
+    m_blk = (g & 1) ? num_m - 1 - local / gn : local / gn;
+  }
 }
 
 template <int BN>
@@ -823,13 +835,20 @@ static int swap_kbox() {
   return v;
 }
 
-// m-blocks per rasterization group: the A band of a group stays in L2 while B streams past it
-static int band_group(int num_m_blk, long long band_bytes_per_m_blk) {
-  const char* e = getenv("KVPR_GEMM_GROUP_M");  // experiment override
-  if (e != nullptr && atoi(e) > 0) return atoi(e) < num_m_blk ? atoi(e) : num_m_blk;
-  long long g = kABandBytes / (band_bytes_per_m_blk > 0 ? band_bytes_per_m_blk : 1);
-  if (g < 1) g = 1;
-  return static_cast<int>(g < num_m_blk ? g : num_m_blk);
+// Rasterization band (tile_coords): +g = bands of g m-blocks (B re-read once per band), -g =
+// bands of g n-blocks (A re-read once per band); whichever reads less from DRAM.  blk_bytes is
+// one m-block of A = one n-block of B (both rows x K fp16 for square tiles).
+static int band_group(int num_m_blk, int num_n_blk, long long a_blk_bytes, long long b_blk_bytes) {
+  const char* e = getenv("KVPR_GEMM_GROUP_M");  // experiment override (negative: n-bands)
+  if (e != nullptr && atoi(e) != 0) return atoi(e);
+  long long gm = kABandBytes / (a_blk_bytes > 0 ? a_blk_bytes : 1);
+  long long gn = kABandBytes / (b_blk_bytes > 0 ? b_blk_bytes : 1);
+  gm = gm < 1 ? 1 : (gm > num_m_blk ? num_m_blk : gm);
+  gn = gn < 1 ? 1 : (gn > num_n_blk ? num_n_blk : gn);
+  const long long a_all = a_blk_bytes * num_m_blk, b_all = b_blk_bytes * num_n_blk;
+  const long long reads_m = a_all + b_all * ((num_m_blk + gm - 1) / gm);
+  const long long reads_n = b_all + a_all * ((num_n_blk + gn - 1) / gn);
+  return reads_n < reads_m ? -static_cast<int>(gn) : static_cast<int>(gm);
 }
 
 template <int BN>
@@ -844,7 +863,8 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
   args.num_m_blk = (args.M + kBM - 1) / kBM;
   args.num_n_blk = (args.N + BN - 1) / BN;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
-  args.group_m = band_group(args.num_m_blk, static_cast<long long>(kBM) * args.K * 2);
+  args.group_m = band_group(args.num_m_blk, args.num_n_blk, static_cast<long long>(kBM) * args.K * 2,
+                            static_cast<long long>(BN) * args.K * 2);
   const int splits = args.k_splits > 1 ? args.k_splits : 1;
   const int tiles = args.num_m_blk * args.num_n_blk * splits;
   int dev = 0;
@@ -903,7 +923,8 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
   args.num_m_blk = (args.M + 2 * kBM - 1) / (2 * kBM);
   args.num_n_blk = (args.N + k2BN - 1) / k2BN;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
-  args.group_m = band_group(args.num_m_blk, static_cast<long long>(2 * kBM) * args.K * 2);
+  args.group_m = band_group(args.num_m_blk, args.num_n_blk, static_cast<long long>(2 * kBM) * args.K * 2,
+                            static_cast<long long>(k2BN) * args.K * 2);
   const int tiles = args.num_m_blk * args.num_n_blk;
   int dev = 0;
   cudaGetDevice(&dev);

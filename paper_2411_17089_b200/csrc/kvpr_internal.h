@@ -30,7 +30,7 @@ struct GemmArgs {
   int k_splits;    // > 1: each CTA reduces a K slice into ws; a second kernel applies the epilogue
   float* ws;       // split-K partials [k_splits][M][ws_ld] fp32
   int ws_ld;
-  int group_m;     // m-blocks per rasterization group (tile_coords)
+  int group_m;     // rasterization band (tile_coords): > 0 m-blocks per band, < 0 n-blocks per band
 };
 
 int sm_count(int device);

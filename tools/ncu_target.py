@@ -14,8 +14,8 @@ which = sys.argv[1] if len(sys.argv) > 1 else "all"
 dev = torch.device("cuda:0")
 b, h, l, s = 32, 4096, 882, 1025
 pages = torch.randn(1056, 2, b, h, device=dev).half()
-if which == "k1chunk":  # one of the runtime's 4 X chunks at config 2 (l ~ 870 -> ~218 positions)
-    l = 218
+if which == "k1chunk":  # one of the runtime's wave-aligned X chunks at config 2 (runtime.wave_positions: 296)
+    l = 296
 if which in ("k1", "k1chunk", "all"):
     x = torch.randn(l, b, h, device=dev).half()
     w = (torch.randn(2 * h, h, device=dev) * 0.02).half()
