@@ -164,8 +164,9 @@ def run_reference(args):
 
 class Clocks:
     def __init__(self):
+        self.nvml = []
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("pci.bus_id,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -174,21 +175,52 @@ class Clocks:
         except Exception:
             self.p = None
 
-    def stop(self, gpu_index=0):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
+    @staticmethod
+    def _pci(gpu_index):
+        """The CUDA device's PCI address (nvidia-smi / NVML enumerate in their own order)."""
+        from paper_2411_17089_b200.multigpu import pci_address
+
+        return pci_address(gpu_index)
+
+    def sample_now(self, gpu_index=0):
+        """One in-process NVML sample (for timed regions shorter than nvidia-smi's 200 ms period):
+        call it while the GPU is busy with the timed work."""
         try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(self._pci(gpu_index).encode())
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                     "sw_power_cap": 0x4}
+            self.nvml.append((float(sm), float(mx), sorted(n for n, bit in names.items() if r & bit)))
+        except Exception as e:  # pragma: no cover - best effort
+            self.nvml_error = str(e)
+
+    def stop(self, gpu_index=0):
+        if self.p is None and not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
         self.f.flush()
         rows = []
+        pci = self._pci(gpu_index)
         for line in Path(self.f.name).read_text().splitlines():
             c = [x.strip() for x in line.split(",")]
-            if len(c) >= 9 and c[0].isdigit() and int(c[0]) == gpu_index:
+            if len(c) >= 9 and c[0].lower().endswith(pci[-12:].lower()):
                 rows.append(c)
         if not rows:
+            if self.nvml:  # region shorter than the nvidia-smi period: the in-process NVML samples
+                sm = sorted(x[0] for x in self.nvml)
+                return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.nvml[0][1],
+                        "reasons": sorted({n for x in self.nvml for n in x[2]}), "samples": len(sm),
+                        "source": "nvml in-process (timed region shorter than the nvidia-smi period)"}
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = sorted(float(r[1]) for r in rows)
         reasons = set()
@@ -289,23 +321,34 @@ def run_kvpr(args):
         dist.barrier()
     clocks = Clocks() if rank == 0 else None
     launches0 = rt.launches
-    tim = DecodeTiming()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
-    if hasattr(rt, "kernel_timing"):
-        rt.kernel_timing = []  # CUDA events around every K1 / K2 launch of the timed steps
+    # the timed region: K steps as a user runs them (no per-kernel instrumentation on the path)
     start.record(rt.cs)
-    rt.decode(splits[args.warmup:], timing=tim)
+    rt.decode(splits[args.warmup:])
     end.record(rt.cs)
+    if clocks:
+        clocks.sample_now(gpu)  # the decode is enqueued and running
     torch.cuda.synchronize(dev)
     launches = rt.launches - launches0
-    kstats = rt.kernel_stats() if hasattr(rt, "kernel_stats") else {}
-    if hasattr(rt, "kernel_timing"):
-        rt.kernel_timing = None
     elapsed = start.elapsed_time(end) / 1e3
     clk = clocks.stop(gpu) if clocks else None
     elapsed = allreduce([elapsed])[0]
     value = gb * args.steps / elapsed  # every rank's slice, over the slowest rank's time
+
+    # instrumented replay of the same K steps (same splits, same start length): CUDA events around
+    # every K1 / K2 launch and after every layer give the per-layer latency and the kernel rooflines
+    tim = DecodeTiming()
+    kstats = {}
+    if hasattr(rt, "reset"):
+        rt.reset(args.prompt + args.warmup)
+        if hasattr(rt, "kernel_timing"):
+            rt.kernel_timing = []
+        rt.decode(splits[args.warmup:], timing=tim)
+        torch.cuda.synchronize(dev)
+        kstats = rt.kernel_stats() if hasattr(rt, "kernel_stats") else {}
+        if hasattr(rt, "kernel_timing"):
+            rt.kernel_timing = None
 
     # per-layer latency and overlap roofline over the timed steps
     L = cfg.layers
