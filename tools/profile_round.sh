@@ -5,7 +5,7 @@ set -u
 tag=${1:-r01}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/${tag}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-alt --no-cpu-baseline > gpurun_out/${tag}_launches_bench.log 2>&1
+    python bench.py --steps 2 --warmup 1 --no-alt --no-cpu-baseline --fixed-profile > gpurun_out/${tag}_launches_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm_tcgen05_2sm -s 1 -c 1 -o gpurun_out/${tag}_k1_chunk \
     python tools/ncu_target.py k1chunk > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decode_attn_kernel -s 1 -c 1 -o gpurun_out/${tag}_k2 \
