@@ -839,8 +839,12 @@ static int swap_kbox() {
 // bands of g n-blocks (A re-read once per band); whichever reads less from DRAM.  blk_bytes is
 // one m-block of A = one n-block of B (both rows x K fp16 for square tiles).
 static int band_group(int num_m_blk, int num_n_blk, long long a_blk_bytes, long long b_blk_bytes) {
-  const char* e = getenv("KVPR_GEMM_GROUP_M");  // experiment override (negative: n-bands)
-  if (e != nullptr && atoi(e) != 0) return atoi(e);
+  static int forced = -1000000;  // experiment override KVPR_GEMM_GROUP_M (negative: n-bands), read once
+  if (forced == -1000000) {
+    const char* e = getenv("KVPR_GEMM_GROUP_M");
+    forced = e != nullptr ? atoi(e) : 0;
+  }
+  if (forced != 0) return forced;
   long long gm = kABandBytes / (a_blk_bytes > 0 ? a_blk_bytes : 1);
   long long gn = kABandBytes / (b_blk_bytes > 0 ? b_blk_bytes : 1);
   gm = gm < 1 ? 1 : (gm > num_m_blk ? num_m_blk : gm);

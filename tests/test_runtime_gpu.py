@@ -244,3 +244,41 @@ def test_decode_orders_after_callers_token_copy():
     got = rt.decode([3], tokens=t).cpu()
     rt.close()
     assert torch.equal(got, ref)
+
+
+def test_full_size_output_independent_of_split_and_rebuild_exact(criterion):
+    """BASELINE config-2 layer shapes (OPT-6.7B widths, b32, prompt 1024; 2 layers to bound the test):
+    size-independent properties at full size.  (1) K1 rebuilding X[0:1024) of a layer (32768 rows, CTA
+    pairs, n-band rasterization) equals the prefill's stored K/V bit for bit; (2) the decode is
+    bit-identical for l = 0, the solver's l (wave-aligned X chunks) and l = s'."""
+    cfg = OPTConfig(hidden=4096, layers=2, heads=32, ffn=16384).with_positions(1040)
+    batch, S0, steps = 32, 1024, 3
+    w, prompt = _setup(cfg, batch, S0, seed=7, std=0.02, emb_std=0.02)
+    wl = WorkloadSpec(batch_size=batch, prompt_len=S0, gen_len=steps)
+    plans = {
+        "naive": constant_plan(wl, "column", 0).splits,
+        "solver": plan_generation(cfg.spec(), wl, B200_GUESS, "column").splits,
+        "full": constant_plan(wl, "column", S0 + steps).splits,
+    }
+    assert 0 < plans["solver"][0] < S0
+    outs = {}
+    for name, splits in plans.items():
+        rt = KVPRRuntime(w, batch, S0 + steps + 1)
+        assert rt.chunk_wave == 296
+        first = rt.prefill(prompt)
+        if name == "naive":
+            x = rt.stores.x[1][:S0].cuda()
+            pages = torch.empty(S0 + steps + 1, 2, batch, cfg.hidden, dtype=torch.float16, device="cuda")
+            kernels.recompute_kv(x, w.layers[1].w_kv, w.layers[1].b_kv, pages, batch, 0, S0)
+            torch.cuda.synchronize()
+            assert torch.equal(pages[:S0], rt.stores.kv[1][:S0].cuda())
+        toks = rt.decode(splits, tokens=first, keep_logits=True)
+        torch.cuda.synchronize()
+        outs[name] = (toks.cpu(), rt.last_logits.cpu())
+        rt.close()
+    ref_t, ref_l = outs["naive"]
+    for name, (t, lg) in outs.items():
+        assert torch.equal(t, ref_t), name
+        assert torch.equal(lg, ref_l), f"{name}: logits differ by {(lg - ref_l).abs().max().item()}"
+    criterion("G4", "config-2 shapes (h4096 b32 s1024): K1 rebuild == stored K/V bitwise; decode bit-identical "
+              f"for l = 0, solver l {plans['solver']}, l = s'", True)
