@@ -424,21 +424,42 @@ def run_kvpr(args):
         kern["k2_decode_attention_standalone"] = {"bound": "hbm", "achieved": by / t_k2 / 1e9, "peak": peaks["hbm_gbs"],
                                        "unit": "GB/s", "frac": by / t_k2 / 1e9 / peaks["hbm_gbs"], "traffic": None,
                                        "us": t_k2 * 1e6}
-        # In the step, K2 always runs while the copy engine streams the next layer's X / KV into HBM
-        # (that is the overlap).  Same launch with a host->device DMA in flight on the H2D stream:
-        # the HBM ceiling K2 actually has inside the step (tools/k2_probe.py isolates the effect).
+        # In the step, K2 is ONE launch per layer and always runs while the copy engine streams the
+        # next layer's X / KV into HBM (that is the overlap).  Its ceiling there: single launches
+        # (each timed alone, median; back-to-back launches overlap their ramp and tail under PDL)
+        # with a host->device DMA in flight on the H2D stream (tools/k2_probe.py isolates the effect).
+        def single_time(fn, reps=9):
+            ts = []
+            for _ in range(reps):
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(rt.cs)
+                fn()
+                e.record(rt.cs)
+                e.synchronize()
+                ts.append(a.elapsed_time(e) / 1e3)
+            return sorted(ts)[len(ts) // 2]
+
+        k2_call = lambda: kernels.decode_attention(rt.q, kvd, rt.attn, rt.ws, b, cfg.heads,  # noqa: E731
+                                                   cfg.head_dim, s, stream=rt.cs)
+        t_k2s = single_time(k2_call)
+        kern["k2_decode_attention_single_launch"] = {"bound": "hbm", "achieved": by / t_k2s / 1e9,
+                                                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                                     "frac": by / t_k2s / 1e9 / peaks["hbm_gbs"],
+                                                     "us": t_k2s * 1e6}
         if hasattr(rt, "stores") and rt.stores.x is not None and rt.nbuf > 1:
             src = rt.stores.x[1]
             n = min(src.numel() * src.element_size(), rt.x_dev[1].numel() * rt.x_dev[1].element_size())
             rt.hs.wait_stream(rt.cs)
             _lib.call("kvpr_copy_async", rt.x_dev[1].data_ptr(), src.data_ptr(), n, rt.hs.cuda_stream)
-            t_k2c = ev_time(lambda: kernels.decode_attention(rt.q, kvd, rt.attn, rt.ws, b, cfg.heads, cfg.head_dim,
-                                                             s, stream=rt.cs))
+            t0_dma = time.perf_counter()
+            t_k2c = single_time(k2_call)
+            span = time.perf_counter() - t0_dma
             rt.hs.synchronize()
-            if n / 55e9 > 13 * t_k2c:  # the DMA outlasted all 13 launches
-                kern["k2_decode_attention_standalone_dma"] = {
+            if n / 55e9 > span:  # the DMA outlasted all the timed launches
+                kern["k2_decode_attention_single_launch_dma"] = {
                     "bound": "hbm", "achieved": by / t_k2c / 1e9, "unit": "GB/s", "us": t_k2c * 1e6,
-                    "dma_bytes": n, "note": "same launch with a concurrent pinned H2D on the copy engine"}
+                    "dma_bytes": n, "note": "single launches with a concurrent pinned H2D on the copy engine "
+                                            "(the in-step condition)"}
 
     # e2e through the public per-step API (host token ids in/out every step)
     rt.reset(args.prompt + args.warmup)
@@ -554,11 +575,12 @@ def run_kvpr(args):
         kern["k2_decode_attention_in_step"] = {"bound": "hbm", "achieved": by / t / 1e9, "peak": peaks["hbm_gbs"],
                                                "unit": "GB/s", "frac": by / t / 1e9 / peaks["hbm_gbs"],
                                                "launches": n, "us_per_launch": t * 1e6}
-        if "k2_decode_attention_standalone_dma" in kern:
-            c = kern["k2_decode_attention_standalone_dma"]["achieved"]
+        if "k2_decode_attention_single_launch_dma" in kern:
+            c = kern["k2_decode_attention_single_launch_dma"]["achieved"]
             kern["k2_decode_attention_in_step"].update(
                 {"frac_vs_dma_ceiling": by / t / 1e9 / c,
-                 "note": "frac_vs_dma_ceiling: vs the same launch timed with a concurrent H2D (the in-step condition)"})
+                 "note": "frac_vs_dma_ceiling: vs single launches of the same K2 timed with a concurrent H2D "
+                         "(the in-step condition)"})
 
     if rank == 0:
         line = {

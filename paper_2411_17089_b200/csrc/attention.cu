@@ -19,6 +19,8 @@
 
 #include <math.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kvpr_internal.h"
 
@@ -349,8 +351,14 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
   int dev = 0;
   cudaGetDevice(&dev);
   const int bh = batch * heads;
-  // enough CTAs for ~8 resident per SM, each split at least 64 positions
-  const int target = 8 * sm_count(dev);
+  // CTAs per SM the split-KV grid aims for (each split >= 64 positions); KVPR_K2_CTAS_PER_SM
+  // overrides for experiments
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const char* e = getenv("KVPR_K2_CTAS_PER_SM");
+    per_sm = (e != nullptr && atoi(e) > 0) ? atoi(e) : 8;
+  }
+  const int target = per_sm * sm_count(dev);
   int splits = (target + bh - 1) / bh;
   const int max_by_len = (seq_len + 63) / 64;
   if (splits > max_by_len) splits = max_by_len;
