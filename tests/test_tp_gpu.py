@@ -65,13 +65,17 @@ def _port():
         return s.getsockname()[1]
 
 
-def _tp_worker(rank, world, port, q):
+def _tp_worker(rank, world, port, q, shared=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    gpu = 0 if shared else rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    if shared:  # both ranks on one B200: NCCL refuses duplicate devices, gloo moves the CUDA tensors
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     try:
         rt = TPRuntime(_weights(dev), B, S0 + len(SPLITS) + 1, block=16, device=dev)
         first = rt.prefill(_prompt())
@@ -83,14 +87,18 @@ def _tp_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_tp_world2_matches_unsharded():
+@pytest.mark.parametrize("shared", [False, True])
+def test_tp_world2_matches_unsharded(shared):
+    """world 2: on two GPUs over NCCL, or (shared) both ranks on cuda:0 over gloo, which exercises the
+    sharded data flow (column/row-parallel kernels, X rounds, all-gathers, all-reduces) on a 1-GPU box."""
+    if not shared and torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
     f0, t0, l0 = _reference()
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q, shared)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
