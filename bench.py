@@ -590,7 +590,8 @@ def run_kvpr(args):
             "config": {
                 "workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV+X offloaded to pinned host",
                 "model": args.model, "global_batch": gb, "batch_per_gpu": b, "seq_len": args.prompt,
-                "parallelism": f"tp{ws} (head-sharded, NCCL)" if args.tp else f"batch-partition x{ws}",
+                "parallelism": (f"tp{ws} (head-sharded, {dist.get_backend().upper() if ws > 1 else 'NCCL'})"
+                                if args.tp else f"batch-partition x{ws}"),
                 "mode": "column", "splits_timed": splits[args.warmup:],
                 "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
                 "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
