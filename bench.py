@@ -601,6 +601,7 @@ def run_kvpr(args):
             "overlap_roofline": {
                 "bound": "pcie", "achieved": achieved_gbs, "peak": bw_peak / 1e9, "unit": "GB/s",
                 "frac": troof / elapsed, "traffic": None,
+                "achieved_vs_gen5_x16_nominal": achieved_gbs / 64.0,
                 "note": "north-star per-layer overlap roofline max(H2D(X[:, :l]+KV[l:s'-1]) / measured pinned H2D "
                         "peak, 4bl h^2 / sustained bf16 peak); frac = T_roof / T_measured over the timed steps",
             },
