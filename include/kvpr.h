@@ -216,6 +216,39 @@ int kvpr_decoder_timeline(void* handle, float* layer_ms, int layer_cap, float* s
 /* Kernel launches (ABI-level) the executor has issued so far. */
 long long kvpr_decoder_launches(void* handle);
 
+/* ---------------------------------------------------------------------------------------------
+ * Fused tensor-parallel projection + all-reduce over peer memory (config 4: head-sharded OPT-30B;
+ * replaces the reference-less NCCL all-reduce after the row-parallel out-proj / fc2).
+ * Peer buffers are CUDA IPC allocations: every rank allocates one region with kvpr_ipc_alloc,
+ * the host exchanges the handles (torch.distributed object all-gather) and opens the peers'
+ * regions with kvpr_ipc_open (cudaIpcMemLazyEnablePeerAccess: NVLink P2P between GPUs). */
+#define KVPR_TP_MAX_WORLD 8
+#define KVPR_TP_MAX_TILES 512
+
+typedef struct kvpr_tp_peers {
+  int rank, world;                     /* 2 <= world <= KVPR_TP_MAX_WORLD */
+  void* recv[KVPR_TP_MAX_WORLD];       /* every rank's receive slots: [world][M][N] fp32 */
+  float* resid[KVPR_TP_MAX_WORLD];     /* every rank's residual [M][N] fp32 (identical before the call) */
+  unsigned* flags[KVPR_TP_MAX_WORLD];  /* every rank's flags: [world][512] push + [512] broadcast, zeroed once */
+  unsigned* err;                       /* this rank's error word: nonzero after a peer wait timed out (5 s) */
+} kvpr_tp_peers;
+
+size_t kvpr_ipc_handle_bytes(void);
+/* cudaMalloc + zero + cudaIpcGetMemHandle; handle receives kvpr_ipc_handle_bytes() bytes */
+int kvpr_ipc_alloc(size_t bytes, void** dptr, void* handle);
+int kvpr_ipc_open(const void* handle, void** dptr);
+int kvpr_ipc_close(void* dptr);
+int kvpr_ipc_free(void* dptr);
+
+/* On every rank r of peers->world, with the same residual R on all ranks before the call:
+ *   R[m, n] <- R[m, n] + (sum_r A_r[m, :] . W_r[n, :] + bias[n])     (M <= 64, fp32 residual)
+ * A_r [M, K] fp16 and W_r [N, K] fp16 are rank r's K slices (row-parallel weights).  Two kernels on
+ * `stream`: the swap-AB GEMM pushing each 128-column tile's partial to its owner (tile % world), and
+ * the owners' rank-ordered sum + broadcast into every residual (deterministic).  `epoch` must grow
+ * by one per call on every rank (same value on all ranks).  Replaces kvpr_linear_ws + all-reduce. */
+int kvpr_linear_allreduce(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                          const void* bias, const kvpr_tp_peers* peers, unsigned epoch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,7 +49,16 @@ EXPORTS = (
     "kvpr_decoder_kernel_stats",
     "kvpr_decoder_timeline",
     "kvpr_decoder_launches",
+    "kvpr_ipc_handle_bytes",
+    "kvpr_ipc_alloc",
+    "kvpr_ipc_open",
+    "kvpr_ipc_close",
+    "kvpr_ipc_free",
+    "kvpr_linear_allreduce",
 )
+
+TP_MAX_WORLD = 8
+TP_MAX_TILES = 512
 
 
 class OutSeg(ctypes.Structure):
@@ -86,6 +95,12 @@ class DecoderDesc(ctypes.Structure):
 
 _lib: ctypes.CDLL | None = None
 
+class TpPeers(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("recv", ctypes.c_void_p * TP_MAX_WORLD), ("resid", ctypes.c_void_p * TP_MAX_WORLD),
+                ("flags", ctypes.c_void_p * TP_MAX_WORLD), ("err", ctypes.c_void_p)]
+
+
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
 _ll = ctypes.c_longlong
@@ -117,6 +132,13 @@ _SIGS = {
                                    ctypes.POINTER(ctypes.c_double)], _i),
     "kvpr_decoder_timeline": ([_vp, ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(ctypes.c_float), _i], _i),
     "kvpr_decoder_launches": ([_vp], _ll),
+    "kvpr_ipc_handle_bytes": ([], _sz),
+    "kvpr_ipc_alloc": ([_sz, ctypes.POINTER(_vp), _vp], _i),
+    "kvpr_ipc_open": ([_vp, ctypes.POINTER(_vp)], _i),
+    "kvpr_ipc_close": ([_vp], _i),
+    "kvpr_ipc_free": ([_vp], _i),
+    "kvpr_linear_allreduce": ([_vp, _ll, _vp, _ll, _i, _i, _i, _vp, ctypes.POINTER(TpPeers), ctypes.c_uint, _vp],
+                              _i),
 }
 
 

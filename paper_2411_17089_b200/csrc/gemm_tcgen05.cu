@@ -28,7 +28,6 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
 constexpr int kBnSwapAB = -1;  // gemm_f16 tile code of the swapped-operand decode GEMM
 constexpr long long kABandBytes = 32ll << 20;
-constexpr int kSwapKBoxDefault = 1;  // L2-resident A band of one rasterization group
 
 // The 1-CTA ring is sized at launch: stage = A box (a_box_rows x 128 B: 16 KB, or only the live
 // rows of a small-M decode GEMM) + B box (BN x 128 B), as many stages as fit in shared memory
@@ -741,6 +740,25 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained into registers
       const int n = n_blk * kBM + q * 32 + lane;
+      if (p.tp_world > 1) {
+        // fused TP all-reduce, push half (csrc/tpcomm.cu): the raw fp32 partial of this tile goes
+        // straight into slot [rank] of the tile owner's receive buffer over NVLink, then the owner's
+        // flag for (rank, tile) is released at system scope
+        const int owner = n_blk % p.tp_world;
+        if (n < p.N) {
+          float* o = p.tp_recv[owner] + static_cast<long long>(p.tp_rank) * p.M * p.N + n;
+#pragma unroll
+          for (int m = 0; m < MP; ++m)
+            if (m < p.M) o[static_cast<long long>(m) * p.N] = __uint_as_float(r[m]);
+        }
+        __threadfence_system();
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this tile
+        if (threadIdx.x == 128) {
+          unsigned* f = p.tp_flags[owner] + p.tp_rank * kTpMaxTiles + n_blk;
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(p.tp_epoch) : "memory");
+        }
+        continue;
+      }
       if (n < p.N) {
         if (splits > 1) {
           float* o = p.ws + static_cast<long long>(ks) * p.M * p.ws_ld + n;
@@ -1053,6 +1071,39 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
       set_error("gemm: unsupported BN=%d", bn);
       return KVPR_EINVAL;
   }
+}
+
+}  // namespace kvpr
+
+namespace kvpr {
+
+// Push half of the fused TP all-reduce: the swap-AB decode GEMM whose epilogue stores raw fp32
+// partials into the tile owners' receive slots and releases their flags (csrc/tpcomm.cu).
+int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                     const GemmArgs& tp, cudaStream_t stream) {
+  if (M <= 0 || M > 64 || N <= 0 || K <= 0 || N % 32 != 0 || K % 8 != 0 || lda % 8 != 0 || ldw % 8 != 0) {
+    set_error("linear_allreduce: need 0 < M <= 64, N %% 32 == 0, K %% 8 == 0 (M=%d N=%d K=%d)", M, N, K);
+    return KVPR_EINVAL;
+  }
+  if ((N + kBM - 1) / kBM > kTpMaxTiles) {
+    set_error("linear_allreduce: N=%d exceeds %d tiles of %d", N, kTpMaxTiles, kBM);
+    return KVPR_EINVAL;
+  }
+  GemmArgs args = tp;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.k_splits = 1;
+  args.ws = nullptr;
+  args.seg_width = ((N + 31) / 32) * 32;
+  args.row_group = M;
+  const int kb = swap_kbox() > 0 ? swap_kbox() : (M <= 16 ? 4 : 2);
+  if (M <= 16) return kb == 4 ? launch_swapab<16, 4>(a, lda, w, ldw, args, stream)
+                              : launch_swapab<16, 2>(a, lda, w, ldw, args, stream);
+  if (M <= 32) return kb == 4 ? launch_swapab<32, 4>(a, lda, w, ldw, args, stream)
+                              : launch_swapab<32, 2>(a, lda, w, ldw, args, stream);
+  return kb == 4 ? launch_swapab<64, 4>(a, lda, w, ldw, args, stream)
+                 : launch_swapab<64, 2>(a, lda, w, ldw, args, stream);
 }
 
 }  // namespace kvpr

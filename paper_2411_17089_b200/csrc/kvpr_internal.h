@@ -10,6 +10,9 @@
 
 namespace kvpr {
 
+constexpr int kTpMaxWorld = 8;     // ranks of one fused TP all-reduce (one NVSwitch domain slice)
+constexpr int kTpMaxTiles = 512;   // 128-column tiles of N per fused all-reduce (N <= 65536)
+
 // Epilogue + shape bundle for the tcgen05 GEMM (passed by value as a kernel arg).
 //   out address of (m, n) = seg_ptr[n / seg_width]
 //                         + (m % row_group) * ld + (m / row_group) * seg_group_stride[seg]
@@ -31,6 +34,11 @@ struct GemmArgs {
   float* ws;       // split-K partials [k_splits][M][ws_ld] fp32
   int ws_ld;
   int group_m;     // rasterization band (tile_coords): > 0 m-blocks per band, < 0 n-blocks per band
+  // fused TP all-reduce (swap-AB kernel only; tp_world > 1): raw partials pushed to the tile owner
+  int tp_rank, tp_world;
+  unsigned tp_epoch;
+  float* tp_recv[kTpMaxWorld];     // per rank: receive slots [world][M][N] fp32
+  unsigned* tp_flags[kTpMaxWorld];  // per rank: push flags [world][kTpMaxTiles]
 };
 
 int sm_count(int device);
@@ -38,6 +46,9 @@ void clear_error();
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0);
+
+int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
+                     const GemmArgs& tp, cudaStream_t stream);
 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch,
                      int heads, int head_dim, int seq_len, float scale, cudaStream_t stream);

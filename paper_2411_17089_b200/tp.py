@@ -127,11 +127,108 @@ def shard_layer(lw: LayerWeights, lay: TPLayout) -> LayerWeights:
     )
 
 
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class PeerBuffers:
+    """Symmetric peer memory for the fused TP all-reduce (csrc/tpcomm.cu, kvpr_linear_allreduce).
+
+    Every rank allocates one CUDA IPC region [receive slots world x M x N fp32 | residual M x N fp32 |
+    flags | error word], the handles are all-gathered over the process group, and every rank opens
+    its peers' regions (NVLink P2P between GPUs; also valid for ranks sharing one GPU).  `resid` is
+    this rank's residual as a torch tensor: the decode keeps its residual stream there, so the owners'
+    broadcasts land in place.
+    """
+
+    def __init__(self, M: int, N: int, group=None, device: torch.device | None = None):
+        import ctypes
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if not 2 <= self.world <= _lib.TP_MAX_WORLD:
+            raise ValueError(f"fused all-reduce needs 2..{_lib.TP_MAX_WORLD} ranks, got {self.world}")
+        if M > 64 or -(-N // 128) > _lib.TP_MAX_TILES:
+            raise ValueError(f"fused all-reduce: M={M} > 64 or N={N} beyond {_lib.TP_MAX_TILES} tiles")
+        self.M, self.N = M, N
+        lib = _lib.load()
+        al = lambda x: -(-x // 256) * 256  # noqa: E731
+        self.off_recv = 0
+        self.off_resid = al(self.world * M * N * 4)
+        self.off_flags = self.off_resid + al(M * N * 4)
+        self.off_err = self.off_flags + al((_lib.TP_MAX_WORLD + 1) * _lib.TP_MAX_TILES * 4)
+        total = self.off_err + 256
+        hb = lib.kvpr_ipc_handle_bytes()
+        handle = (ctypes.c_char * hb)()
+        base = ctypes.c_void_p()
+        _lib.check(lib.kvpr_ipc_alloc(total, ctypes.byref(base), handle), "kvpr_ipc_alloc")
+        self._own = base.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self._opened = []
+        bases = []
+        for r, hnd in enumerate(handles):
+            if r == self.rank:
+                bases.append(self._own)
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_char * hb).from_buffer_copy(hnd)
+            _lib.check(lib.kvpr_ipc_open(buf, ctypes.byref(p)), "kvpr_ipc_open")
+            self._opened.append(p.value)
+            bases.append(p.value)
+        pe = _lib.TpPeers()
+        pe.rank, pe.world = self.rank, self.world
+        for r, bp in enumerate(bases):
+            pe.recv[r] = bp + self.off_recv
+            pe.resid[r] = bp + self.off_resid
+            pe.flags[r] = bp + self.off_flags
+        pe.err = self._own + self.off_err
+        self.peers = pe
+        self.resid = torch.as_tensor(_CudaArray(self._own + self.off_resid, (M, N), "<f4"), device=device)
+        self._err = torch.as_tensor(_CudaArray(self._own + self.off_err, (1,), "<u4"), device=device)
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def linear_allreduce(self, a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, M: int, stream) -> None:
+        """resid += sum over ranks of a_r[:M] . w_r^T + bias, on every rank (all ranks call it in lockstep)."""
+        import ctypes
+
+        self.epoch += 1
+        N, K = w.shape
+        _lib.check(_lib.load().kvpr_linear_allreduce(
+            a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K,
+            bias.data_ptr() if bias is not None else None, ctypes.byref(self.peers), self.epoch & 0xFFFFFFFF,
+            stream.cuda_stream), "kvpr_linear_allreduce")
+
+    def error(self) -> int:
+        """Nonzero once a peer wait timed out (the fused all-reduce then produced garbage)."""
+        return int(self._err.to(torch.int64).item())
+
+    def close(self, group=None) -> None:
+        """Unmap the peers' regions, wait for every rank to do the same, then free this rank's."""
+        lib = _lib.load()
+        torch.cuda.synchronize()
+        for p in self._opened:
+            lib.kvpr_ipc_close(p)
+        self._opened = []
+        if dist.is_initialized():
+            dist.barrier(group=group)
+        if self._own:
+            lib.kvpr_ipc_free(self._own)
+            self._own = None
+
+
 class TPRuntime:
     """One rank of the head-sharded decoder.  `weights` are the full (unsharded) weights on this GPU."""
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, group=None, block: int = 64,
-                 device: torch.device | None = None):
+                 device: torch.device | None = None, fused: bool | None = None):
+        """fused (default: world > 1 and batch <= 64): the decode's row-parallel projections end in the
+        fused peer-memory all-reduce (PeerBuffers / csrc/tpcomm.cu) instead of a collective call."""
         cfg = weights.cfg
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -143,6 +240,8 @@ class TPRuntime:
         self.capacity = capacity
         cap_x = ((capacity + R - 1) // R) * R  # gathered rounds may run past the capacity
         self.layers = [shard_layer(lw, lay) for lw in weights.layers]
+        # the fused all-reduce adds the bias once, at the owner, so every rank keeps the full biases
+        self.bias_full = [(lw.bo, lw.b2) for lw in weights.layers]
         self.embed, self.pos, self.lnf_g, self.lnf_b = weights.embed, weights.pos, weights.lnf_g, weights.lnf_b
         self.group = group
         if self.world > 1:
@@ -169,7 +268,9 @@ class TPRuntime:
         self.kv_dev = z(2, capacity, 2, b, hs)
         self.x_dev = z(2, cap_x, b, h)
         self.x_new = z(2, b, h)
-        self.hres = z(b, h, dt=F32)
+        self.fused = (self.world > 1 and b <= 64) if fused is None else bool(fused and self.world > 1)
+        self.peer = PeerBuffers(b, h, group=group, device=self.dev) if self.fused else None
+        self.hres = self.peer.resid if self.fused else z(b, h, dt=F32)
         self.q, self.attn = z(b, hs), z(b, hs)
         self.y, self.mid, self.zf = z(b, h), z(b, fs), z(b, h)
         self.logits = z(b, cfg.vocab, dt=F32)
@@ -323,10 +424,17 @@ class TPRuntime:
             self._k1(xd, lw, kvd, r0, r1, cs)
         cs.wait_event(ekv)
         kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, lay.heads_local, lay.head_dim, s, stream=cs)
-        self._rowpar(self.attn, lw.wo, lw.bo, self.hres, b)
+        bo, b2 = self.bias_full[j]
+        if self.fused:
+            self.peer.linear_allreduce(self.attn, lw.wo, bo, b, cs)
+        else:
+            self._rowpar(self.attn, lw.wo, lw.bo, self.hres, b)
         kernels.layernorm(self.hres, lw.ln2_g, lw.ln2_b, self.y, eps=cfg.eps, stream=cs)
         kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
-        self._rowpar(self.mid, lw.w2, lw.b2, self.hres, b)
+        if self.fused:
+            self.peer.linear_allreduce(self.mid, lw.w2, b2, b, cs)
+        else:
+            self._rowpar(self.mid, lw.w2, lw.b2, self.hres, b)
         ev["done"][u] = torch.cuda.Event()
         ev["done"][u].record(cs)
 
@@ -397,5 +505,11 @@ class TPRuntime:
         return out
 
     def close(self):
+        if self.peer is not None:
+            err = self.peer.error()
+            self.peer.close(self.group)
+            self.peer = None
+            if err:
+                raise RuntimeError("fused TP all-reduce: a peer flag wait timed out (results are invalid)")
         for t in (self.store_x, self.store_kv):
             torch.cuda.cudart().cudaHostUnregister(t.data_ptr())

@@ -65,7 +65,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _tp_worker(rank, world, port, q, shared=False):
+def _tp_worker(rank, world, port, q, shared=False, fused=None):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -77,7 +77,7 @@ def _tp_worker(rank, world, port, q, shared=False):
     else:
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     try:
-        rt = TPRuntime(_weights(dev), B, S0 + len(SPLITS) + 1, block=16, device=dev)
+        rt = TPRuntime(_weights(dev), B, S0 + len(SPLITS) + 1, block=16, device=dev, fused=fused)
         first = rt.prefill(_prompt())
         toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
         torch.cuda.synchronize(dev)
@@ -87,10 +87,12 @@ def _tp_worker(rank, world, port, q, shared=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shared", [False, True])
-def test_tp_world2_matches_unsharded(shared):
+@pytest.mark.parametrize("shared,fused", [(False, None), (True, False), (True, True)])
+def test_tp_world2_matches_unsharded(shared, fused):
     """world 2: on two GPUs over NCCL, or (shared) both ranks on cuda:0 over gloo, which exercises the
-    sharded data flow (column/row-parallel kernels, X rounds, all-gathers, all-reduces) on a 1-GPU box."""
+    sharded data flow (column/row-parallel kernels, X rounds, all-gathers, all-reduces) on a 1-GPU box.
+    fused: the row-parallel projections end in the peer-memory all-reduce (csrc/tpcomm.cu) over CUDA
+    IPC instead of the process-group all-reduce."""
     if not shared and torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     f0, t0, l0 = _reference()
@@ -98,7 +100,7 @@ def test_tp_world2_matches_unsharded(shared):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q, shared)) for r in range(world)]
+    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q, shared, fused)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
@@ -109,3 +111,65 @@ def test_tp_world2_matches_unsharded(shared):
         assert torch.equal(first, f0) and torch.equal(toks, t0), rank
         rel = ((lg - l0).abs().amax(dim=-1) / l0.abs().amax(dim=-1)).max().item()
         assert rel <= 2e-2, rel
+
+
+def _allreduce_worker(rank, world, port, q, M, N, K, calls):
+    import torch.distributed as dist
+
+    from paper_2411_17089_b200.tp import PeerBuffers
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(100)
+        resid0 = torch.randn(M, N, generator=g)
+        a = [(torch.randn(M, K, generator=g) * 0.5).half() for _ in range(world * calls)]
+        w = [(torch.randn(N, K, generator=g) * 0.05).half() for _ in range(world * calls)]
+        bias = (torch.randn(N, generator=g) * 0.1).half()
+        pb = PeerBuffers(M, N, device=torch.device("cuda", 0))
+        pb.resid.copy_(resid0.cuda())
+        ad = [x.cuda() for x in a]
+        wd = [x.cuda() for x in w]
+        bd = bias.cuda()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s = torch.cuda.Stream()
+        for c in range(calls):
+            i = c * world + rank
+            pb.linear_allreduce(ad[i], wd[i], bd, M, s)
+        s.synchronize()
+        out = pb.resid.cpu().clone()
+        err = pb.error()
+        pb.close()
+        ref = resid0.double()
+        for c in range(calls):
+            ref = ref + sum(a[c * world + r].double() @ w[c * world + r].double().T for r in range(world))
+            ref = ref + bias.double()
+        q.put((rank, out, ref.float(), err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("M,N,K", [(4, 1536, 384), (64, 7168, 896)])
+def test_fused_linear_allreduce_matches_reference(M, N, K):
+    """kvpr_linear_allreduce (push GEMM + owner reduce/broadcast over CUDA IPC peer memory), two ranks
+    sharing cuda:0, three back-to-back calls (epoch flags): every rank ends with the same residual, bit
+    for bit, within fp32-accumulation tolerance of the float64 reference.  (64, 7168, 896) is the
+    OPT-30B TP8 out-proj shape (b64, hidden 7168, 7 of 56 heads)."""
+    world, calls = 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_allreduce_worker, args=(r, world, port, q, M, N, K, calls)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in ps], key=lambda x: x[0])
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(r[3] == 0 for r in res), "peer wait timed out"
+    assert torch.equal(res[0][1], res[1][1])
+    out, ref = res[0][1], res[0][2]
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-3, err
