@@ -325,7 +325,8 @@ def run_kvpr(args):
     if ws > 1:
         dist.barrier()
     clocks = Clocks() if rank == 0 else None
-    launches0 = rt.launches
+    lib = _lib.load()
+    launches0 = lib.kvpr_kernel_launches()  # every kernel libkvpr launches in this process
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     # the timed region: K steps as a user runs them (no per-kernel instrumentation on the path)
@@ -335,7 +336,8 @@ def run_kvpr(args):
     if clocks:
         clocks.sample_now(gpu)  # the decode is enqueued and running
     torch.cuda.synchronize(dev)
-    launches = rt.launches - launches0
+    launches = lib.kvpr_kernel_launches() - launches0
+    launches = int(allreduce([launches], op="sum")[0])  # all ranks
     elapsed = start.elapsed_time(end) / 1e3
     clk = clocks.stop(gpu) if clocks else None
     elapsed = allreduce([elapsed])[0]

@@ -70,6 +70,8 @@ typedef struct kvpr_epilogue {
 
 /* Thread-local description of the last failure ("" if none). */
 const char* kvpr_last_error(void);
+/* Kernels this library has launched in this process (all entry points; for launch accounting). */
+long long kvpr_kernel_launches(void);
 
 /* ABI version (bumped on any signature change). */
 int kvpr_version(void);

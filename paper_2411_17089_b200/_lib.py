@@ -28,6 +28,7 @@ EPI_ACCUM = 4
 EXPORTS = (
     "kvpr_last_error",
     "kvpr_version",
+    "kvpr_kernel_launches",
     "kvpr_sm_count",
     "kvpr_recompute_kv",
     "kvpr_linear",
@@ -110,6 +111,7 @@ _sz = ctypes.c_size_t
 _SIGS = {
     "kvpr_last_error": ([], ctypes.c_char_p),
     "kvpr_version": ([], _i),
+    "kvpr_kernel_launches": ([], _ll),
     "kvpr_sm_count": ([_i], _i),
     "kvpr_recompute_kv": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_linear": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp], _i),

@@ -34,6 +34,8 @@ int check_launch(const char* what) {
   return KVPR_OK;
 }
 
+std::atomic<long long> g_kernel_launches{0};
+
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -78,6 +80,8 @@ extern "C" {
 const char* kvpr_last_error(void) { return g_err; }
 
 int kvpr_version(void) { return 1; }
+
+long long kvpr_kernel_launches(void) { return g_kernel_launches.load(std::memory_order_relaxed); }
 
 int kvpr_sm_count(int device) { return sm_count(device); }
 

@@ -411,6 +411,7 @@ int prefill_attention(const __half* q, const __half* kv, __half* out, int batch,
     prefill_attn_kernel<128><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
   else
     prefill_attn_kernel<64><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return check_launch("prefill_attention");
 }
 

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "kvpr kernels target sm_100a only"
 #endif
@@ -205,6 +207,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();  // KVPR_PDL=0 in the environment turns the attribute off (A/B measurements)
 
+extern std::atomic<long long> g_kernel_launches;  // every kernel this library launched (kvpr_kernel_launches)
+
 template <typename... KArgs, typename... Args>
 inline int launch(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   Args... args) {
@@ -224,6 +228,7 @@ inline int launch(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 bloc
     set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
     return KVPR_ECUDA;
   }
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return check_launch(what);
 }
 

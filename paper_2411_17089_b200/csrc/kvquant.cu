@@ -104,6 +104,7 @@ int kv4_quantize(const __half* pages, uint8_t* qpages, int batch, int hidden, in
   const long long total = gpp * (pos_end - pos_begin);
   const int threads = 256;
   const long long blocks = (total * 32 + threads - 1) / threads;
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   kv4_quantize_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(pages, qpages, batch, hidden, pos_begin,
                                                                              gpp, total);
   return check_launch("kv4_quantize");
@@ -117,6 +118,7 @@ int kv4_dequantize(const uint8_t* qpages, __half* pages, int batch, int hidden, 
   const long long total = gpp * (pos_end - pos_begin);
   const int threads = 256;
   const long long blocks = (total * 32 + threads - 1) / threads;
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   kv4_dequantize_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(qpages, pages, batch, hidden,
                                                                                pos_begin, gpp, total);
   return check_launch("kv4_dequantize");
