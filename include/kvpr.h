@@ -197,6 +197,7 @@ typedef struct kvpr_decoder_desc {
   void *compute_stream, *h2d_stream, *d2h_stream;
   int chunk_rows; /* minimum positions per X chunk / K1 launch (runtime.KVPRRuntime.chunk_rows) */
   int chunk_wave; /* > 0: X chunks are multiples of this many positions (whole K1 tile waves) */
+  void* recompute_stream; /* non-NULL: K1 runs here, issued a unit ahead (overlaps the previous layer) */
 } kvpr_decoder_desc;
 
 int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);

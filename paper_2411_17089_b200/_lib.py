@@ -91,7 +91,8 @@ class DecoderDesc(ctypes.Structure):
         ("eps", ctypes.c_float)] + [(n, ctypes.c_void_p) for n in (
             "embed", "pos", "lnf_g", "lnf_b", "kv_dev", "x_dev", "hres", "q", "attn", "y", "mid", "zf", "logits",
             "tok", "ws")] + [("ws_bytes", ctypes.c_size_t)] + [(n, ctypes.c_void_p) for n in (
-                "compute_stream", "h2d_stream", "d2h_stream")] + [("chunk_rows", ctypes.c_int), ("chunk_wave", ctypes.c_int)]
+                "compute_stream", "h2d_stream", "d2h_stream")] + [("chunk_rows", ctypes.c_int), ("chunk_wave", ctypes.c_int),
+                                                      ("recompute_stream", ctypes.c_void_p)]
 
 
 _lib: ctypes.CDLL | None = None

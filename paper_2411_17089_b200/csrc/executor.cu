@@ -41,7 +41,7 @@ struct Decoder {
   kvpr_decoder_desc d;
   std::vector<kvpr_layer_desc> layer;
   int R = 0;
-  std::vector<cudaEvent_t> ev_x, ev_kv, ev_qkv, ev_d2h, ev_done;  // ring of R units (ev_x: R*chunks)
+  std::vector<cudaEvent_t> ev_x, ev_kv, ev_qkv, ev_d2h, ev_done, ev_k1;  // ring of R units (ev_x: R*chunks)
   bool timing = false;  // bracket K1 / K2 launches with timing events (kvpr_decoder_kernel_stats)
   std::vector<KTime> kt;
   std::vector<cudaEvent_t> pool;  // timing events, created once and reused across runs
@@ -199,6 +199,49 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   return ck(cudaEventRecord(D.ev_kv[x.r], hs), "record KV");
 }
 
+// K1 chunks of unit x on stream st, each after its X chunk landed
+int issue_k1_on(Decoder& D, const Unit& x, __half* xd, __half* kvd, cudaStream_t st) {
+  const kvpr_decoder_desc& d = D.d;
+  const kvpr_layer_desc& Lw = D.layer[x.j];
+  const int b = d.batch, h = d.hidden;
+  int cb[16][2];
+  const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb, chunk_rows(d), d.x_resident ? 0 : d.chunk_wave);
+  const __half* wkv = static_cast<const __half*>(Lw.wqkv) + static_cast<size_t>(h) * h;
+  const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
+  for (int c = 0; c < nc; ++c) {
+    if (!d.x_resident) KV_TRY(ck(cudaStreamWaitEvent(st, D.ev_x[x.r * d.chunks + c], 0), "wait X chunk"));
+    KTime t;
+    KV_TRY(kt_begin(D, 0, 4.0 * b * (cb[c][1] - cb[c][0]) * static_cast<double>(h) * h, st, &t));
+    KV_TRY(kvpr_recompute_kv(xd, wkv, bkv, kvd, b, cb[c][0], cb[c][1], h, st));
+    KV_TRY(kt_end(D, &t, st));
+    ++D.launches;
+  }
+  return KVPR_OK;
+}
+
+// K1 of unit u on the recompute stream, issued one unit ahead of its layer's compute so the rebuild
+// overlaps the previous layer's tail (small models: the layer chain is latency bound).  Hazards:
+// its pages [0, l) of buffer u % nbuf were last read by K2(u - nbuf); its X rows come from the H2D
+// of u (which waited for that K2) or, X resident, from LN1 of the same layer one step back.
+int issue_k1(Decoder& D, int u, int base, const int* splits) {
+  const kvpr_decoder_desc& d = D.d;
+  const Unit x = unit_of(D, u, base, splits);
+  cudaStream_t rs = static_cast<cudaStream_t>(d.recompute_stream);
+  if (d.x_resident) {
+    if (u >= d.nbuf) KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_done[(u - d.nbuf) % D.R], 0), "k1 wait buffer"));
+    if (u >= d.layers) KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_qkv[(u - d.layers) % D.R], 0), "k1 wait X row"));
+  } else if (u >= d.nbuf) {
+    KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_done[(u - d.nbuf) % D.R], 0), "k1 wait buffer"));
+  }
+  const long long bh = static_cast<long long>(d.batch) * d.hidden;
+  const kvpr_layer_desc& Lw = D.layer[x.j];
+  __half* xd = d.x_resident ? static_cast<__half*>(Lw.dev_x)
+                            : static_cast<__half*>(d.x_dev) + static_cast<size_t>(x.buf) * d.capacity * bh;
+  __half* kvd = static_cast<__half*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * bh;
+  KV_TRY(issue_k1_on(D, x, xd, kvd, rs));
+  return ck(cudaEventRecord(D.ev_k1[x.r], rs), "record K1");
+}
+
 int head(Decoder& D, cudaStream_t cs) {
   const kvpr_decoder_desc& d = D.d;
   KV_TRY(layernorm(d.hres, d.hidden, static_cast<const __half*>(d.lnf_g), static_cast<const __half*>(d.lnf_b),
@@ -257,20 +300,12 @@ int compute(Decoder& D, int u, int base, const int* splits) {
                             cudaMemcpyDefault, ds),
             "d2h KV"));
   KV_TRY(ck(cudaEventRecord(D.ev_d2h[x.r], ds), "record d2h"));
-  // K1 per landed chunk (one launch when X is resident)
-  {
-    int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.x_resident ? 1 : d.chunks, cb, chunk_rows(d), d.x_resident ? 0 : d.chunk_wave);
-    const __half* wkv = static_cast<const __half*>(Lw.wqkv) + static_cast<size_t>(h) * h;
-    const __half* bkv = static_cast<const __half*>(Lw.bqkv) + h;
-    for (int c = 0; c < nc; ++c) {
-      if (!d.x_resident) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_x[x.r * d.chunks + c], 0), "wait X chunk"));
-      KTime t;
-      KV_TRY(kt_begin(D, 0, 4.0 * b * (cb[c][1] - cb[c][0]) * static_cast<double>(h) * h, cs, &t));
-      KV_TRY(kvpr_recompute_kv(xd, wkv, bkv, kvd, b, cb[c][0], cb[c][1], h, cs));
-      KV_TRY(kt_end(D, &t, cs));
-      ++D.launches;
-    }
+  // K1 per landed chunk (one launch when X is resident); on its own stream it was issued a unit
+  // ahead (issue_k1) and only its completion gates K2
+  if (d.recompute_stream == nullptr) {
+    KV_TRY(issue_k1_on(D, x, xd, kvd, cs));
+  } else {
+    KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_k1[x.r], 0), "wait K1"));
   }
   KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_kv[x.r], 0), "wait KV"));
   KTime t2;
@@ -322,7 +357,7 @@ int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* la
     return true;
   };
   if (!mk(D->ev_x, D->R * desc->chunks) || !mk(D->ev_kv, D->R) || !mk(D->ev_qkv, D->R) || !mk(D->ev_d2h, D->R) ||
-      !mk(D->ev_done, D->R)) {
+      !mk(D->ev_done, D->R) || !mk(D->ev_k1, D->R)) {
     set_error("decoder_create: cudaEventCreate failed");
     delete D;
     return KVPR_ECUDA;
@@ -410,7 +445,7 @@ int kvpr_decoder_destroy(void* handle) {
   if (D == nullptr) return KVPR_OK;
   kvpr_decoder_set_timing(handle, 0);
   for (auto e : D->pool) cudaEventDestroy(e);
-  for (auto* v : {&D->ev_x, &D->ev_kv, &D->ev_qkv, &D->ev_d2h, &D->ev_done})
+  for (auto* v : {&D->ev_x, &D->ev_kv, &D->ev_qkv, &D->ev_d2h, &D->ev_done, &D->ev_k1})
     for (auto e : *v) cudaEventDestroy(e);
   delete D;
   return KVPR_OK;
@@ -442,9 +477,17 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
     KV_TRY(pool_take(*D, &D->t0));
     KV_TRY(ck(cudaEventRecord(D->t0, cs), "record start"));
   }
+  const bool k1_stream = d.recompute_stream != nullptr;
+  if (k1_stream) {  // the recompute stream joins the run after everything the caller enqueued on cs
+    KV_TRY(ck(cudaEventRecord(D->ev_k1[(D->R - 1) % D->R], cs), "record fork"));
+    KV_TRY(ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(d.recompute_stream), D->ev_k1[(D->R - 1) % D->R], 0),
+              "fork"));
+  }
   KV_TRY(issue_h2d(*D, 0, base_len, splits));
+  if (k1_stream) KV_TRY(issue_k1(*D, 0, base_len, splits));
   for (int u = 0; u < n; ++u) {
     if (u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
+    if (u + 1 < n && k1_stream) KV_TRY(issue_k1(*D, u + 1, base_len, splits));
     KV_TRY(compute(*D, u, base_len, splits));
     KV_TRY(mark(*D, D->layer_marks, cs));
     if (u % d.layers == d.layers - 1) {

@@ -27,6 +27,8 @@ KV[l:s'-1] are single contiguous byte ranges.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import torch
@@ -130,7 +132,8 @@ class KVPRRuntime:
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
                  chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None,
-                 x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None):
+                 x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None,
+                 k1_stream: bool | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
 
         x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
@@ -159,6 +162,10 @@ class KVPRRuntime:
             self.cs = torch.cuda.Stream(self.dev, priority=-1)  # compute
             self.hs = torch.cuda.Stream(self.dev)              # H2D copy engine
             self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
+            self.rs = torch.cuda.Stream(self.dev)              # K1 issued a unit ahead (native executor)
+        # native executor: K1 on its own stream, issued a unit ahead (KVPR_K1_STREAM=0 turns it off)
+        env = os.environ.get("KVPR_K1_STREAM")
+        self.k1_stream = (env != "0") if k1_stream is None else bool(k1_stream)
         self.qbytes = kernels.kv4_page_bytes(b, h) if kv_bits == 4 else None
         self.page_bytes = self.qbytes if kv_bits == 4 else 2 * b * h * 2
         self.x_resident = x_resident
@@ -450,6 +457,7 @@ class KVPRRuntime:
         d.compute_stream, d.h2d_stream, d.d2h_stream = self.cs.cuda_stream, self.hs.cuda_stream, self.ds.cuda_stream
         d.chunk_rows = self.chunk_rows
         d.chunk_wave = self.chunk_wave
+        d.recompute_stream = self.rs.cuda_stream if self.k1_stream else None
         h = ctypes.c_void_p()
         _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
         self._native_keep = (d, layers)

@@ -14,8 +14,10 @@ from paper_2411_17089_b200.weights import OPTConfig, OPTWeights
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("x_resident,wave", [(False, 0), (True, 0), (False, 24)])
-def test_native_equals_python_loop_bitwise(x_resident, wave):
+@pytest.mark.parametrize("x_resident,wave,k1s", [(False, 0, False), (True, 0, False), (False, 24, False),
+                                                  (False, 24, True), (True, 0, True)])
+def test_native_equals_python_loop_bitwise(x_resident, wave, k1s):
+    """k1s: the executor issues K1 a unit ahead on its own stream (only the schedule changes)."""
     cfg = OPTConfig(hidden=512, layers=4, heads=8, ffn=2048, vocab=2048, max_pos=512)
     b, S0 = 3, 150
     splits = [75, 0, 152, 1, 154, 100, 3]
@@ -23,7 +25,8 @@ def test_native_equals_python_loop_bitwise(x_resident, wave):
     prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(32))
     outs = []
     for native in (False, True):
-        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, chunk_rows=64, chunk_wave=wave)
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, chunk_rows=64, chunk_wave=wave,
+                         k1_stream=k1s)
         first = rt.prefill(prompt)
         toks = rt.decode(splits, tokens=first, keep_logits=True, native=native)
         torch.cuda.synchronize()
