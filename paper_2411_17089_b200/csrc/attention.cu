@@ -21,10 +21,14 @@
 
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kvpr_internal.h"
 
 namespace kvpr {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -189,9 +193,15 @@ __device__ __forceinline__ void merge_in_warp(Softmax8& st) {
   }
 }
 
+constexpr int kMaxClusterSplits = 8;  // portable cluster size
+
 // grid: (batch*heads, splits), block: 128 threads.  Q4: positions [q4.lo, q4.hi) come from
 // compressed pages (the caller passes base/page_bytes/lo/hi; per-lane offsets are set here).
-template <int D, bool Q4>
+// CL: the splits of one (sequence, head) form a thread-block cluster; every split writes its
+// softmax state into the cluster leader's shared memory (DSMEM) and the leader merges them in
+// split order -- the same arithmetic as decode_attn_combine_kernel, without the second launch
+// or the round trip through global memory.
+template <int D, bool Q4, bool CL>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
                                                           __half* __restrict__ out, float* __restrict__ ws, int batch,
                                                           int heads, int seq_len, int chunk, float qscale, Q4Src q4) {
@@ -232,6 +242,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
 
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][D];
+  __shared__ float sm_part[CL ? kMaxClusterSplits : 1][D + 2];  // cluster leader: every split's state
   if (lane < LPP) {
     if (lane == 0) {
       sm_m[warp] = st.m;
@@ -255,12 +266,38 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
     }
     if (gridDim.y == 1) {
       out[(long long)b * hidden + hd * D + dd] = __float2half_rn(a / l);
+    } else if constexpr (CL) {
+      float* w = cg::this_cluster().map_shared_rank(&sm_part[0][0], 0) + split * (D + 2);
+      w[2 + dd] = a;
+      if (dd == 0) {
+        w[0] = m;
+        w[1] = l;
+      }
     } else {
       float* w = ws + ((long long)bh * gridDim.y + split) * (D + 2);
       w[2 + dd] = a;
       if (dd == 0) {
         w[0] = m;
         w[1] = l;
+      }
+    }
+  }
+  if constexpr (CL) {
+    if (gridDim.y > 1) {
+      cg::this_cluster().sync();  // every split's state is in the leader's smem
+      if (split == 0 && threadIdx.x < D) {
+        const int dd = threadIdx.x;
+        const int splits = gridDim.y;
+        float m = -INFINITY;
+        for (int s2 = 0; s2 < splits; ++s2) m = fmaxf(m, sm_part[s2][0]);
+        float l = 0.f, a = 0.f;
+        for (int s2 = 0; s2 < splits; ++s2) {
+          const float ms = sm_part[s2][0];
+          const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - m);
+          l += sm_part[s2][1] * f;
+          a += sm_part[s2][2 + dd] * f;
+        }
+        out[(long long)b * hidden + hd * D + dd] = __float2half_rn(a / l);
       }
     }
   }
@@ -319,6 +356,33 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(const __half* __restr
   }
 }
 
+// (bh, splits) grid in clusters of (1, splits): one cluster per (sequence, head), PDL-chained
+template <typename... KArgs, typename... Args>
+int launch_cluster(void (*kern)(KArgs...), dim3 grid, int splits, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = splits;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    set_error("decode_attention (cluster): launch failed: %s", cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return check_launch("decode_attention");
+}
+
 }  // namespace
 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch, int heads,
@@ -362,9 +426,14 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
   int splits = (target + bh - 1) / bh;
   const int max_by_len = (seq_len + 63) / 64;
   if (splits > max_by_len) splits = max_by_len;
+  // up to kMaxClusterSplits splits merge in the cluster leader's smem (no workspace); more need the
+  // fp32 partials in ws and the combine kernel
   const size_t per_split = (size_t)bh * (head_dim + 2) * sizeof(float);
-  if (ws == nullptr || ws_bytes < per_split) splits = 1;
-  else if ((size_t)splits * per_split > ws_bytes) splits = (int)(ws_bytes / per_split);
+  if (splits > kMaxClusterSplits) {
+    if (ws == nullptr || ws_bytes < per_split) splits = kMaxClusterSplits;
+    else if ((size_t)splits * per_split > ws_bytes) splits = (int)(ws_bytes / per_split);
+    if (splits < kMaxClusterSplits) splits = kMaxClusterSplits;
+  }
   if (splits < 1) splits = 1;
   const int chunk = (seq_len + splits - 1) / splits;
   splits = (seq_len + chunk - 1) / chunk;
@@ -377,21 +446,34 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
     q4.lo = q_lo;
     q4.hi = q_hi;
   }
+  const char* cl_env = getenv("KVPR_K2_CLUSTER");  // "0": merge with the combine kernel (A/B tests)
+  const bool cluster_merge = !(cl_env != nullptr && cl_env[0] == '0') || ws == nullptr;
+  if (splits > 1 && splits <= kMaxClusterSplits && cluster_merge) {  // merge in DSMEM: one launch
+    if (head_dim == 128)
+      return use_q4 ? launch_cluster(decode_attn_kernel<128, true, true>, grid, splits, stream, q, kv, out, ws, batch,
+                                     heads, seq_len, chunk, qscale, q4)
+                    : launch_cluster(decode_attn_kernel<128, false, true>, grid, splits, stream, q, kv, out, ws, batch,
+                                     heads, seq_len, chunk, qscale, q4);
+    return use_q4 ? launch_cluster(decode_attn_kernel<64, true, true>, grid, splits, stream, q, kv, out, ws, batch,
+                                   heads, seq_len, chunk, qscale, q4)
+                  : launch_cluster(decode_attn_kernel<64, false, true>, grid, splits, stream, q, kv, out, ws, batch,
+                                   heads, seq_len, chunk, qscale, q4);
+  }
   int rc;
   if (head_dim == 128) {
     if (use_q4)
-      rc = launch("decode_attention", decode_attn_kernel<128, true>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
-                  seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<128, true, false>, grid, 128, 0, stream, q, kv, out, ws,
+                  batch, heads, seq_len, chunk, qscale, q4);
     else
-      rc = launch("decode_attention", decode_attn_kernel<128, false>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
-                  seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<128, false, false>, grid, 128, 0, stream, q, kv, out, ws,
+                  batch, heads, seq_len, chunk, qscale, q4);
   } else {
     if (use_q4)
-      rc = launch("decode_attention", decode_attn_kernel<64, true>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
-                  seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<64, true, false>, grid, 128, 0, stream, q, kv, out, ws,
+                  batch, heads, seq_len, chunk, qscale, q4);
     else
-      rc = launch("decode_attention", decode_attn_kernel<64, false>, grid, 128, 0, stream, q, kv, out, ws, batch, heads,
-                  seq_len, chunk, qscale, q4);
+      rc = launch("decode_attention", decode_attn_kernel<64, false, false>, grid, 128, 0, stream, q, kv, out, ws,
+                  batch, heads, seq_len, chunk, qscale, q4);
   }
   if (rc || splits == 1) return rc;
   if (head_dim == 128)

@@ -369,3 +369,20 @@ def test_split_k_decode_gemm(dev, M, N, K):
     _close(out, ref.clamp_min(0))
     assert torch.equal(out, out2)
     _close(acc, resid + ref, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("batch,heads,d,seq", [(32, 32, 128, 1025), (4, 12, 64, 257), (2, 4, 128, 300)])
+def test_decode_attention_cluster_merge_equals_combine_kernel(dev, batch, heads, d, seq, monkeypatch):
+    """Split-KV merge in the cluster leader's shared memory (one launch) == the combine kernel, bit for bit."""
+    h = heads * d
+    q = _rand(batch, h, scale=1.0, seed=81)
+    pages = _rand(seq + 3, 2, batch, h, scale=1.0, seed=82)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KVPR_K2_CLUSTER", flag)
+        o = torch.empty(batch, h, dtype=torch.float16, device=dev)
+        kernels.decode_attention(q, pages, o, ws, batch, heads, d, seq)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
