@@ -163,9 +163,14 @@ class KVPRRuntime:
             self.hs = torch.cuda.Stream(self.dev)              # H2D copy engine
             self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
             self.rs = torch.cuda.Stream(self.dev)              # K1 issued a unit ahead (native executor)
-        # native executor: K1 on its own stream, issued a unit ahead (KVPR_K1_STREAM=0 turns it off)
+        # native executor: K1 on its own stream, issued a unit ahead, where the layer chain is GPU-bound
+        # (X resident = the row schedule, or small models whose K1 never fills a wave).  A PCIe-bound
+        # column schedule hides K1 anyway and keeps it on the compute stream, uncontended.
+        # KVPR_K1_STREAM=0/1 forces it.
         env = os.environ.get("KVPR_K1_STREAM")
-        self.k1_stream = (env != "0") if k1_stream is None else bool(k1_stream)
+        if k1_stream is None:
+            k1_stream = (env == "1") if env in ("0", "1") else None
+        self.k1_stream = (x_resident or self.chunk_wave == 0) if k1_stream is None else bool(k1_stream)
         self.qbytes = kernels.kv4_page_bytes(b, h) if kv_bits == 4 else None
         self.page_bytes = self.qbytes if kv_bits == 4 else 2 * b * h * 2
         self.x_resident = x_resident
