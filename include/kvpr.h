@@ -225,6 +225,9 @@ long long kvpr_decoder_launches(void* handle);
  * Peer buffers are CUDA IPC allocations: every rank allocates one region with kvpr_ipc_alloc,
  * the host exchanges the handles (torch.distributed object all-gather) and opens the peers'
  * regions with kvpr_ipc_open (cudaIpcMemLazyEnablePeerAccess: NVLink P2P between GPUs). */
+/* Diagnostic only (tools/k2_probe.py): host -> device copy by SM loads from page-locked host memory. */
+int kvpr_debug_sm_pull(const void* host, void* dev, size_t bytes, int ctas, void* stream);
+
 #define KVPR_TP_MAX_WORLD 8
 #define KVPR_TP_MAX_TILES 512
 

@@ -56,6 +56,7 @@ EXPORTS = (
     "kvpr_ipc_close",
     "kvpr_ipc_free",
     "kvpr_linear_allreduce",
+    "kvpr_debug_sm_pull",
 )
 
 TP_MAX_WORLD = 8
@@ -136,6 +137,7 @@ _SIGS = {
     "kvpr_decoder_timeline": ([_vp, ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(ctypes.c_float), _i], _i),
     "kvpr_decoder_launches": ([_vp], _ll),
     "kvpr_ipc_handle_bytes": ([], _sz),
+    "kvpr_debug_sm_pull": ([_vp, _vp, _sz, _i, _vp], _i),
     "kvpr_ipc_alloc": ([_sz, ctypes.POINTER(_vp), _vp], _i),
     "kvpr_ipc_open": ([_vp, ctypes.POINTER(_vp)], _i),
     "kvpr_ipc_close": ([_vp], _i),

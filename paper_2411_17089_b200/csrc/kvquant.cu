@@ -125,3 +125,38 @@ int kv4_dequantize(const uint8_t* qpages, __half* pages, int batch, int hidden, 
 }
 
 }  // namespace kvpr
+
+// ---------------------------------------------------------------------------
+// Diagnostic: host -> device copy driven by SM loads from page-locked host memory (UVA,
+// zero-copy) instead of a copy engine.  Used by tools/k2_probe.py to tell copy-engine/PCIe-write
+// interference apart from PCIe-read traffic; not on the decode path.
+namespace kvpr {
+namespace {
+__global__ void __launch_bounds__(256) sm_pull_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                      long long n16) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * 4;
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n16; i += stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n16) v[u] = src[i + u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n16) dst[i + u] = v[u];
+  }
+}
+}  // namespace
+}  // namespace kvpr
+
+extern "C" int kvpr_debug_sm_pull(const void* host, void* dev, size_t bytes, int ctas, void* stream) {
+  using namespace kvpr;
+  if (host == nullptr || dev == nullptr || bytes % 16 != 0 || ctas <= 0) {
+    set_error("debug_sm_pull: need non-null pointers, bytes %% 16 == 0, ctas > 0");
+    return KVPR_EINVAL;
+  }
+  sm_pull_kernel<<<ctas, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4*>(host),
+                                                                      static_cast<uint4*>(dev),
+                                                                      static_cast<long long>(bytes / 16));
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return check_launch("debug_sm_pull");
+}
