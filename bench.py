@@ -150,6 +150,7 @@ def run_reference(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV offloaded to host",
+                   "batch": args.batch, "prompt_len": args.prompt,
                    "mode": "column", "profile": "b200-guess (1391.2e12 FLOP/s, 55e9 B/s) for the split"},
         "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample,
                          "host_cpus": os.cpu_count()},
@@ -304,6 +305,7 @@ def run_kvpr(args):
     except ImportError:
         pass
     w = OPTWeights.random(cfg, seed=0, device=dev)
+    weights_bytes = w.nbytes()
     g = torch.Generator().manual_seed(1)
     prompt = torch.randint(0, cfg.vocab, (gb, args.prompt), generator=g)[sl.start:sl.start + b]  # this rank's rows
     if args.tp:
@@ -591,11 +593,14 @@ def run_kvpr(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
             "config": {
                 "workload": f"{args.model} b{args.batch} prompt{args.prompt} decode, KV+X offloaded to pinned host",
-                "model": args.model, "global_batch": gb, "batch_per_gpu": b, "seq_len": args.prompt,
+                "geometry": cfg.describe(), "batch": gb,
+                "batch_per_gpu": b, "prompt_len": args.prompt, "decode_steps_timed": args.steps,
                 "parallelism": (f"tp{ws} (head-sharded, {dist.get_backend().upper() if ws > 1 else 'NCCL'})"
                                 if args.tp else f"batch-partition x{ws}"),
                 "mode": "column", "splits_timed": splits[args.warmup:],
-                "l2": "inputs larger than L2 (per-step KV/X streamed from host, 13 GB weights)",
+                "l2": (f"inputs larger than L2: per step {h2d_alg / args.steps / 1e6:.0f} MB of X/KV streamed from "
+                       f"host and {weights_bytes / 1e9:.2f} GB of "
+                       "weights read"),
                 "per_layer_ms": steady_layer_s * 1e3, "prefill_s": prefill_s,
                 "numa": numa,
             },

@@ -38,6 +38,10 @@ class OPTConfig:
         return ModelSpec(hidden_dim=self.hidden, num_layers=self.layers, num_heads=self.heads, ffn_dim=self.ffn,
                          precision_bytes=2)
 
+    def describe(self) -> str:
+        return (f"OPT decoder h{self.hidden} x{self.layers} layers, {self.heads} heads, ffn {self.ffn}, "
+                f"vocab {self.vocab} (random init)")
+
     def with_positions(self, n: int) -> "OPTConfig":
         """Synthetic learned-position table long enough for n positions (config 5 sweeps past 2048)."""
         return OPTConfig(self.hidden, self.layers, self.heads, self.ffn, self.vocab, max(self.max_pos, n), self.eps)
