@@ -81,7 +81,8 @@ def _tp_worker(rank, world, port, q, shared=False, fused=None):
         first = rt.prefill(_prompt())
         toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
         torch.cuda.synchronize(dev)
-        q.put((rank, first.cpu(), toks.cpu(), rt.last_logits.cpu()))
+        # numpy by value: a torch CPU tensor would travel as a file descriptor that dies with this process
+        q.put((rank, first.cpu().numpy(), toks.cpu().numpy(), rt.last_logits.cpu().numpy()))
         rt.close()
     finally:
         dist.destroy_process_group()
@@ -108,6 +109,7 @@ def test_tp_world2_matches_unsharded(shared, fused):
         p.join(timeout=120)
         assert p.exitcode == 0
     for rank, first, toks, lg in res:
+        first, toks, lg = torch.from_numpy(first), torch.from_numpy(toks), torch.from_numpy(lg)
         assert torch.equal(first, f0) and torch.equal(toks, t0), rank
         rel = ((lg - l0).abs().amax(dim=-1) / l0.abs().amax(dim=-1)).max().item()
         assert rel <= 2e-2, rel
@@ -146,7 +148,7 @@ def _allreduce_worker(rank, world, port, q, M, N, K, calls):
         for c in range(calls):
             ref = ref + sum(a[c * world + r].double() @ w[c * world + r].double().T for r in range(world))
             ref = ref + bias.double()
-        q.put((rank, out, ref.float(), err))
+        q.put((rank, out.numpy(), ref.float().numpy(), err))
     finally:
         dist.destroy_process_group()
 
@@ -169,7 +171,7 @@ def test_fused_linear_allreduce_matches_reference(M, N, K):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(r[3] == 0 for r in res), "peer wait timed out"
-    assert torch.equal(res[0][1], res[1][1])
-    out, ref = res[0][1], res[0][2]
+    assert (res[0][1] == res[1][1]).all()
+    out, ref = torch.from_numpy(res[0][1]), torch.from_numpy(res[0][2])
     err = (out - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item() + 1e-3, err
