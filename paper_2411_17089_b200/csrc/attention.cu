@@ -424,7 +424,12 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
   }
   const int target = per_sm * sm_count(dev);
   int splits = (target + bh - 1) / bh;
-  const int max_by_len = (seq_len + 63) / 64;
+  static int min_pos = -1;  // positions per split at least (KVPR_K2_MIN_POS overrides for experiments)
+  if (min_pos < 0) {
+    const char* e = getenv("KVPR_K2_MIN_POS");
+    min_pos = (e != nullptr && atoi(e) > 0) ? atoi(e) : 64;
+  }
+  const int max_by_len = (seq_len + min_pos - 1) / min_pos;
   if (splits > max_by_len) splits = max_by_len;
   // up to kMaxClusterSplits splits merge in the cluster leader's smem (no workspace); more need the
   // fp32 partials in ws and the combine kernel
