@@ -16,6 +16,8 @@
 //   x^ = half(mn + q * sc)                   (no FMA contraction)
 // One warp per group of 64: each lane owns two elements (one code byte).
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kvpr_internal.h"
 
@@ -132,31 +134,45 @@ int kv4_dequantize(const uint8_t* qpages, __half* pages, int batch, int hidden, 
 // interference apart from PCIe-read traffic; not on the decode path.
 namespace kvpr {
 namespace {
-__global__ void __launch_bounds__(256) sm_pull_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                                      long long n16) {
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * 4;
-  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n16; i += stride) {
-    uint4 v[4];
+template <int U>
+__global__ void __launch_bounds__(1024) sm_pull_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                       long long n16) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * U;
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * U; i < n16; i += stride) {
+    uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (i + u < n16) v[u] = src[i + u];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (i + u < n16) dst[i + u] = v[u];
   }
 }
 }  // namespace
 }  // namespace kvpr
 
+// threads per CTA and 16-byte loads in flight per thread come from KVPR_PULL_THREADS (256) and
+// KVPR_PULL_UNROLL (4 / 8 / 16; default 4): bytes in flight per SM = threads x unroll x 16
 extern "C" int kvpr_debug_sm_pull(const void* host, void* dev, size_t bytes, int ctas, void* stream) {
   using namespace kvpr;
   if (host == nullptr || dev == nullptr || bytes % 16 != 0 || ctas <= 0) {
     set_error("debug_sm_pull: need non-null pointers, bytes %% 16 == 0, ctas > 0");
     return KVPR_EINVAL;
   }
-  sm_pull_kernel<<<ctas, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4*>(host),
-                                                                      static_cast<uint4*>(dev),
-                                                                      static_cast<long long>(bytes / 16));
+  const char* te = getenv("KVPR_PULL_THREADS");
+  const char* ue = getenv("KVPR_PULL_UNROLL");
+  const int threads = te != nullptr && atoi(te) >= 32 && atoi(te) <= 1024 ? atoi(te) : 256;
+  const int unroll = ue != nullptr ? atoi(ue) : 4;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint4* src = static_cast<const uint4*>(host);
+  uint4* dst = static_cast<uint4*>(dev);
+  const long long n16 = static_cast<long long>(bytes / 16);
+  if (unroll >= 16)
+    sm_pull_kernel<16><<<ctas, threads, 0, s>>>(src, dst, n16);
+  else if (unroll >= 8)
+    sm_pull_kernel<8><<<ctas, threads, 0, s>>>(src, dst, n16);
+  else
+    sm_pull_kernel<4><<<ctas, threads, 0, s>>>(src, dst, n16);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return check_launch("debug_sm_pull");
 }
