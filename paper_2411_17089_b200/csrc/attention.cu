@@ -451,7 +451,9 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
     q4.lo = q_lo;
     q4.hi = q_hi;
   }
-  const char* cl_env = getenv("KVPR_K2_CLUSTER");  // "0": merge with the combine kernel (A/B tests)
+  // KVPR_K2_CLUSTER=0: merge with the combine kernel instead (A/B tests; read per call so a test can
+  // flip it, a getenv is ~100 ns against a >= 5 us kernel)
+  const char* cl_env = getenv("KVPR_K2_CLUSTER");
   const bool cluster_merge = !(cl_env != nullptr && cl_env[0] == '0') || ws == nullptr;
   if (splits > 1 && splits <= kMaxClusterSplits && cluster_merge) {  // merge in DSMEM: one launch
     if (head_dim == 128)
