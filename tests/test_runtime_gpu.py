@@ -283,3 +283,31 @@ def test_full_size_output_independent_of_split_and_rebuild_exact(criterion):
         assert torch.equal(lg, ref_l), f"{name}: logits differ by {(lg - ref_l).abs().max().item()}"
     criterion("G4", "config-2 shapes (h4096 b32 s1024): K1 rebuild == stored K/V bitwise; decode bit-identical "
               f"for l = 0, solver l {plans['solver']}, l = s'", True)
+
+
+@pytest.mark.parametrize("batch,S0", [(1, 1), (1, 37), (5, 2)])
+def test_edge_shapes_match_oracle_for_every_split(batch, S0):
+    """Edge shapes: a single sequence, a one-token prompt, odd batch sizes.  Every split plan (l = 0,
+    l = s', and a ragged one) gives the same tokens and logits bit for bit, within 2e-2 of the oracle."""
+    cfg = OPTConfig(hidden=256, layers=2, heads=4, ffn=1024, vocab=1024, max_pos=128)
+    steps = 5
+    w, prompt = _setup(cfg, batch, S0, seed=21)
+    wl = WorkloadSpec(batch_size=batch, prompt_len=S0, gen_len=steps)
+    plans = {
+        "naive": constant_plan(wl, "column", 0).splits,
+        "full": constant_plan(wl, "column", S0 + steps).splits,
+        "ragged": [min(S0 + i + 1, (7 * i + 1) % (S0 + i + 2)) for i in range(steps)],
+    }
+    outs = {}
+    for name, splits in plans.items():
+        toks, rt = generate(w, prompt, splits, keep_logits=True)
+        outs[name] = (toks, rt.last_logits.float().cpu().numpy())
+        rt.close()
+    ref_t, ref_l = outs["naive"]
+    for name, (t, lg) in outs.items():
+        assert torch.equal(t, ref_t), name
+        assert (lg == ref_l).all(), name
+    o_toks, o_logits, _ = opt_ref.generate(_oracle_shape(cfg), w.numpy_dict(), prompt.numpy(), plans["ragged"])
+    err = max(float(np.abs(ref_l[i] - o_logits[i + 1]).max() / np.abs(o_logits[i + 1]).max()) for i in range(steps))
+    assert err <= LOGIT_RTOL, err
+    assert (ref_t.numpy() == o_toks).all()
