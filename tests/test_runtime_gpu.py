@@ -247,13 +247,15 @@ def test_decode_orders_after_callers_token_copy():
     assert torch.equal(got, ref)
 
 
-def test_full_size_output_independent_of_split_and_rebuild_exact(criterion):
-    """BASELINE config-2 layer shapes (OPT-6.7B widths, b32, prompt 1024; 2 layers to bound the test):
-    size-independent properties at full size.  (1) K1 rebuilding X[0:1024) of a layer (32768 rows, CTA
-    pairs, n-band rasterization) equals the prefill's stored K/V bit for bit; (2) the decode is
-    bit-identical for l = 0, the solver's l (wave-aligned X chunks) and l = s'."""
-    cfg = OPTConfig(hidden=4096, layers=2, heads=32, ffn=16384).with_positions(1040)
-    batch, S0, steps = 32, 1024, 3
+@pytest.mark.parametrize("S0,layers", [(1024, 2), (8192, 1)])
+def test_full_size_output_independent_of_split_and_rebuild_exact(criterion, S0, layers):
+    """BASELINE config-2 layer shapes (OPT-6.7B widths, b32, prompt 1024; and config 5's longest
+    prompt, 8192), reduced layer counts to bound the test: size-independent properties at full size.
+    (1) K1 rebuilding X[0:S0) of a layer (32768 / 262144 rows, CTA pairs, n-band rasterization)
+    equals the prefill's stored K/V bit for bit; (2) the decode is bit-identical for l = 0, the
+    solver's l (wave-aligned X chunks) and l = s'."""
+    cfg = OPTConfig(hidden=4096, layers=layers, heads=32, ffn=16384).with_positions(S0 + 16)
+    batch, steps = 32, 3
     w, prompt = _setup(cfg, batch, S0, seed=7, std=0.02, emb_std=0.02)
     wl = WorkloadSpec(batch_size=batch, prompt_len=S0, gen_len=steps)
     plans = {
@@ -268,11 +270,13 @@ def test_full_size_output_independent_of_split_and_rebuild_exact(criterion):
         assert rt.chunk_wave == 296
         first = rt.prefill(prompt)
         if name == "naive":
-            x = rt.stores.x[1][:S0].cuda()
+            j = layers - 1
+            x = rt.stores.x[j][:S0].cuda()
             pages = torch.empty(S0 + steps + 1, 2, batch, cfg.hidden, dtype=torch.float16, device="cuda")
-            kernels.recompute_kv(x, w.layers[1].w_kv, w.layers[1].b_kv, pages, batch, 0, S0)
+            kernels.recompute_kv(x, w.layers[j].w_kv, w.layers[j].b_kv, pages, batch, 0, S0)
             torch.cuda.synchronize()
-            assert torch.equal(pages[:S0], rt.stores.kv[1][:S0].cuda())
+            assert torch.equal(pages[:S0], rt.stores.kv[j][:S0].cuda())
+            del x, pages
         toks = rt.decode(splits, tokens=first, keep_logits=True)
         torch.cuda.synchronize()
         outs[name] = (toks.cpu(), rt.last_logits.cpu())
@@ -281,8 +285,8 @@ def test_full_size_output_independent_of_split_and_rebuild_exact(criterion):
     for name, (t, lg) in outs.items():
         assert torch.equal(t, ref_t), name
         assert torch.equal(lg, ref_l), f"{name}: logits differ by {(lg - ref_l).abs().max().item()}"
-    criterion("G4", "config-2 shapes (h4096 b32 s1024): K1 rebuild == stored K/V bitwise; decode bit-identical "
-              f"for l = 0, solver l {plans['solver']}, l = s'", True)
+    criterion(f"G4-{S0}", f"config-2 widths (h4096 b32 s{S0}): K1 rebuild == stored K/V bitwise; decode "
+              f"bit-identical for l = 0, solver l {plans['solver']}, l = s'", True)
 
 
 @pytest.mark.parametrize("batch,S0", [(1, 1), (1, 37), (5, 2)])
