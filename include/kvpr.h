@@ -100,12 +100,16 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
  * bn selects the tile: 32 / 64 / 128 / 256 = 128 x bn tile on one CTA; 512 = 256 x 256 tile on a
  * CTA pair (tcgen05 cta_group::2); -1 = weight-streaming decode GEMM with the operands swapped
  * (128 weight rows x all M <= 64 activation rows per tile); 0 = auto (-1 for M <= 64).  All
- * variants accumulate K in the same order, so without a K split they produce identical bits. */
+ * variants accumulate K in the same order, so without a K split they produce identical bits.
+ * -2 = CUDA-core decode projection for M <= 8 (see kvpr_linear_ws; different k order). */
 int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                 const kvpr_epilogue* epi, int bn, void* stream);
 
 /* kvpr_linear with an fp32 scratch buffer: single-row-block (decode) GEMMs may then split K
- * across CTAs (deterministic: partials reduced in slice order, then the same epilogue). */
+ * across CTAs (deterministic: partials reduced in slice order, then the same epilogue).
+ * bn = -2 (and bn = 0 for M <= 8, unless KVPR_GEMV=0) selects the CUDA-core decode projection
+ * (weight streaming with 16-byte loads, fixed reduction order): deterministic, but its k order
+ * is not the tensor-core kernels', so the runtime never routes the q/k/v projection here. */
 int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                    const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream);
 

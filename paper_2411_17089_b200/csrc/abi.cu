@@ -45,6 +45,18 @@ bool pdl_enabled() {
   return v == 1;
 }
 
+// KVPR_GEMV: the largest weight (MB) auto mode routes to the CUDA-core decode projection;
+// 0 = never, < 0 = any size (A/B knob for tools/decode_gemm_bench.py).  Default 8 MB: below it the
+// swap-AB kernel has too few 128-row tiles to stream at HBM rate; above it, it has enough
+static long long gemv_max_weight_bytes() {
+  static long long v = -2;
+  if (v == -2) {
+    const char* e = getenv("KVPR_GEMV");
+    v = e == nullptr ? (8ll << 20) : static_cast<long long>(atof(e) * (1 << 20));
+  }
+  return v;
+}
+
 int sm_count(int device) {
   static int cache[64] = {0};
   if (device >= 0 && device < 64 && cache[device] > 0) return cache[device];
@@ -155,7 +167,13 @@ int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, i
     cudaGetDevice(&dev);
     const int sms = sm_count(dev);
     const long long m_blk = (M + 127) / 128;
-    if (M <= 64) {
+    const long long gemv_cap = gemv_max_weight_bytes();
+    if (M <= kGemvMaxM && ws != nullptr && gemv_smem_bytes(M, K) <= static_cast<size_t>(kGemvMaxSmem) &&
+        (gemv_cap < 0 || static_cast<long long>(N) * K * 2 <= gemv_cap)) {
+      // decode at batch <= 8 through the split-capable entry (out-proj, fc1, fc2, LM head — never
+      // the q/k/v projection, whose k, v must carry K1's bits): CUDA-core weight streaming (gemv.cu)
+      bn = -2;
+    } else if (M <= 64) {
       // decode (M = batch): weight streaming with the operands swapped (gemm_swapab_kernel)
       bn = -1;
     } else if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {

@@ -27,6 +27,7 @@ namespace kvpr {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
 constexpr int kBnSwapAB = -1;  // gemm_f16 tile code of the swapped-operand decode GEMM
+constexpr int kBnGemv = -2;    // CUDA-core decode projection, M <= kGemvMaxM (gemv.cu)
 constexpr long long kABandBytes = 32ll << 20;
 
 // The 1-CTA ring is sized at launch: stage = A box (a_box_rows x 128 B: 16 KB, or only the live
@@ -1038,6 +1039,8 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
     return KVPR_EINVAL;
   }
   switch (bn) {
+    case kBnGemv:
+      return gemv_f16(a, lda, w, ldw, args, stream);
     case kBnSwapAB:  // weight-streaming decode GEMM, M <= 64
       if (M > 64) {
         set_error("gemm: swap-AB decode GEMM needs M <= 64 (M=%d)", M);

@@ -47,6 +47,14 @@ void clear_error();
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0);
 
+// CUDA-core projection for decode batches M <= kGemvMaxM (gemv.cu); deterministic, but not the
+// tensor-core kernels' k order (never used for outputs K1 rebuilds)
+constexpr int kGemvMaxM = 8;
+constexpr int kGemvMaxSmem = 96 * 1024;  // activations staged per CTA: M * K * 2 bytes
+size_t gemv_smem_bytes(int M, int K);
+int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream);
+int gemv_slices(int N, int device);
+
 int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                      const GemmArgs& tp, cudaStream_t stream);
 

@@ -173,6 +173,86 @@ def test_linear_epilogues(dev):
     _close(pages[:, 1].reshape(M2, seg), ref2[:, 2 * seg:])
 
 
+@pytest.mark.parametrize(
+    "M,N,K",
+    [
+        (4, 768, 768),  # config-1 out-proj (KS = 4 k-slices per column group)
+        (4, 3072, 768),  # config-1 fc1
+        (4, 768, 3072),  # config-1 fc2 (units beyond the prefetched ones: main loop)
+        (4, 50272, 768),  # config-1 LM head (N tail inside the last CTA)
+        (1, 64, 128),  # single row, N < one CTA's columns, most lanes idle
+        (8, 1024, 6144),  # long main loop (software-pipelined batches), MP = 8, 96 KB of staged A
+        (5, 640, 1000),  # MP = 8 with 3 dead rows; K not a multiple of 256 (partial unit slices)
+        (3, 96, 8),  # K = one 16-byte unit
+    ],
+)
+def test_gemv_matches_fp32(dev, M, N, K):
+    """CUDA-core decode projection (bn = -2): fp32 accumulation, every epilogue form."""
+    a = _rand(M, K, scale=0.5, seed=81)
+    w = _rand(N, K, scale=0.05, seed=82)
+    bias = _rand(N, scale=0.1, seed=83)
+    ref = a.float() @ w.float().T + bias.float()
+    out = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, out, bn=-2)
+    relu = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.linear_simple(a, w, bias, relu, flags=_lib.EPI_RELU, bn=-2)
+    resid = torch.randn(M, N, device=dev)
+    acc = resid.clone()
+    kernels.linear_simple(a, w, bias, acc, flags=_lib.EPI_ACCUM, bn=-2)
+    acc2 = resid.clone()
+    kernels.linear_simple(a, w, bias, acc2, flags=_lib.EPI_ACCUM, bn=-2)
+    torch.cuda.synchronize()
+    _close(out, ref)
+    _close(relu, ref.clamp_min(0))
+    _close(acc, resid + ref, rtol=1e-5, atol=1e-4)
+    assert torch.equal(acc, acc2)  # fixed reduction order
+
+
+def test_gemv_segments_and_auto_routing(dev):
+    """Segment scatter / scale through the GEMV epilogue; auto mode picks it only via the ws entry
+    at M <= 8 (kvpr_linear keeps the K1-compatible swap-AB kernel)."""
+    seg, K, B = 128, 512, 4
+    a = _rand(B, K, scale=0.5, seed=84)
+    w = _rand(3 * seg, K, scale=0.05, seed=85)
+    b = _rand(3 * seg, scale=0.1, seed=86)
+    ref = a.float() @ w.float().T + b.float()
+    qbuf = torch.zeros(B, seg, dtype=torch.float16, device=dev)
+    page = torch.zeros(2, B, seg, dtype=torch.float16, device=dev)
+    epi = _lib.make_epilogue([(qbuf.data_ptr(), 0), (page[0].data_ptr(), 0), (page[1].data_ptr(), 0)],
+                             seg_width=seg, ld=seg, row_group=B, bias=b.data_ptr(), scale=0.125, scale_cols=seg)
+    kernels.linear(a, w, epi, M=B, bn=-2)
+    torch.cuda.synchronize()
+    _close(qbuf, ref[:, :seg] * 0.125)
+    _close(page[0], ref[:, seg:2 * seg])
+    _close(page[1], ref[:, 2 * seg:])
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+    outs = {}
+    for name, bn, wsb in (("gemv", -2, None), ("swap", -1, None), ("auto_ws", 0, ws), ("auto", 0, None)):
+        o = torch.empty(B, 3 * seg, dtype=torch.float16, device=dev)
+        kernels.linear_simple(a, w, b, o, bn=bn, ws=wsb)
+        outs[name] = o
+    torch.cuda.synchronize()
+    assert torch.equal(outs["auto_ws"], outs["gemv"])
+    assert torch.equal(outs["auto"], outs["swap"])
+
+
+def test_gemv_rejects_large_m_and_k(dev):
+    a = _rand(9, 64, seed=87)
+    w = _rand(64, 64, seed=88)
+    out = torch.empty(9, 64, dtype=torch.float16, device=dev)
+    with pytest.raises(ValueError, match="gemv"):
+        kernels.linear_simple(a, w, None, out, bn=-2)
+    a = _rand(8, 8192, seed=89)  # 128 KB of activations to stage
+    w = _rand(64, 8192, seed=90)
+    out = torch.empty(8, 64, dtype=torch.float16, device=dev)
+    with pytest.raises(ValueError, match="gemv"):
+        kernels.linear_simple(a, w, None, out, bn=-2)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
+    kernels.linear_simple(a, w, None, out, ws=ws)  # auto mode falls back to the swap-AB kernel
+    torch.cuda.synchronize()
+    _close(out, a.float() @ w.float().T)
+
+
 @pytest.mark.parametrize("batch,hidden,p0,p1", [(4, 768, 0, 257), (4, 768, 3, 250), (3, 256, 5, 6), (32, 512, 0, 40)])
 def test_recompute_kv_writes_pages(dev, batch, hidden, p0, p1):
     S = p1 + 3

@@ -110,9 +110,24 @@ def test_tp_world2_matches_unsharded(shared, fused):
         assert p.exitcode == 0
     for rank, first, toks, lg in res:
         first, toks, lg = torch.from_numpy(first), torch.from_numpy(toks), torch.from_numpy(lg)
-        assert torch.equal(first, f0) and torch.equal(toks, t0), rank
-        rel = ((lg - l0).abs().amax(dim=-1) / l0.abs().amax(dim=-1)).max().item()
-        assert rel <= 2e-2, rel
+        assert torch.equal(first, f0), rank
+        _greedy_agrees(toks, lg, t0, l0)
+
+
+def _greedy_agrees(toks, lg, t0, l0, rtol=2e-2):
+    """Sharding changes the fp32 summation order of every row-parallel projection, so tokens equal
+    the unsharded run's on every DECIDED choice: per sequence, logits within rtol of the unsharded
+    ones and the same argmax until the first near-tie (unsharded top-1 vs the sharded pick within
+    twice the measured logit error), after which that sequence legitimately free-runs elsewhere."""
+    steps, b = t0.shape
+    for j in range(b):
+        for i in range(steps):
+            err = (lg[i, j] - l0[i, j]).abs().max().item()
+            assert err <= rtol * l0[i, j].abs().max().item(), (i, j, err)
+            if toks[i, j] != t0[i, j]:
+                margin = (l0[i, j, t0[i, j]] - l0[i, j, toks[i, j]]).item()
+                assert margin <= 2 * err, f"seq {j} step {i}: diverged at a decided choice (margin {margin:.3e})"
+                break
 
 
 def _allreduce_worker(rank, world, port, q, M, N, K, calls):

@@ -62,6 +62,18 @@ def main():
                               "tflops": round(2 * M * N * K / t / 1e12, 1)}), flush=True)
     if "--k1-only" in sys.argv:
         return
+    if "--gemv" in sys.argv:
+        # CUDA-core decode projection (bn -2) vs the swap-AB tensor-core kernel (with its split-K
+        # workspace) at batch <= 8: config-1 shapes, then OPT-6.7B / 13B shapes at b4 / b8
+        gshapes = [(m, n, k) for m in (1, 4, 8) for (n, k) in ((768, 768), (3072, 768), (768, 3072), (50272, 768))]
+        gshapes += [(m, n, k) for m in (4, 8) for (n, k) in ((4096, 4096), (16384, 4096), (4096, 16384),
+                                                             (5120, 5120), (20480, 5120), (5120, 20480))]
+        for M, N, K in gshapes:
+            for bn in (-2, -1):
+                t = run(M, N, K, bn, ws=wsb)
+                print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "split_ws": True, "us": round(t * 1e6, 2),
+                                  "weight_gbs": round(N * K * 2 / t / 1e9, 1)}), flush=True)
+        return
     for M, N, K in shapes:
         for bn in ((-1,) if "--swap-only" in sys.argv else (-1, 32, 128, 0)):
             for split in (False, True):
