@@ -109,6 +109,27 @@ def cpu_reference_sample(hidden, heads, seq_len, split, budget_s=12.0, max_reps=
     return float(np.median(ts)), len(ts)
 
 
+def cpu_oracle_e2e(cfg, w, prompt, splits, prompt_len):
+    """the fp32 CPU OPT decoder (oracle/opt_ref.py: host X/KV stores, split-merge
+    rebuild at the same l per step) end to end on this host, same weights and prompt; decode steps
+    timed after an untimed prefill."""
+    import numpy as np
+
+    from oracle import opt_ref
+
+    shape = opt_ref.OPTShape(cfg.hidden, cfg.layers, cfg.heads, cfg.ffn, cfg.vocab, cfg.max_pos, cfg.eps)
+    o = opt_ref.OPTOracle(shape, w.numpy_dict(), prompt.shape[0], storage=np.float16, compute=np.float32)
+    lg = o.prefill(prompt.numpy(), capacity=prompt_len + len(splits) + 1)
+    tok = opt_ref.greedy(lg)
+    t0 = time.perf_counter()
+    for l in splits:
+        tok = opt_ref.greedy(o.decode_step(tok, min(l, o.len + 1)))
+    dt = time.perf_counter() - t0
+    return {"value": prompt.shape[0] * len(splits) / dt, "unit": "tok/s", "cores": blas_threads(), "kind": "port",
+            "sample": f"{len(splits)} decode steps x b{prompt.shape[0]} of the fp32 NumPy OPT decoder "
+                      f"(oracle/opt_ref.py, host stores + split-merge rebuild), after an untimed prefill"}
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -496,6 +517,8 @@ def run_kvpr(args):
                           f"oracle/numerics_ref.py) at s'={mid.seq_len}, l={mid.recompute_len}; "
                           f"tok/s = 1/(t x {L} layers)"),
                "host_cpus": os.cpu_count()}
+        if cfg.hidden * cfg.layers <= 1024 * 24:  # config-1-sized: the whole CPU decoder fits the budget
+            cpu["oracle_e2e"] = cpu_oracle_e2e(cfg, w, prompt, splits[args.warmup:args.warmup + 4], args.prompt)
 
     # row schedule (the reference's other mode, graph.py:16-17): X resident in HBM, only KV[l:] on PCIe
     alt_row = None

@@ -113,6 +113,16 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
 int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                    const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream);
 
+/* K5 + K6: y = LayerNorm(x) (fp32 rows [M][ldx] -> fp16 [M][ldy], as kvpr_layernorm) and
+ * out = epilogue(y . W^T + bias) (as kvpr_linear_ws).  With KVPR_LN_FUSE=1 in the environment and
+ * the projection on the CUDA-core path (bn -2, or auto at M <= 8) this is ONE launch: every CTA
+ * normalises the rows into its staging buffer with kvpr_layernorm's exact arithmetic and CTA 0
+ * stores y (measured slower than two launches at config 1, so not the default).  Otherwise the two
+ * launches.  y and out are bit-identical to kvpr_layernorm followed by kvpr_linear_ws either way. */
+int kvpr_layernorm_linear_ws(const float* x, long long ldx, const void* gamma, const void* beta, float eps, void* y,
+                             long long ldy, const void* w, long long ldw, int M, int N, int K,
+                             const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream);
+
 /* K2 — split-KV decode attention over the merged cache, read in place.
  * Replaces numerics.decode_attention's per-head loop (numerics.py:166-190):
  * per (sequence b, head) softmax(scale * K q) V over positions [0, seq_len)

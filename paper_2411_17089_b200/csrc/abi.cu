@@ -153,6 +153,32 @@ int kvpr_linear(const void* a, long long lda, const void* w, long long ldw, int 
   return kvpr_linear_ws(a, lda, w, ldw, M, N, K, epi, bn, nullptr, 0, stream);
 }
 
+// bn = 0: the tile / kernel for this shape (has_ws: the caller's entry allows a different k order)
+static int auto_bn(int M, int N, int K, bool has_ws) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sm_count(dev);
+  const long long m_blk = (M + 127) / 128;
+  const long long gemv_cap = gemv_max_weight_bytes();
+  if (M <= kGemvMaxM && has_ws && gemv_smem_bytes(M, K) <= static_cast<size_t>(kGemvMaxSmem) &&
+      (gemv_cap < 0 || static_cast<long long>(N) * K * 2 <= gemv_cap)) {
+    // decode at batch <= 8 through the split-capable entry (out-proj, fc1, fc2, LM head — never
+    // the q/k/v projection, whose k, v must carry K1's bits): CUDA-core weight streaming (gemv.cu)
+    return -2;
+  }
+  if (M <= 64) return -1;  // decode (M = batch): weight streaming with the operands swapped (gemm_swapab_kernel)
+  if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) return 512;
+  // one row block: weight-streaming; per-CTA k-loop throughput, not CTA count, limits
+  // it, so wide N tiles win (measured: tools/gemm_bench.py, profiles/r01_gemm_variants.jsonl)
+  if (m_blk == 1) return 128;
+  // large GEMMs: CTA-pair 256x256 tiles when they fill the SM pairs; otherwise narrower N tiles
+  // give more CTAs
+  int bn = 256;
+  if (m_blk * ((N + 255) / 256) < sms) bn = 128;
+  if (m_blk * ((N + 127) / 128) < sms) bn = 64;
+  return bn;
+}
+
 int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                    const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
@@ -160,36 +186,38 @@ int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, i
     set_error("linear: null pointer");
     return KVPR_EINVAL;
   }
-  if (bn == 0) {
-    // large GEMMs: CTA-pair 256x256 tiles when they fill the SM pairs; small-M (decode) GEMMs are
-    // weight-streaming, so narrower N tiles give more CTAs
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int sms = sm_count(dev);
-    const long long m_blk = (M + 127) / 128;
-    const long long gemv_cap = gemv_max_weight_bytes();
-    if (M <= kGemvMaxM && ws != nullptr && gemv_smem_bytes(M, K) <= static_cast<size_t>(kGemvMaxSmem) &&
-        (gemv_cap < 0 || static_cast<long long>(N) * K * 2 <= gemv_cap)) {
-      // decode at batch <= 8 through the split-capable entry (out-proj, fc1, fc2, LM head — never
-      // the q/k/v projection, whose k, v must carry K1's bits): CUDA-core weight streaming (gemv.cu)
-      bn = -2;
-    } else if (M <= 64) {
-      // decode (M = batch): weight streaming with the operands swapped (gemm_swapab_kernel)
-      bn = -1;
-    } else if (((M + 255) / 256) * (long long)((N + 255) / 256) >= sms / 2) {
-      bn = 512;
-    } else if (m_blk == 1) {
-      // one row block: weight-streaming; per-CTA k-loop throughput, not CTA count, limits
-      // it, so wide N tiles win (measured: tools/gemm_bench.py, profiles/r01_gemm_variants.jsonl)
-      bn = 128;
-    } else {
-      bn = 256;
-      if (m_blk * ((N + 255) / 256) < sms) bn = 128;
-      if (m_blk * ((N + 127) / 128) < sms) bn = 64;
-    }
-  }
+  if (bn == 0) bn = auto_bn(M, N, K, ws != nullptr);
   return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream),
                   static_cast<float*>(ws), ws_bytes);
+}
+
+int kvpr_layernorm_linear_ws(const float* x, long long ldx, const void* gamma, const void* beta, float eps, void* y,
+                             long long ldy, const void* w, long long ldw, int M, int N, int K,
+                             const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  if (epi == nullptr || x == nullptr || y == nullptr || w == nullptr || gamma == nullptr || beta == nullptr) {
+    set_error("layernorm_linear: null pointer");
+    return KVPR_EINVAL;
+  }
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bn == 0) bn = auto_bn(M, N, K, ws != nullptr);
+  // KVPR_LN_FUSE=1: the one-launch form.  Off by default: measured slower at config 1 (0.736 vs
+  // 0.700 ms/step, profiles/r01_ln_fuse_ab.jsonl) — every CTA's LN prologue sits after its PDL
+  // wait, which costs more than the separate 4-CTA LN launch it replaces
+  static const bool fuse = [] {
+    const char* e = getenv("KVPR_LN_FUSE");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (bn == -2 && fuse) {
+    // one launch: every CTA normalises the M rows into its staging buffer (CTA 0 also writes y)
+    const GemvLn ln{x, ldx, static_cast<const __half*>(gamma), static_cast<const __half*>(beta), eps,
+                    static_cast<__half*>(y), ldy};
+    return gemm_f16(y, ldy, w, ldw, M, N, K, to_args(epi), bn, s, static_cast<float*>(ws), ws_bytes, &ln);
+  }
+  const int rc = layernorm(x, ldx, static_cast<const __half*>(gamma), static_cast<const __half*>(beta),
+                           static_cast<__half*>(y), ldy, M, K, eps, s);
+  if (rc) return rc;
+  return gemm_f16(y, ldy, w, ldw, M, N, K, to_args(epi), bn, s, static_cast<float*>(ws), ws_bytes);
 }
 
 int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* ws, size_t ws_bytes, int batch,

@@ -246,6 +246,32 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// LayerNorm arithmetic on one float4 of a row, shared by layernorm_kernel (elementwise.cu) and the
+// LN-fused decode projection (gemv.cu): one definition, so both produce the same bits
+__device__ __forceinline__ float ln_vec_sum(const float4& v) { return v.x + v.y + v.z + v.w; }
+
+__device__ __forceinline__ float ln_vec_sq(const float4& v, float mean) {
+  const float a = v.x - mean, b = v.y - mean, c = v.z - mean, d = v.w - mean;
+  return a * a + b * b + c * c + d * d;
+}
+
+__device__ __forceinline__ float ln_rstd(float sq_total, int hidden, float eps) {
+  return rsqrtf(sq_total / hidden + eps);
+}
+
+// gamma/beta at columns [4c, 4c+4)
+__device__ __forceinline__ uint2 ln_vec_out(const float4& v, float mean, float rstd, const __half* gamma,
+                                            const __half* beta, int c) {
+  const __half2* g2 = reinterpret_cast<const __half2*>(gamma + 4 * c);
+  const __half2* b2 = reinterpret_cast<const __half2*>(beta + 4 * c);
+  const float2 g0 = __half22float2(g2[0]), g1 = __half22float2(g2[1]);
+  const float2 c0 = __half22float2(b2[0]), c1 = __half22float2(b2[1]);
+  uint2 w;
+  w.x = pack_half2((v.x - mean) * rstd * g0.x + c0.x, (v.y - mean) * rstd * g0.y + c0.y);
+  w.y = pack_half2((v.z - mean) * rstd * g1.x + c1.x, (v.w - mean) * rstd * g1.y + c1.y);
+  return w;
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -51,33 +51,21 @@ __global__ void __launch_bounds__(kRowThreads) layernorm_kernel(const float* __r
   for (int i = 0; i < VPT; ++i) {
     const int c = threadIdx.x + i * kRowThreads;
     v[i] = (c < nvec) ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    s += v[i].x + v[i].y + v[i].z + v[i].w;
+    s += ln_vec_sum(v[i]);
   }
   const float mean = block_sum(s, red) / hidden;
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int c = threadIdx.x + i * kRowThreads;
-    if (c < nvec) {
-      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
-      ss += a * a + b * b + cc * cc + d * d;
-    }
+    if (c < nvec) ss += ln_vec_sq(v[i], mean);
   }
-  const float rstd = rsqrtf(block_sum(ss, red) / hidden + eps);
+  const float rstd = ln_rstd(block_sum(ss, red), hidden, eps);
   __half* o = out + row * ldo;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int c = threadIdx.x + i * kRowThreads;
-    if (c < nvec) {
-      const __half2* g2 = reinterpret_cast<const __half2*>(gamma + 4 * c);
-      const __half2* b2 = reinterpret_cast<const __half2*>(beta + 4 * c);
-      const float2 g0 = __half22float2(g2[0]), g1 = __half22float2(g2[1]);
-      const float2 c0 = __half22float2(b2[0]), c1 = __half22float2(b2[1]);
-      uint2 w;
-      w.x = pack_half2((v[i].x - mean) * rstd * g0.x + c0.x, (v[i].y - mean) * rstd * g0.y + c0.y);
-      w.y = pack_half2((v[i].z - mean) * rstd * g1.x + c1.x, (v[i].w - mean) * rstd * g1.y + c1.y);
-      *reinterpret_cast<uint2*>(o + 4 * c) = w;
-    }
+    if (c < nvec) *reinterpret_cast<uint2*>(o + 4 * c) = ln_vec_out(v[i], mean, rstd, gamma, beta, c);
   }
 }
 

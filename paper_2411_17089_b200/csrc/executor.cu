@@ -214,7 +214,6 @@ int issue_k1_on(Decoder& D, const Unit& x, __half* xd, __half* kvd, cudaStream_t
     KV_TRY(kt_begin(D, 0, 4.0 * b * (cb[c][1] - cb[c][0]) * static_cast<double>(h) * h, st, &t));
     KV_TRY(kvpr_recompute_kv(xd, wkv, bkv, kvd, b, cb[c][0], cb[c][1], h, st));
     KV_TRY(kt_end(D, &t, st));
-    ++D.launches;
   }
   return KVPR_OK;
 }
@@ -314,16 +313,15 @@ int compute(Decoder& D, int u, int base, const int* splits) {
                           static_cast<float*>(d.ws), d.ws_bytes, b, d.heads, h / d.heads, x.s,
                           static_cast<float>(1.0 / sqrt(static_cast<double>(h / d.heads))), cs));
   KV_TRY(kt_end(D, &t2, cs));
-  D.launches += 10;  // LN1, qkv, K2 (+ combine), out-proj, LN2, fc1, fc2 (+ split-K reduce)
   {
     kvpr_epilogue e = simple_epi(d.hres, h, b, h, Lw.bo, KVPR_EPI_F32 | KVPR_EPI_ACCUM);
     KV_TRY(kvpr_linear_ws(d.attn, h, Lw.wo, h, b, h, h, &e, 0, d.ws, d.ws_bytes, cs));
   }
-  KV_TRY(layernorm(d.hres, h, static_cast<const __half*>(Lw.ln2_g), static_cast<const __half*>(Lw.ln2_b),
-                   static_cast<__half*>(d.y), h, b, h, d.eps, cs));
   {
+    // LN2 + fc1 + ReLU: one launch on the CUDA-core decode path (batch <= 8), else LN then GEMM
     kvpr_epilogue e = simple_epi(d.mid, d.ffn, b, d.ffn, Lw.b1, KVPR_EPI_RELU);
-    KV_TRY(kvpr_linear_ws(d.y, h, Lw.w1, h, b, d.ffn, h, &e, 0, d.ws, d.ws_bytes, cs));
+    KV_TRY(kvpr_layernorm_linear_ws(d.hres, h, Lw.ln2_g, Lw.ln2_b, d.eps, d.y, h, Lw.w1, h, b, d.ffn, h, &e, 0, d.ws,
+                                    d.ws_bytes, cs));
   }
   {
     kvpr_epilogue e = simple_epi(d.hres, h, b, h, Lw.b2, KVPR_EPI_F32 | KVPR_EPI_ACCUM);
@@ -485,6 +483,11 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
   }
   KV_TRY(issue_h2d(*D, 0, base_len, splits));
   if (k1_stream) KV_TRY(issue_k1(*D, 0, base_len, splits));
+  struct CountLaunches {  // every kernel libkvpr launched during this run (exact, all streams)
+    Decoder* D;
+    long long start = g_kernel_launches.load();
+    ~CountLaunches() { D->launches += g_kernel_launches.load() - start; }
+  } counter{D};
   for (int u = 0; u < n; ++u) {
     if (u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
     if (u + 1 < n && k1_stream) KV_TRY(issue_k1(*D, u + 1, base_len, splits));
@@ -493,7 +496,6 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
     if (u % d.layers == d.layers - 1) {
       const int i = u / d.layers;
       KV_TRY(head(*D, cs));
-      D->launches += 3;
       if (out_tokens)
         KV_TRY(ck(cudaMemcpyAsync(out_tokens + static_cast<size_t>(i) * d.batch, d.tok, d.batch * sizeof(int),
                                   cudaMemcpyDeviceToDevice, cs),

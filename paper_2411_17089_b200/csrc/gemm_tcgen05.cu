@@ -962,7 +962,11 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
 }
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
-             int bn, cudaStream_t stream, float* ws, size_t ws_bytes) {
+             int bn, cudaStream_t stream, float* ws, size_t ws_bytes, const GemvLn* ln) {
+  if (ln != nullptr && bn != kBnGemv) {
+    set_error("gemm: a LayerNorm prologue needs the CUDA-core decode projection (bn=-2)");
+    return KVPR_EINVAL;
+  }
   GemmArgs args = epi;
   args.M = M;
   args.N = N;
@@ -1040,7 +1044,7 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
   }
   switch (bn) {
     case kBnGemv:
-      return gemv_f16(a, lda, w, ldw, args, stream);
+      return gemv_f16(a, lda, w, ldw, args, stream, ln);
     case kBnSwapAB:  // weight-streaming decode GEMM, M <= 64
       if (M > 64) {
         set_error("gemm: swap-AB decode GEMM needs M <= 64 (M=%d)", M);

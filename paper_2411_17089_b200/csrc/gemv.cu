@@ -84,10 +84,13 @@ __device__ __forceinline__ void store_one(const GemmArgs& p, int m, int n, float
   }
 }
 
-template <int MP>
+// LN-fused variant: A = LayerNorm(x) of fp32 rows, computed by every CTA into its staging buffer with
+// layernorm_kernel's exact arithmetic (same thread -> column map, helpers, reduction tree), so A and
+// the output carry the bits of the two-kernel LN -> projection sequence; CTA 0 also stores A to y
+template <int MP, bool kLN>
 __global__ void __launch_bounds__(kGemvWarps * 32)
     gemv_kernel(const __half* __restrict__ a, long long lda, const __half* __restrict__ w, long long ldw,
-                const GemmArgs p, int ks_log2) {
+                const GemmArgs p, int ks_log2, const GemvLn ln) {
   extern __shared__ uint4 sa[];  // A staged once per CTA: [M][K/8] 16-byte units
   __shared__ float red[kGemvWarps][kNC * MP];
   pdl_trigger();
@@ -120,10 +123,85 @@ __global__ void __launch_bounds__(kGemvWarps * 32)
     for (int c = 0; c < kNC; ++c) cur[j][c] = (u < u1 && live[c]) ? ld_stream(wr[c] + u * 8) : make_uint4(0, 0, 0, 0);
   }
   pdl_wait();
-  // A (written by the previous kernel): every 16-byte unit in flight at once, then shared memory
-  for (int i = threadIdx.x; i < p.M * units; i += blockDim.x) {
-    const int m = i / units;
-    sa[i] = __ldg(reinterpret_cast<const uint4*>(a + m * lda) + (i - m * units));
+  if constexpr (kLN) {
+    __shared__ float lnred[MP][kGemvWarps];
+    __shared__ float lnstat[MP];
+    const int nvec = p.K >> 2;
+    const int vpt = (nvec + kGemvWarps * 32 - 1) / (kGemvWarps * 32);
+    float mean[MP], rstd[MP], acc_ln[MP];
+    // pass 1: row sums -> mean
+#pragma unroll
+    for (int m = 0; m < MP; ++m) {
+      acc_ln[m] = 0.f;
+      if (m < p.M) {
+        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
+        for (int i = 0; i < vpt; ++i) {
+          const int c = threadIdx.x + i * kGemvWarps * 32;
+          acc_ln[m] += ln_vec_sum(c < nvec ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+      acc_ln[m] = warp_sum(acc_ln[m]);
+      if (lane == 0) lnred[m][warp] = acc_ln[m];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int m = 0; m < MP; ++m) {
+        const float t = warp_sum(lane < kGemvWarps ? lnred[m][lane] : 0.f);
+        if (lane == 0) lnstat[m] = t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MP; ++m) mean[m] = lnstat[m] / p.K;
+    __syncthreads();
+    // pass 2: centred squares -> rstd
+#pragma unroll
+    for (int m = 0; m < MP; ++m) {
+      acc_ln[m] = 0.f;
+      if (m < p.M) {
+        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
+        for (int i = 0; i < vpt; ++i) {
+          const int c = threadIdx.x + i * kGemvWarps * 32;
+          if (c < nvec) acc_ln[m] += ln_vec_sq(xr[c], mean[m]);
+        }
+      }
+      acc_ln[m] = warp_sum(acc_ln[m]);
+      if (lane == 0) lnred[m][warp] = acc_ln[m];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int m = 0; m < MP; ++m) {
+        const float t = warp_sum(lane < kGemvWarps ? lnred[m][lane] : 0.f);
+        if (lane == 0) lnstat[m] = t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MP; ++m) rstd[m] = ln_rstd(lnstat[m], p.K, ln.eps);
+    // normalise into the staging buffer (and y, from CTA 0)
+    uint2* sa2 = reinterpret_cast<uint2*>(sa);
+#pragma unroll
+    for (int m = 0; m < MP; ++m) {
+      if (m < p.M) {
+        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
+        for (int i = 0; i < vpt; ++i) {
+          const int c = threadIdx.x + i * kGemvWarps * 32;
+          if (c < nvec) {
+            const uint2 o = ln_vec_out(xr[c], mean[m], rstd[m], ln.gamma, ln.beta, c);
+            sa2[m * nvec + c] = o;
+            if (blockIdx.x == 0 && ln.y != nullptr) *reinterpret_cast<uint2*>(ln.y + m * ln.ldy + 4 * c) = o;
+          }
+        }
+      }
+    }
+  } else {
+    // A (written by the previous kernel): every 16-byte unit in flight at once, then shared memory
+    for (int i = threadIdx.x; i < p.M * units; i += blockDim.x) {
+      const int m = i / units;
+      sa[i] = __ldg(reinterpret_cast<const uint4*>(a + m * lda) + (i - m * units));
+    }
   }
   __syncthreads();
 
@@ -196,7 +274,8 @@ int gemv_slices(int N, int device) {
 
 size_t gemv_smem_bytes(int M, int K) { return static_cast<size_t>(M) * K * 2; }
 
-int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream) {
+int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream,
+             const GemvLn* ln) {
   if (args.M < 1 || args.M > kGemvMaxM) {
     set_error("gemv: needs 1 <= M <= %d (M=%d)", kGemvMaxM, args.M);
     return KVPR_EINVAL;
@@ -206,12 +285,19 @@ int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const G
     set_error("gemv: M*K*2 = %zu B of staged activations exceeds %d B", smem, kGemvMaxSmem);
     return KVPR_EINVAL;
   }
+  if (ln != nullptr && (ln->x == nullptr || ln->gamma == nullptr || ln->beta == nullptr || ln->ldx % 4 != 0 ||
+                        ln->ldy % 4 != 0 || args.K % 4 != 0)) {
+    set_error("gemv: LayerNorm operands null or strides not multiples of 4");
+    return KVPR_EINVAL;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   static int attr_done[64] = {0};
   if (dev < 64 && !attr_done[dev]) {
-    cudaFuncSetAttribute(gemv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
-    cudaFuncSetAttribute(gemv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
+    cudaFuncSetAttribute(gemv_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
+    cudaFuncSetAttribute(gemv_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
+    cudaFuncSetAttribute(gemv_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
+    cudaFuncSetAttribute(gemv_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvMaxSmem);
     attr_done[dev] = 1;
   }
   const int ks_log2 = gemv_slices(args.N, dev);
@@ -219,9 +305,14 @@ int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const G
   const unsigned grid = static_cast<unsigned>((args.N + cols_per_cta - 1) / cols_per_cta);
   const __half* ap = static_cast<const __half*>(a);
   const __half* wp = static_cast<const __half*>(w);
-  if (args.M <= 4)
-    return launch("gemv", gemv_kernel<4>, grid, kGemvWarps * 32, smem, stream, ap, lda, wp, ldw, args, ks_log2);
-  return launch("gemv", gemv_kernel<8>, grid, kGemvWarps * 32, smem, stream, ap, lda, wp, ldw, args, ks_log2);
+  const GemvLn l = ln != nullptr ? *ln : GemvLn{};
+  const unsigned thr = kGemvWarps * 32;
+  if (ln != nullptr) {
+    if (args.M <= 4) return launch("gemv_ln", gemv_kernel<4, true>, grid, thr, smem, stream, ap, lda, wp, ldw, args, ks_log2, l);
+    return launch("gemv_ln", gemv_kernel<8, true>, grid, thr, smem, stream, ap, lda, wp, ldw, args, ks_log2, l);
+  }
+  if (args.M <= 4) return launch("gemv", gemv_kernel<4, false>, grid, thr, smem, stream, ap, lda, wp, ldw, args, ks_log2, l);
+  return launch("gemv", gemv_kernel<8, false>, grid, thr, smem, stream, ap, lda, wp, ldw, args, ks_log2, l);
 }
 
 }  // namespace kvpr

@@ -44,16 +44,28 @@ struct GemmArgs {
 int sm_count(int device);
 void clear_error();
 
-int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
-             int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0);
+
 
 // CUDA-core projection for decode batches M <= kGemvMaxM (gemv.cu); deterministic, but not the
 // tensor-core kernels' k order (never used for outputs K1 rebuilds)
 constexpr int kGemvMaxM = 8;
 constexpr int kGemvMaxSmem = 96 * 1024;  // activations staged per CTA: M * K * 2 bytes
 size_t gemv_smem_bytes(int M, int K);
-int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream);
+struct GemvLn {  // LayerNorm prologue of the fused decode projection (A = LN(x) rows)
+  const float* x;
+  long long ldx;
+  const __half* gamma;
+  const __half* beta;
+  float eps;
+  __half* y;  // LN output [M][ldy], written by CTA 0 (may be null)
+  long long ldy;
+};
+int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream,
+             const GemvLn* ln = nullptr);
 int gemv_slices(int N, int device);
+
+int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
+             int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0, const GemvLn* ln = nullptr);
 
 int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                      const GemmArgs& tp, cudaStream_t stream);

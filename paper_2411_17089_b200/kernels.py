@@ -141,6 +141,26 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, out: tor
     return out
 
 
+def layernorm_linear(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, y: torch.Tensor, w: torch.Tensor,
+                     bias: torch.Tensor | None, out: torch.Tensor, rows: int, eps: float = 1e-5, flags: int = 0,
+                     bn: int = 0, stream=None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """y[:rows] = LayerNorm(x[:rows]) (fp16) and out[:rows] = epilogue(y . w^T + bias); one launch when the
+    projection takes the CUDA-core decode path (rows <= 8 with ws), bit-identical to layernorm + linear."""
+    _need(x, torch.float32, "x")
+    _need(y, torch.float16, "y")
+    _need(w, torch.float16, "w")
+    N, K = w.shape
+    if out.dtype == torch.float32:
+        flags |= _lib.EPI_F32
+    epi = _lib.make_epilogue([(out.data_ptr(), 0)], seg_width=((N + 31) // 32) * 32, ld=out.stride(0), row_group=rows,
+                             bias=bias.data_ptr() if bias is not None else None, flags=flags)
+    _lib.call("kvpr_layernorm_linear_ws", x.data_ptr(), x.stride(0), gamma.data_ptr(), beta.data_ptr(), float(eps),
+              y.data_ptr(), y.stride(0), w.data_ptr(), w.stride(0), rows, N, K, epi, bn,
+              ws.data_ptr() if ws is not None else None, ws.numel() * ws.element_size() if ws is not None else 0,
+              _stream(stream))
+    return out
+
+
 def embed(tokens: torch.Tensor, tok_emb: torch.Tensor, pos_emb: torch.Tensor, out: torch.Tensor, batch: int,
           pos_begin: int, pos_offset: int = 2, stream=None) -> torch.Tensor:
     _need(tokens, torch.int32, "tokens")

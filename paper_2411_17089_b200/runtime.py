@@ -312,8 +312,8 @@ class KVPRRuntime:
     def _ffn(self, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
         cfg = self.cfg
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
-        kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, ybuf, rows=M, eps=cfg.eps, stream=stream)
-        kernels.linear_simple(ybuf[:M], lw.w1, lw.b1, mid[:M], flags=_lib.EPI_RELU, stream=stream, ws=self.ws)
+        kernels.layernorm_linear(hres, lw.ln2_g, lw.ln2_b, ybuf, lw.w1, lw.b1, mid, rows=M, eps=cfg.eps,
+                                 flags=_lib.EPI_RELU, stream=stream, ws=self.ws)
         kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream, ws=self.ws)
         self._k(3)
 

@@ -236,6 +236,72 @@ def test_gemv_segments_and_auto_routing(dev):
     assert torch.equal(outs["auto"], outs["swap"])
 
 
+@pytest.mark.parametrize("M,N,K", [(4, 3072, 768), (1, 256, 64), (8, 512, 5120), (3, 640, 1000), (32, 1024, 768)])
+def test_layernorm_linear_fused_bitwise(dev, M, N, K):
+    """kvpr_layernorm_linear_ws: y and out bit-identical to kvpr_layernorm + kvpr_linear_ws.  The
+    one-launch form (KVPR_LN_FUSE=1, CUDA-core path at M <= 8) runs in a subprocess, since the switch
+    is read once per process; here the default two-launch form."""
+    x = torch.randn(M + 2, K + 4, device=dev) * 3 + 0.5  # row stride > K
+    g = _rand(K, scale=0.2, seed=91) + 1
+    be = _rand(K, scale=0.2, seed=92)
+    w = _rand(N, K, scale=0.05, seed=93)
+    bias = _rand(N, scale=0.1, seed=94)
+    ws = torch.empty(1 << 22, dtype=torch.uint8, device=dev)
+    y1 = torch.zeros(M, K, dtype=torch.float16, device=dev)
+    o1 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.layernorm(x, g, be, y1, rows=M)
+    kernels.linear_simple(y1, w, bias, o1, flags=_lib.EPI_RELU, ws=ws)
+    y2 = torch.zeros(M, K, dtype=torch.float16, device=dev)
+    o2 = torch.empty(M, N, dtype=torch.float16, device=dev)
+    kernels.layernorm_linear(x, g, be, y2, w, bias, o2, rows=M, flags=_lib.EPI_RELU, ws=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(o1, o2)
+    xr = x[:M, :K]
+    ref_y = (xr - xr.mean(-1, keepdim=True)) / torch.sqrt(xr.var(-1, unbiased=False, keepdim=True) + 1e-5)
+    _close(y2, ref_y * g.float() + be.float())
+
+
+_FUSED_LN_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2411_17089_b200 import _lib, kernels
+torch.manual_seed(0)
+for M, N, K in ((4, 3072, 768), (8, 512, 5120), (3, 640, 1000)):
+    x = torch.randn(M + 2, K + 4, device="cuda") * 3 + 0.5
+    g = torch.randn(K, device="cuda").half() * 0.2 + 1
+    be = torch.randn(K, device="cuda").half() * 0.2
+    w = (torch.randn(N, K, device="cuda") * 0.05).half()
+    bias = (torch.randn(N, device="cuda") * 0.1).half()
+    ws = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    y1 = torch.zeros(M, K, dtype=torch.float16, device="cuda"); o1 = torch.empty(M, N, dtype=torch.float16, device="cuda")
+    kernels.layernorm(x, g, be, y1, rows=M)
+    kernels.linear_simple(y1, w, bias, o1, flags=_lib.EPI_RELU, ws=ws)
+    y2 = torch.zeros_like(y1); o2 = torch.empty_like(o1)
+    n0 = _lib.load().kvpr_kernel_launches()
+    kernels.layernorm_linear(x, g, be, y2, w, bias, o2, rows=M, flags=_lib.EPI_RELU, ws=ws)
+    n = _lib.load().kvpr_kernel_launches() - n0
+    torch.cuda.synchronize()
+    assert n == 1, n
+    assert torch.equal(y1, y2) and torch.equal(o1, o2), (M, N, K)
+print("fused ok")
+"""
+
+
+def test_layernorm_linear_one_launch_form_bitwise(dev):
+    """KVPR_LN_FUSE=1: LN computed inside every CTA of the CUDA-core projection (one launch), y and
+    out bit-identical to the LN kernel + projection."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _FUSED_LN_SCRIPT, root], env={**os.environ, "KVPR_LN_FUSE": "1"},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_gemv_rejects_large_m_and_k(dev):
     a = _rand(9, 64, seed=87)
     w = _rand(64, 64, seed=88)
