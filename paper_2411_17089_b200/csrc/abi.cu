@@ -201,14 +201,15 @@ int kvpr_layernorm_linear_ws(const float* x, long long ldx, const void* gamma, c
   }
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (bn == 0) bn = auto_bn(M, N, K, ws != nullptr);
-  // KVPR_LN_FUSE=1: the one-launch form.  Off by default: measured slower at config 1 (0.736 vs
-  // 0.700 ms/step, profiles/r01_ln_fuse_ab.jsonl) — every CTA's LN prologue sits after its PDL
-  // wait, which costs more than the separate 4-CTA LN launch it replaces
+  // KVPR_LN_FUSE=1: the one-launch form.  Off by default: at config 1 it measured 0.736 vs 0.700
+  // ms/step with the rows re-read per pass, and 0.7101 vs 0.7067 with the rows held in registers
+  // (profiles/r01_ln_fuse_ab.jsonl) — every CTA's LN prologue sits after its PDL wait and costs
+  // about what the separate 4-CTA LN launch does
   static const bool fuse = [] {
     const char* e = getenv("KVPR_LN_FUSE");
     return e != nullptr && e[0] == '1';
   }();
-  if (bn == -2 && fuse) {
+  if (bn == -2 && fuse && K <= kGemvLnMaxK) {
     // one launch: every CTA normalises the M rows into its staging buffer (CTA 0 also writes y)
     const GemvLn ln{x, ldx, static_cast<const __half*>(gamma), static_cast<const __half*>(beta), eps,
                     static_cast<__half*>(y), ldy};

@@ -27,6 +27,7 @@ namespace {
 constexpr int kGemvWarps = 8;
 constexpr int kNC = 2;  // output columns per warp
 constexpr int kPF = 4;  // 16-byte units per lane and column issued before the PDL wait
+constexpr int kLnVec = 2;  // LN prologue: float4 per thread per row held in registers (hidden <= 2048)
 
 __device__ __forceinline__ uint4 ld_stream(const __half* p) {
   uint4 r;
@@ -124,24 +125,29 @@ __global__ void __launch_bounds__(kGemvWarps * 32)
   }
   pdl_wait();
   if constexpr (kLN) {
+    // the rows are loaded once into registers (hidden <= 4 * 256 * kLnVec, checked on the host);
+    // the passes then run from registers like layernorm_kernel's
     __shared__ float lnred[MP][kGemvWarps];
     __shared__ float lnstat[MP];
     const int nvec = p.K >> 2;
-    const int vpt = (nvec + kGemvWarps * 32 - 1) / (kGemvWarps * 32);
-    float mean[MP], rstd[MP], acc_ln[MP];
+    float4 xv[MP][kLnVec];
+#pragma unroll
+    for (int m = 0; m < MP; ++m)
+#pragma unroll
+      for (int i = 0; i < kLnVec; ++i) {
+        const int c = threadIdx.x + i * kGemvWarps * 32;
+        xv[m][i] = (m < p.M && c < nvec) ? reinterpret_cast<const float4*>(ln.x + m * ln.ldx)[c]
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    float mean[MP], rstd[MP];
     // pass 1: row sums -> mean
 #pragma unroll
     for (int m = 0; m < MP; ++m) {
-      acc_ln[m] = 0.f;
-      if (m < p.M) {
-        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
-        for (int i = 0; i < vpt; ++i) {
-          const int c = threadIdx.x + i * kGemvWarps * 32;
-          acc_ln[m] += ln_vec_sum(c < nvec ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f));
-        }
-      }
-      acc_ln[m] = warp_sum(acc_ln[m]);
-      if (lane == 0) lnred[m][warp] = acc_ln[m];
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < kLnVec; ++i) a += ln_vec_sum(xv[m][i]);
+      a = warp_sum(a);
+      if (lane == 0) lnred[m][warp] = a;
     }
     __syncthreads();
     if (warp == 0) {
@@ -158,16 +164,12 @@ __global__ void __launch_bounds__(kGemvWarps * 32)
     // pass 2: centred squares -> rstd
 #pragma unroll
     for (int m = 0; m < MP; ++m) {
-      acc_ln[m] = 0.f;
-      if (m < p.M) {
-        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
-        for (int i = 0; i < vpt; ++i) {
-          const int c = threadIdx.x + i * kGemvWarps * 32;
-          if (c < nvec) acc_ln[m] += ln_vec_sq(xr[c], mean[m]);
-        }
-      }
-      acc_ln[m] = warp_sum(acc_ln[m]);
-      if (lane == 0) lnred[m][warp] = acc_ln[m];
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < kLnVec; ++i)
+        if (threadIdx.x + i * kGemvWarps * 32 < nvec) a += ln_vec_sq(xv[m][i], mean[m]);
+      a = warp_sum(a);
+      if (lane == 0) lnred[m][warp] = a;
     }
     __syncthreads();
     if (warp == 0) {
@@ -185,11 +187,11 @@ __global__ void __launch_bounds__(kGemvWarps * 32)
 #pragma unroll
     for (int m = 0; m < MP; ++m) {
       if (m < p.M) {
-        const float4* xr = reinterpret_cast<const float4*>(ln.x + m * ln.ldx);
-        for (int i = 0; i < vpt; ++i) {
+#pragma unroll
+        for (int i = 0; i < kLnVec; ++i) {
           const int c = threadIdx.x + i * kGemvWarps * 32;
           if (c < nvec) {
-            const uint2 o = ln_vec_out(xr[c], mean[m], rstd[m], ln.gamma, ln.beta, c);
+            const uint2 o = ln_vec_out(xv[m][i], mean[m], rstd[m], ln.gamma, ln.beta, c);
             sa2[m * nvec + c] = o;
             if (blockIdx.x == 0 && ln.y != nullptr) *reinterpret_cast<uint2*>(ln.y + m * ln.ldy + 4 * c) = o;
           }
@@ -286,8 +288,8 @@ int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const G
     return KVPR_EINVAL;
   }
   if (ln != nullptr && (ln->x == nullptr || ln->gamma == nullptr || ln->beta == nullptr || ln->ldx % 4 != 0 ||
-                        ln->ldy % 4 != 0 || args.K % 4 != 0)) {
-    set_error("gemv: LayerNorm operands null or strides not multiples of 4");
+                        ln->ldy % 4 != 0 || args.K % 4 != 0 || args.K > kGemvLnMaxK)) {
+    set_error("gemv: LayerNorm operands null, strides not multiples of 4, or hidden %d > %d", args.K, kGemvLnMaxK);
     return KVPR_EINVAL;
   }
   int dev = 0;

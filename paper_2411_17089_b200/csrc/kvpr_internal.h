@@ -50,6 +50,7 @@ void clear_error();
 // tensor-core kernels' k order (never used for outputs K1 rebuilds)
 constexpr int kGemvMaxM = 8;
 constexpr int kGemvMaxSmem = 96 * 1024;  // activations staged per CTA: M * K * 2 bytes
+constexpr int kGemvLnMaxK = 2048;        // LN prologue holds a row in 2 float4 per thread
 size_t gemv_smem_bytes(int M, int K);
 struct GemvLn {  // LayerNorm prologue of the fused decode projection (A = LN(x) rows)
   const float* x;
