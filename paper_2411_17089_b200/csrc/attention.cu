@@ -209,6 +209,11 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
   constexpr int PPW = 32 / LPP;  // positions per warp step
   constexpr int NW = 4;
   pdl_trigger();
+  // DSMEM rule: a CTA may touch a peer's shared memory only once every CTA of the cluster has
+  // started; the arrival here and the wait just before the remote stores cost nothing in between
+  if constexpr (CL) {
+    if (gridDim.y > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  }
   pdl_wait();  // q (qkv GEMM), pages [0, l) (K1) come from the preceding kernels
   const int bh = blockIdx.x;
   const int b = bh / heads;
@@ -252,6 +257,9 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
     for (int i = 0; i < 8; ++i) sm_acc[warp][glane * 8 + i] = st.acc[i];
   }
   __syncthreads();
+  if constexpr (CL) {
+    if (gridDim.y > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
   if (threadIdx.x < D) {
     const int dd = threadIdx.x;
     float m = -INFINITY;
