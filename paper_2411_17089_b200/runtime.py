@@ -147,10 +147,13 @@ class KVPRRuntime:
             raise ValueError(f"capacity {capacity} exceeds the position table ({cfg.max_pos})")
         self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
         self.dev = torch.device(device) if device is not None else weights.embed.device
-        self.chunks, self.nbuf = chunks, nbuf
-        # a K1 chunk carries >= 4 MiB of X (>= 64 positions): small models issue one X copy + one K1
-        # per layer instead of paying per-call latency `chunks` times (tests lower it to cover chunking)
-        self.chunk_rows = chunk_rows or max(64, -(-(4 << 20) // (batch * cfg.hidden * 2)))
+        self.chunks, self.nbuf = int(os.environ.get("KVPR_CHUNKS", chunks)), nbuf  # env: A/B knob
+        # a K1 chunk carries >= KVPR_CHUNK_MB (default 32) MiB of X (>= 64 positions): every extra X
+        # DMA costs copy-engine time (OPT-6.7B b4: 1/2/4/8 chunks of ~30 MB of X in total -> 98.8 /
+        # 97.4 / 96.0 / 94.1% of the overlap roofline, profiles/r01_chunk_ab.jsonl), so small batches
+        # and small models issue one X copy + one K1 per layer (tests lower it to cover chunking)
+        chunk_mb = float(os.environ.get("KVPR_CHUNK_MB", 32))
+        self.chunk_rows = chunk_rows or max(64, -(-int(chunk_mb * (1 << 20)) // (batch * cfg.hidden * 2)))
         # X chunks in whole K1 waves when the wave is short enough to still pipeline (<= l / 2)
         if chunk_wave is None:
             chunk_wave = 0 if chunk_rows else wave_positions(
