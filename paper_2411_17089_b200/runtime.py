@@ -203,14 +203,11 @@ class KVPRRuntime:
         self.ev_qkv = [ev() for _ in range(R)]
         self.ev_d2h = [ev() for _ in range(R)]
         self.ev_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
-        self.launches = 0  # kernels issued (for bench's gpu_launches)
+        self.launches = 0  # kernels libkvpr launched for this runtime's decode calls (library counter)
         self._trace = None
         self.kernel_timing: list | None = None  # set to [] to time K1 / K2 launches with CUDA events
 
     # ------------------------------------------------------------------ utils
-    def _k(self, n: int = 1) -> None:
-        self.launches += n
-
     def _ktimer(self, name: str, units: float, stream):
         """With kernel_timing enabled, bracket one hot-kernel launch with CUDA events on its stream."""
         if self.kernel_timing is None:
@@ -303,13 +300,11 @@ class KVPRRuntime:
             seg_width=h, ld=h, row_group=b, bias=lw.bqkv.data_ptr(),
         )
         kernels.linear(x, lw.wqkv, epi, M=M, stream=stream)
-        self._k()
 
     def _mlp(self, attn: torch.Tensor, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
         """h += attn W_o^T + b_o;  h += relu(LN2(h) W_1^T + b_1) W_2^T + b_2  (OPT pre-LN block)."""
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.linear_simple(attn[:M], lw.wo, lw.bo, hres[:M], flags=acc, stream=stream, ws=self.ws)
-        self._k()
         self._ffn(M, lw, hres, ybuf, mid, stream)
 
     def _ffn(self, M: int, lw, hres: torch.Tensor, ybuf: torch.Tensor, mid: torch.Tensor, stream):
@@ -318,7 +313,6 @@ class KVPRRuntime:
         kernels.layernorm_linear(hres, lw.ln2_g, lw.ln2_b, ybuf, lw.w1, lw.b1, mid, rows=M, eps=cfg.eps,
                                  flags=_lib.EPI_RELU, stream=stream, ws=self.ws)
         kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream, ws=self.ws)
-        self._k(3)
 
     def _head(self, hrows: torch.Tensor, stream) -> None:
         """Final LN, tied LM head (fp32 logits) and greedy argmax into self.tok."""
@@ -326,7 +320,6 @@ class KVPRRuntime:
         kernels.layernorm(hrows, self.w.lnf_g, self.w.lnf_b, self.zf, eps=cfg.eps, stream=stream)
         kernels.linear_simple(self.zf, self.w.embed, None, self.logits, stream=stream, ws=self.ws)
         kernels.argmax(self.logits, self.tok, stream=stream)
-        self._k(3)
 
     # ------------------------------------------------------------------ decode
     def _unit(self, u: int, base_len: int, splits: list[int]):
@@ -381,11 +374,9 @@ class KVPRRuntime:
         # new token: X = LN1(h) straight into the X slot of position s'-1, q/k/v with k,v into page s'-1
         sp = tr.begin(cs, "compute_mha", I, J, "proj") if tr else None
         kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
-        self._k()
         self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
         if self.kv_bits == 4:  # the stored copy of the new page is compressed; K2 reads the exact fp16 page
             kernels.kv4_quantize(kvd[s - 1:s], self.qnew[buf:buf + 1], b, 0, 1, stream=cs)
-            self._k()
         if sp:
             tr.end(cs, sp)
         self.ev_qkv[r].record(cs)
@@ -413,7 +404,6 @@ class KVPRRuntime:
             self._ktimer_end(kt, cs)
             if sp:
                 tr.end(cs, sp)
-            self._k()
         cs.wait_event(self.ev_kv[r])
         # K2 over the merged pages [0, s') in place (4-bit tail [lp, s'-1) dequantised inside K2), then W_O
         sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
@@ -425,10 +415,8 @@ class KVPRRuntime:
             kt = self._ktimer("k2", 2 * b * s * h * 2, cs)
             kernels.decode_attention(self.q, kvd, self.attn, self.ws, b, cfg.heads, cfg.head_dim, s, stream=cs)
         self._ktimer_end(kt, cs)
-        self._k(2)
         acc = _lib.EPI_F32 | _lib.EPI_ACCUM
         kernels.linear_simple(self.attn, lw.wo, lw.bo, self.hres, flags=acc, stream=cs, ws=self.ws)
-        self._k()
         if sp:
             tr.end(cs, sp)
         sp = tr.begin(cs, "compute_ffn", I, J) if tr else None
@@ -478,12 +466,10 @@ class KVPRRuntime:
 
         arr = (ctypes.c_int * len(splits))(*splits)
         lib, h = _lib.load(), self._native_handle()
-        before = lib.kvpr_decoder_launches(h)
         timed = self.kernel_timing is not None or timing is not None
         _lib.check(lib.kvpr_decoder_set_timing(h, int(timed)), "kvpr_decoder_set_timing")
         _lib.check(lib.kvpr_decoder_run(h, self.len, arr, len(splits), out_tokens.data_ptr(),
                                         logits.data_ptr() if logits is not None else None), "kvpr_decoder_run")
-        self.launches += lib.kvpr_decoder_launches(h) - before
         if timing is not None:
             L, n = self.cfg.layers, len(splits)
             lay, stp = (ctypes.c_float * (n * L))(), (ctypes.c_float * n)()
@@ -521,8 +507,10 @@ class KVPRRuntime:
                 self.tok.copy_(tokens.to(torch.int32), non_blocking=True)
         if native is None:  # the C executor covers the plain path (timed or not); tracing / 4-bit KV stay in Python
             native = trace is None and self.kv_bits is None
+        n0 = _lib.load().kvpr_kernel_launches()
         if native:
             self._decode_native(splits, out_tokens, logits, timing)
+            self.launches += _lib.load().kvpr_kernel_launches() - n0
             self.len = base + steps
             cur = torch.cuda.current_stream(self.dev)
             cur.wait_stream(cs)
@@ -541,7 +529,6 @@ class KVPRRuntime:
             i, j = divmod(u, L)
             if j == 0:
                 kernels.embed(self.tok, self.w.embed, self.w.pos, self.hres, batch=b, pos_begin=base + i, stream=cs)
-                self._k()
             self._compute_layer(u, base, splits)
             if timing is not None:
                 e = torch.cuda.Event(enable_timing=True)
@@ -576,6 +563,7 @@ class KVPRRuntime:
                     prev = e
                 timing.layer_ms.append(row)
                 prev = step_marks[i]
+        self.launches += _lib.load().kvpr_kernel_launches() - n0
         self._last_logits = logits
         return out_tokens
 

@@ -276,7 +276,6 @@ class StreamedRuntime:
             kernels.layernorm(hres, lw.ln2_g, lw.ln2_b, self.y, eps=cfg.eps, stream=cs)
             kernels.linear_simple(self.y, lw.w1, lw.b1, self.mid, flags=_lib.EPI_RELU, stream=cs, ws=self.ws)
             kernels.linear_simple(self.mid, lw.w2, lw.b2, hres, flags=acc, stream=cs, ws=self.ws)
-            self.launches += 12 + len(ev["x"][u])
             ev["done"][u] = E()
             ev["done"][u].record(cs)
             if k == K - 1:
@@ -288,6 +287,7 @@ class StreamedRuntime:
                     if logits is not None:
                         logits[i, k].copy_(self.logits, non_blocking=True)
 
+        n0 = _lib.load().kvpr_kernel_launches()
         issue(0)
         for u in range(n):
             if u + 1 < n:
@@ -299,6 +299,7 @@ class StreamedRuntime:
                 for key in [key for key in d if key < lim]:
                     del d[key]
         self.len = base + steps
+        self.launches += _lib.load().kvpr_kernel_launches() - n0
         cur.wait_stream(cs)
         cur.wait_stream(ds)
         self.last_logits = logits

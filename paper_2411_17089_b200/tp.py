@@ -465,6 +465,7 @@ class TPRuntime:
         t0 = torch.cuda.Event(enable_timing=True) if timing is not None else None
         if t0 is not None:
             t0.record(cs)
+        n0 = _lib.load().kvpr_kernel_launches()
         self._issue_loads(0, base, splits, ev)
         for u in range(n):
             if u + 1 < n:
@@ -473,7 +474,6 @@ class TPRuntime:
             if j == 0:
                 kernels.embed(self.tok, self.embed, self.pos, self.hres, batch=b, pos_begin=base + i, stream=cs)
             self._compute(u, base, splits, ev)
-            self.launches += 12 + len(self.lay.rounds(min(splits[i], base + i)))
             if timing is not None:
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(cs)
@@ -488,6 +488,7 @@ class TPRuntime:
                 for key in [k for k in d if k < u - L - 2]:
                     del d[key]
         self.len = base + steps
+        self.launches += _lib.load().kvpr_kernel_launches() - n0
         cur = torch.cuda.current_stream(self.dev)
         cur.wait_stream(cs)
         cur.wait_stream(self.ds)
