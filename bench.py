@@ -139,10 +139,22 @@ def blas_threads():
         return os.cpu_count()
 
 
+def use_all_host_threads():
+    """torchrun exports OMP_NUM_THREADS=1 to every rank; the CPU reference arm is rank 0 alone, so it
+    lifts the BLAS pool back to every host core."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        pass
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    use_all_host_threads()
     from paper_2411_17089_b200.costmodel import WorkloadSpec
     from paper_2411_17089_b200.hwprofile import HardwareProfile
     from paper_2411_17089_b200.scheduler import plan_generation
@@ -508,7 +520,7 @@ def run_kvpr(args):
         h2d_step, d2h_step = allreduce([h2d_step, d2h_step], op="sum")
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # the CPU baseline is an N=1 measurement
         t_seq_layer, n = cpu_reference_sample(cfg.hidden, cfg.heads, mid.seq_len, mid.recompute_len,
                                               budget_s=args.cpu_budget)
         cpu_tok_s = 1.0 / (t_seq_layer * L)
