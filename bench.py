@@ -552,14 +552,22 @@ def run_kvpr(args):
         torch.cuda.synchronize(dev)
         row_s = r0.elapsed_time(r1) / 1e3
         row_s = allreduce([row_s])[0]
-        troof_r = 0.0
+        troof_r, tgpu_r = 0.0, 0.0
+        hbm = peaks["hbm_gbs"] * 1e9
         for d in plan_r.decisions[args.warmup:]:
-            troof_r += max(kv_remainder_bytes(cfg.spec(), wl, d.seq_len, d.recompute_len) / bw_peak,
-                           recompute_flops(cfg.spec(), wl, d.recompute_len) / f_peak) * L
+            t_rec = recompute_flops(cfg.spec(), wl, d.recompute_len) / f_peak
+            troof_r += max(kv_remainder_bytes(cfg.spec(), wl, d.seq_len, d.recompute_len) / bw_peak, t_rec) * L
+            # the rest of the layer streams its weights (~12 h^2 fp16) and the whole KV cache (K2) from HBM
+            # on the same SMs K1 occupies, so a GPU-bound row step is at best K1 + that, serially
+            rest = (12 * cfg.hidden * cfg.hidden * 2 + 2 * b * d.seq_len * cfg.hidden * 2) / hbm
+            tgpu_r += (t_rec + rest) * L
         alt_row = {"value": gb * args.steps / row_s, "unit": "tok/s", "splits": plan_r.splits[args.warmup:],
                    "ms_per_step": row_s / args.steps * 1e3, "roofline_frac": troof_r / row_s,
+                   "gpu_serial_roofline_frac": tgpu_r / row_s,
                    "note": "row schedule: layer inputs X resident in HBM (8.9 GB), only KV[l:s'] over PCIe; "
-                           "reference solver in mode 'row' (t_act = 0); roofline max(KV bytes/BW, FLOPs/F_sust)"}
+                           "reference solver in mode 'row' (t_act = 0); roofline max(KV bytes/BW, FLOPs/F_sust); "
+                           "GPU-bound, so also gpu_serial_roofline_frac = (K1 FLOPs/F_sust + decode weights and "
+                           "KV-cache HBM bytes/HBM peak) / measured"}
 
     # compressed KV offload (§8f: 4-bit groupwise KV, kv_bytes_per_element 0.5625), same model / batch
     alt_kv4 = None
