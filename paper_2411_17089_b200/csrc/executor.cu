@@ -488,10 +488,17 @@ int kvpr_decoder_run(void* handle, int base_len, const int* splits, int steps, i
     long long start = g_kernel_launches.load();
     ~CountLaunches() { D->launches += g_kernel_launches.load() - start; }
   } counter{D};
+  // unit u+1's loads (and its K1) are issued ahead of unit u's compute, except with a single layer:
+  // there they wait on unit u's own D2H of the new position (graph.py:286-287), recorded by compute(u)
+  const bool ahead = d.layers > 1;
   for (int u = 0; u < n; ++u) {
-    if (u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
-    if (u + 1 < n && k1_stream) KV_TRY(issue_k1(*D, u + 1, base_len, splits));
+    if (ahead && u + 1 < n) KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
+    if (ahead && u + 1 < n && k1_stream) KV_TRY(issue_k1(*D, u + 1, base_len, splits));
     KV_TRY(compute(*D, u, base_len, splits));
+    if (!ahead && u + 1 < n) {
+      KV_TRY(issue_h2d(*D, u + 1, base_len, splits));
+      if (k1_stream) KV_TRY(issue_k1(*D, u + 1, base_len, splits));
+    }
     KV_TRY(mark(*D, D->layer_marks, cs));
     if (u % d.layers == d.layers - 1) {
       const int i = u / d.layers;

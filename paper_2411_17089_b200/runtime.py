@@ -523,8 +523,11 @@ class KVPRRuntime:
         if t_start is not None:
             t_start.record(cs)
         self._issue_h2d(0, base, splits)
+        # unit u+1's loads are issued ahead of unit u's compute, except with a single layer, where they
+        # wait on unit u's own D2H of the new position (graph.py:286-287), recorded by that compute
+        ahead = L > 1
         for u in range(n_units):
-            if u + 1 < n_units:
+            if ahead and u + 1 < n_units:
                 self._issue_h2d(u + 1, base, splits)
             i, j = divmod(u, L)
             if j == 0:
@@ -544,6 +547,8 @@ class KVPRRuntime:
                     e = torch.cuda.Event(enable_timing=True)
                     e.record(cs)
                     step_marks.append(e)
+            if not ahead and u + 1 < n_units:
+                self._issue_h2d(u + 1, base, splits)
         self.len = base + steps
         self._trace = None
         cur = torch.cuda.current_stream(self.dev)

@@ -289,10 +289,13 @@ class StreamedRuntime:
 
         n0 = _lib.load().kvpr_kernel_launches()
         issue(0)
+        ahead = L * K > 1  # a single unit per step: unit u+1's loads wait on unit u's D2H (its compute)
         for u in range(n):
-            if u + 1 < n:
+            if ahead and u + 1 < n:
                 issue(u + 1)
             compute(u)
+            if not ahead and u + 1 < n:
+                issue(u + 1)
             g_now = u // K
             for name, d in ev.items():  # drop events no longer referenced (unit- or layer-keyed)
                 lim = g_now - 4 if name in ("wkv", "wrest", "layer_done") else u - L * K - 4

@@ -467,8 +467,9 @@ class TPRuntime:
             t0.record(cs)
         n0 = _lib.load().kvpr_kernel_launches()
         self._issue_loads(0, base, splits, ev)
+        ahead = L > 1  # one layer: unit u+1's loads wait on unit u's D2H, recorded by its compute
         for u in range(n):
-            if u + 1 < n:
+            if ahead and u + 1 < n:
                 self._issue_loads(u + 1, base, splits, ev)
             i, j = divmod(u, L)
             if j == 0:
@@ -484,6 +485,8 @@ class TPRuntime:
                     out[i].copy_(self.tok, non_blocking=True)
                     if logits is not None:
                         logits[i].copy_(self.logits, non_blocking=True)
+            if not ahead and u + 1 < n:
+                self._issue_loads(u + 1, base, splits, ev)
             for d in (ev["done"], ev["d2h"]):
                 for key in [k for k in d if k < u - L - 2]:
                     del d[key]

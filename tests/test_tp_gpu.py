@@ -26,23 +26,37 @@ CFG = OPTConfig(hidden=512, layers=3, heads=8, ffn=2048, vocab=2048, max_pos=512
 B, S0 = 4, 200
 SPLITS = [150, 0, 201, 77, 203, 5]
 
+# case -> (config, batch, prompt, splits, weight std): "small" is the default geometry above;
+# "config4" is BASELINE config 4's widths (OPT-30B: h7168, 56 heads, ffn 28672; b64, prompt 2048)
+# with one layer to bound memory, at the reference solver's column l
+CASES = {
+    "small": (CFG, B, S0, SPLITS, 0.1),
+    "config4": (OPTConfig(hidden=7168, layers=1, heads=56, ffn=28672, vocab=50272, max_pos=2048 + 16), 64, 2048,
+                [1596, 1597, 1598], 0.02),
+}
 
-def _weights(dev):
-    return OPTWeights.random(CFG, seed=13, device=dev, std=0.1, emb_std=0.1)
+
+def _weights(dev, case="small"):
+    cfg, _, _, _, std = CASES[case]
+    return OPTWeights.random(cfg, seed=13, device=dev, std=std, emb_std=std)
 
 
-def _prompt():
-    return torch.randint(0, CFG.vocab, (B, S0), generator=torch.Generator().manual_seed(14))
+def _prompt(case="small"):
+    cfg, b, s0, _, _ = CASES[case]
+    return torch.randint(0, cfg.vocab, (b, s0), generator=torch.Generator().manual_seed(14))
 
 
-def _reference(dev="cuda:0"):
-    w = _weights(dev)
-    rt = KVPRRuntime(w, B, S0 + len(SPLITS) + 1, device=dev)
-    first = rt.prefill(_prompt())
-    toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
+def _reference(dev="cuda:0", case="small"):
+    _, b, s0, splits, _ = CASES[case]
+    w = _weights(dev, case)
+    rt = KVPRRuntime(w, b, s0 + len(splits) + 1, device=dev)
+    first = rt.prefill(_prompt(case))
+    toks = rt.decode(splits, tokens=first, keep_logits=True)
     torch.cuda.synchronize()
     out = (first.cpu(), toks.cpu(), rt.last_logits.cpu())
     rt.close()
+    del w
+    torch.cuda.empty_cache()
     return out
 
 
@@ -65,7 +79,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _tp_worker(rank, world, port, q, shared=False, fused=None):
+def _tp_worker(rank, world, port, q, shared=False, fused=None, case="small"):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -77,9 +91,10 @@ def _tp_worker(rank, world, port, q, shared=False, fused=None):
     else:
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     try:
-        rt = TPRuntime(_weights(dev), B, S0 + len(SPLITS) + 1, block=16, device=dev, fused=fused)
-        first = rt.prefill(_prompt())
-        toks = rt.decode(SPLITS, tokens=first, keep_logits=True)
+        _, b, s0, splits, _ = CASES[case]
+        rt = TPRuntime(_weights(dev, case), b, s0 + len(splits) + 1, block=16, device=dev, fused=fused)
+        first = rt.prefill(_prompt(case))
+        toks = rt.decode(splits, tokens=first, keep_logits=True)
         torch.cuda.synchronize(dev)
         # numpy by value: a torch CPU tensor would travel as a file descriptor that dies with this process
         q.put((rank, first.cpu().numpy(), toks.cpu().numpy(), rt.last_logits.cpu().numpy()))
@@ -88,20 +103,21 @@ def _tp_worker(rank, world, port, q, shared=False, fused=None):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shared,fused", [(False, None), (True, False), (True, True)])
-def test_tp_world2_matches_unsharded(shared, fused):
+@pytest.mark.parametrize("shared,fused,case", [(False, None, "small"), (True, False, "small"), (True, True, "small"),
+                                               (True, True, "config4")])
+def test_tp_world2_matches_unsharded(shared, fused, case):
     """world 2: on two GPUs over NCCL, or (shared) both ranks on cuda:0 over gloo, which exercises the
     sharded data flow (column/row-parallel kernels, X rounds, all-gathers, all-reduces) on a 1-GPU box.
     fused: the row-parallel projections end in the peer-memory all-reduce (csrc/tpcomm.cu) over CUDA
-    IPC instead of the process-group all-reduce."""
+    IPC instead of the process-group all-reduce.  case "config4": OPT-30B widths, b64, prompt 2048."""
     if not shared and torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
-    f0, t0, l0 = _reference()
+    f0, t0, l0 = _reference(case=case)
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q, shared, fused)) for r in range(world)]
+    ps = [ctx.Process(target=_tp_worker, args=(r, world, port, q, shared, fused, case)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=600) for _ in ps]
