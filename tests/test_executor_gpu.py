@@ -37,6 +37,40 @@ def test_native_equals_python_loop_bitwise(x_resident, wave, k1s):
         assert torch.equal(a, c)
 
 
+@pytest.mark.parametrize("layers", [1, 3])
+def test_issue_schedule_variants_bitwise(layers):
+    """Only the schedule may change with the issue knobs: 2 or 3 device buffers, 1 or 4 X chunks
+    (chunk_rows), K1 on its own stream or not, native or Python issue, X streamed or resident -- all
+    give the same tokens, logits and host stores bit for bit.  layers = 1 covers the single-layer
+    ordering (unit u+1's loads wait on unit u's own D2H of the new position)."""
+    cfg = OPTConfig(hidden=256, layers=layers, heads=4, ffn=1024, vocab=1024, max_pos=256)
+    b, S0 = 2, 90
+    splits = [45, 91, 0, 93, 10, 95, 60, 1]
+    w = OPTWeights.random(cfg, seed=41, device="cuda", std=0.1, emb_std=0.1)
+    prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(42))
+    variants = [dict(nbuf=2, chunk_rows=1000, k1_stream=False, native=True),
+                dict(nbuf=3, chunk_rows=1000, k1_stream=False, native=True),
+                dict(nbuf=2, chunk_rows=12, k1_stream=False, native=True),
+                dict(nbuf=3, chunk_rows=12, k1_stream=True, native=True),
+                dict(nbuf=2, chunk_rows=12, k1_stream=True, native=False),
+                dict(nbuf=3, chunk_rows=12, k1_stream=False, native=False),
+                dict(nbuf=2, chunk_rows=12, k1_stream=True, native=True, x_resident=True)]
+    outs = []
+    for v in variants:
+        v = dict(v)
+        native = v.pop("native")
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, chunk_wave=0, **v)
+        first = rt.prefill(prompt)
+        toks = rt.decode(splits, tokens=first, keep_logits=True, native=native)
+        torch.cuda.synchronize()
+        n = S0 + len(splits)
+        outs.append((toks.cpu(), rt.last_logits.cpu(), rt.stores.kv[:, :n].clone()))
+        rt.close()
+    for k, o in enumerate(outs[1:], start=1):
+        for a, c in zip(outs[0], o):
+            assert torch.equal(a, c), variants[k]
+
+
 def test_native_loop_cuts_host_time():
     """Config-1 geometry is host bound under the Python loop; the executor issues a step far faster."""
     cfg = OPTConfig(hidden=768, layers=12, heads=12, ffn=3072)
