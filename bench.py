@@ -691,6 +691,10 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="config 4: head-sharded tensor parallelism over the torchrun ranks (NCCL)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != ws:
+        sys.exit(f"bench.py --gpus {args.gpus} needs that many ranks: launch it under torchrun "
+                 f"--nproc-per-node {args.gpus} (WORLD_SIZE is {ws})")
     if args.impl == "reference":
         run_reference(args)
     else:
