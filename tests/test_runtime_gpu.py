@@ -141,6 +141,23 @@ def test_config2_widths_parity_teacher_forced(criterion):
     assert not mismatched, mismatched
 
 
+def test_kv4_row_schedule_equals_column_schedule():
+    """4-bit KV pages with X resident (row schedule) or streamed (column): only the transfer plan
+    differs, so tokens and logits are bit-identical."""
+    cfg = OPTConfig(hidden=256, layers=2, heads=4, ffn=1024, vocab=1024, max_pos=256)
+    w, prompt = _setup(cfg, 3, 80, seed=3)
+    splits = [40, 0, 83, 10, 85]
+    outs = []
+    for xr in (False, True):
+        rt = KVPRRuntime(w, 3, 80 + len(splits) + 1, kv_bits=4, x_resident=xr)
+        first = rt.prefill(prompt)
+        toks = rt.decode(splits, tokens=first, keep_logits=True)
+        torch.cuda.synchronize()
+        outs.append((toks.cpu(), rt.last_logits.cpu()))
+        rt.close()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
 def test_recompute_reproduces_stored_cache_bitwise():
     """KVPR exactness (numerics.py:1-11) on the device: K1(X[0:s)) == the prefill's stored K/V, bit for bit."""
     cfg = OPTConfig(hidden=512, layers=2, heads=8, ffn=2048, vocab=1024)
