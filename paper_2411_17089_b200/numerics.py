@@ -80,6 +80,56 @@ def _pad_to(n: int, m: int) -> int:
     return (n + m - 1) // m * m
 
 
+def _heads(rows: np.ndarray, heads: int) -> np.ndarray:
+    """(n, h) -> (heads, n, d) (numerics.py:35-40)."""
+    n, h = rows.shape
+    if h % heads:
+        raise ValueError("hidden size not divisible by head count")
+    return np.ascontiguousarray(rows.reshape(n, heads, h // heads).transpose(1, 0, 2))
+
+
+def _k1_rows(x: np.ndarray, w_k: np.ndarray, w_v: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """K = x W_k, V = x W_v for the rows of x, by K1 (the tcgen05 recompute GEMM) into a page buffer."""
+    n, h = x.shape
+    dev = _dev()
+    hp = _pad_to(h, 64)  # GEMM needs K % 8 and N % 32; pad the hidden dim with zeros
+    xd = torch.zeros(n, 1, hp, dtype=torch.float16, device=dev)
+    xd[:, 0, :h] = torch.from_numpy(x).to(dev, torch.float16)
+    w = torch.zeros(2 * hp, hp, dtype=torch.float16, device=dev)
+    w[:h, :h] = torch.from_numpy(w_k.T.copy()).to(dev, torch.float16)
+    w[hp:hp + h, :h] = torch.from_numpy(w_v.T.copy()).to(dev, torch.float16)
+    pages = torch.empty(n, 2, 1, hp, dtype=torch.float16, device=dev)
+    kernels.recompute_kv(xd, w, None, pages, 1, 0, n)
+    kv = pages[:, :, 0, :h].double().cpu().numpy()  # [n, 2, h]
+    return kv[:, 0], kv[:, 1]
+
+
+def project_qkv(x, w_q, w_k, w_v, num_heads: int):
+    """Q/K/V of the rows of x, per head (numerics.py:75-92): one tcgen05 GEMM against [W_q|W_k|W_v]."""
+    x = _mat("x", x)
+    n, h = x.shape
+    mats = [_mat(name, m, h, h) for name, m in (("w_q", w_q), ("w_k", w_k), ("w_v", w_v))]
+    dev = _dev()
+    hp = _pad_to(h, 64)
+    xd = torch.zeros(n, hp, dtype=torch.float16, device=dev)
+    xd[:, :h] = torch.from_numpy(x).to(dev, torch.float16)
+    w = torch.zeros(3 * hp, hp, dtype=torch.float16, device=dev)
+    for i, m in enumerate(mats):
+        w[i * hp:i * hp + h, :h] = torch.from_numpy(m.T.copy()).to(dev, torch.float16)
+    out = torch.empty(n, 3 * hp, dtype=torch.float32, device=dev)
+    kernels.linear_simple(xd, w, None, out)
+    o = out.double().cpu().numpy()
+    return tuple(_heads(o[:, i * hp:i * hp + h], num_heads) for i in range(3))
+
+
+def build_kv(x, w_k, w_v, num_heads: int) -> KVState:
+    """Full cache from all layer inputs (numerics.py:95-104), by K1."""
+    x = _mat("x", x)
+    h = x.shape[1]
+    k, v = _k1_rows(x, _mat("w_k", w_k, h, h), _mat("w_v", w_v, h, h))
+    return KVState(_heads(k, num_heads), _heads(v, num_heads))
+
+
 def split_merge_kv(x_full, split: int, w_k, w_v, kv_suffix: KVState) -> KVState:
     """K1 rebuild of [0, split) concatenated with the transferred suffix (numerics.py:107-137)."""
     x_full = _mat("x_full", x_full)
@@ -90,23 +140,33 @@ def split_merge_kv(x_full, split: int, w_k, w_v, kv_suffix: KVState) -> KVState:
         raise ValueError(f"suffix covers {kv_suffix.seq_len} positions, expected {seq - split}")
     if split == 0:
         return kv_suffix
-    w_k = _mat("w_k", w_k, h, h)
-    w_v = _mat("w_v", w_v, h, h)
+    k, v = _k1_rows(x_full[:split], _mat("w_k", w_k, h, h), _mat("w_v", w_v, h, h))
     heads = kv_suffix.num_heads
-    dev = _dev()
-    hp = _pad_to(h, 64)  # GEMM needs K % 8 and N % 32; pad the hidden dim with zeros
-    x = torch.zeros(split, 1, hp, dtype=torch.float16, device=dev)
-    x[:, 0, :h] = torch.from_numpy(x_full[:split]).to(dev, torch.float16)
-    w = torch.zeros(2 * hp, hp, dtype=torch.float16, device=dev)
-    w[:h, :h] = torch.from_numpy(w_k.T.copy()).to(dev, torch.float16)
-    w[hp:hp + h, :h] = torch.from_numpy(w_v.T.copy()).to(dev, torch.float16)
-    pages = torch.empty(split, 2, 1, hp, dtype=torch.float16, device=dev)
-    kernels.recompute_kv(x, w, None, pages, 1, 0, split)
-    kv = pages[:, :, 0, :h].double().cpu().numpy()  # [split, 2, h]
-    d = h // heads
-    kp = kv[:, 0].reshape(split, heads, d).transpose(1, 0, 2)
-    vp = kv[:, 1].reshape(split, heads, d).transpose(1, 0, 2)
-    return KVState(np.concatenate([kp, kv_suffix.keys], axis=1), np.concatenate([vp, kv_suffix.values], axis=1))
+    return KVState(np.concatenate([_heads(k, heads), kv_suffix.keys], axis=1),
+                   np.concatenate([_heads(v, heads), kv_suffix.values], axis=1))
+
+
+def append_token_kv(kv: KVState, x_new, w_k, w_v) -> KVState:
+    """The cache with the new token's k, v appended (numerics.py:140-156); K1 on one row, so the
+    appended entry carries the bits a later split_merge_kv rebuild of that position produces."""
+    row = np.asarray(x_new, dtype=np.float64)
+    if row.ndim == 1:
+        row = row[None, :]
+    row = _mat("x_new", row, rows=1)
+    h = row.shape[1]
+    if kv.num_heads * kv.head_dim != h:
+        raise ValueError("token width does not match cache geometry")
+    k, v = _k1_rows(row, _mat("w_k", w_k, h, h), _mat("w_v", w_v, h, h))
+    return KVState(np.concatenate([kv.keys, _heads(k, kv.num_heads)], axis=1),
+                   np.concatenate([kv.values, _heads(v, kv.num_heads)], axis=1))
+
+
+def stable_softmax(logits) -> np.ndarray:
+    """Max-subtracted softmax of a 1-D vector (numerics.py:159-163).  A host-side utility of the
+    reference API (K2 fuses its own exp2-domain online softmax); computed on the device in fp64."""
+    z = torch.from_numpy(np.asarray(logits, dtype=np.float64)).to(_dev())
+    e = torch.exp(z - z.max())
+    return (e / e.sum()).cpu().numpy()
 
 
 def decode_attention(q_token, kv: KVState, w_o) -> np.ndarray:

@@ -68,3 +68,25 @@ def test_validation_matches_reference():
     bad[0, 0] = np.inf
     with pytest.raises(ValueError, match="finite"):
         gn.split_merge_kv(x, 3, bad, w_v, gn.KVState(full.keys[:, 3:], full.values[:, 3:]))
+
+
+@pytest.mark.parametrize("heads,d,seq", [(4, 64, 70), (2, 128, 33)])
+def test_build_append_project_match_oracle(heads, d, seq):
+    """build_kv / append_token_kv / project_qkv / stable_softmax on the GPU vs the fp64 oracle; the
+    appended token equals what split_merge_kv rebuilds for that position, bit for bit (both K1)."""
+    x, w_k, w_v, w_o, q = _case(9, heads, d, seq)
+    full = gn.build_kv(x, w_k, w_v, heads)
+    ref = nr.build_kv(x, w_k, w_v, heads)
+    assert _rel(full.keys, ref.keys) <= RTOL and _rel(full.values, ref.values) <= RTOL
+    grown = gn.append_token_kv(gn.build_kv(x[:-1], w_k, w_v, heads), x[-1], w_k, w_v)
+    assert np.array_equal(grown.keys, full.keys) and np.array_equal(grown.values, full.values)
+    rebuilt = gn.split_merge_kv(x, seq, w_k, w_v, gn.KVState(full.keys[:, :0], full.values[:, :0]))
+    assert np.array_equal(rebuilt.keys, full.keys)
+    w_q = w_o  # any h x h matrix
+    qh, kh, vh = gn.project_qkv(x, w_q, w_k, w_v, heads)
+    assert _rel(qh, nr.per_head(x @ w_q, heads)) <= RTOL
+    assert _rel(kh, ref.keys) <= RTOL and _rel(vh, ref.values) <= RTOL
+    z = np.random.default_rng(1).standard_normal(37) * 5
+    assert np.max(np.abs(gn.stable_softmax(z) - nr.stable_softmax(z))) <= 1e-12
+    with pytest.raises(ValueError, match="width"):
+        gn.append_token_kv(full, x[-1, :-1], w_k[:-1, :-1], w_v[:-1, :-1])
