@@ -225,9 +225,11 @@ def cmd_run(a) -> int:
     return EXIT_OK
 
 
-def cmd_validate(a) -> int:
-    """Device split/merge exactness: K1-rebuilt pages == the prefill's stored pages, bit for bit, and the
-    decode output is identical for every split, on randomized small geometries (cli.py:343-390 analogue)."""
+def run_validation_cases(seed: int, cases: int) -> list[str]:
+    """Randomized split/merge exactness on the device (cli.py:343-377 analogue); returns failure lines.
+
+    Per case: K1-rebuilt pages == the prefill's stored pages, bit for bit, and the decode output is
+    identical for every split, on randomized small geometries."""
     import random
 
     import torch
@@ -236,9 +238,9 @@ def cmd_validate(a) -> int:
     from .runtime import KVPRRuntime
     from .weights import OPTConfig, OPTWeights
 
-    rng = random.Random(a.seed)
+    rng = random.Random(seed)
     failures = []
-    for case in range(a.cases):
+    for case in range(cases):
         heads = rng.choice([1, 2, 4, 8])
         d = rng.choice([64, 128])
         h = heads * d
@@ -264,6 +266,11 @@ def cmd_validate(a) -> int:
         for l, lg in outs[1:]:
             if not torch.equal(lg, outs[0][1]):
                 failures.append(f"case={case} h={h} b={b} s'={S0 + 1} l={l}: logits differ from l=0")
+    return failures
+
+
+def cmd_validate(a) -> int:
+    failures = run_validation_cases(a.seed, a.cases)
     if failures:
         for f in failures:
             print(f"FAIL {f}", file=sys.stderr)
