@@ -33,6 +33,9 @@ CASES = {
     "small": (CFG, B, S0, SPLITS, 0.1),
     "config4": (OPTConfig(hidden=7168, layers=1, heads=56, ffn=28672, vocab=50272, max_pos=2048 + 16), 64, 2048,
                 [1596, 1597, 1598], 0.02),
+    # eight ranks (config 4's world size): one head of 128 per rank
+    "world8": (OPTConfig(hidden=1024, layers=2, heads=8, ffn=4096, vocab=2048, max_pos=256), 4, 100,
+               [50, 0, 101, 7, 103], 0.1),
 }
 
 
@@ -103,17 +106,18 @@ def _tp_worker(rank, world, port, q, shared=False, fused=None, case="small"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shared,fused,case", [(False, None, "small"), (True, False, "small"), (True, True, "small"),
-                                               (True, True, "config4")])
-def test_tp_world2_matches_unsharded(shared, fused, case):
+@pytest.mark.parametrize("shared,fused,case,world", [(False, None, "small", 2), (True, False, "small", 2),
+                                                     (True, True, "small", 2), (True, True, "config4", 2),
+                                                     (True, False, "world8", 8), (True, True, "world8", 8)])
+def test_tp_world2_matches_unsharded(shared, fused, case, world):
     """world 2: on two GPUs over NCCL, or (shared) both ranks on cuda:0 over gloo, which exercises the
     sharded data flow (column/row-parallel kernels, X rounds, all-gathers, all-reduces) on a 1-GPU box.
     fused: the row-parallel projections end in the peer-memory all-reduce (csrc/tpcomm.cu) over CUDA
-    IPC instead of the process-group all-reduce.  case "config4": OPT-30B widths, b64, prompt 2048."""
-    if not shared and torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+    IPC instead of the process-group all-reduce.  case "config4": OPT-30B widths, b64, prompt 2048;
+    case "world8": eight ranks sharing the GPU (config 4's world size, one head per rank)."""
+    if not shared and torch.cuda.device_count() < world:
+        pytest.skip(f"needs >= {world} GPUs")
     f0, t0, l0 = _reference(case=case)
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
