@@ -69,7 +69,7 @@ def main():
         gshapes += [(m, n, k) for m in (4, 8) for (n, k) in ((4096, 4096), (16384, 4096), (4096, 16384),
                                                              (5120, 5120), (20480, 5120), (5120, 20480))]
         for M, N, K in gshapes:
-            for bn in (-2, -1):
+            for bn in ((-2, -1) if M * K * 2 <= 96 * 1024 else (-1,)):  # gemv stages M x K of A in smem
                 t = run(M, N, K, bn, ws=wsb)
                 print(json.dumps({"M": M, "N": N, "K": K, "bn": bn, "split_ws": True, "us": round(t * 1e6, 2),
                                   "weight_gbs": round(N * K * 2 / t / 1e9, 1)}), flush=True)
