@@ -17,7 +17,22 @@ ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-_ACCEPTANCE: dict[str, tuple[str, bool]] = {}
+class _Criteria:
+    """Headline properties the tests establish, printed as one [PASS]/[FAIL] line each after the run
+    (the reference's acceptance-summary output format)."""
+
+    def __init__(self) -> None:
+        self.results: dict[str, tuple[str, bool]] = {}
+
+    def __call__(self, key: str, desc: str, ok: bool) -> bool:
+        self.results[key] = (desc, bool(ok))
+        return bool(ok)
+
+    def lines(self):
+        return [f"[{'PASS' if ok else 'FAIL'}] criterion {k}: {d}" for k, (d, ok) in sorted(self.results.items())]
+
+
+_CRITERIA = _Criteria()
 
 
 def pytest_configure(config):
@@ -44,22 +59,16 @@ def pytest_collection_modifyitems(config, items):
 
 @pytest.fixture
 def criterion():
-    """Record an acceptance criterion outcome; returns the ok flag."""
-
-    def record(key: str, desc: str, ok: bool) -> bool:
-        _ACCEPTANCE[key] = (desc, bool(ok))
-        return bool(ok)
-
-    return record
+    """record(key, description, ok) -> ok."""
+    return _CRITERIA
 
 
 def pytest_terminal_summary(terminalreporter, exitstatus, config):
-    if not _ACCEPTANCE:
-        return
-    terminalreporter.section("acceptance criteria")
-    for key in sorted(_ACCEPTANCE):
-        desc, ok = _ACCEPTANCE[key]
-        terminalreporter.write_line(f"[{'PASS' if ok else 'FAIL'}] criterion {key}: {desc}")
+    lines = _CRITERIA.lines()
+    if lines:
+        terminalreporter.section("acceptance criteria")
+        for line in lines:
+            terminalreporter.write_line(line)
 
 
 @pytest.fixture(scope="session")
