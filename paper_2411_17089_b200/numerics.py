@@ -24,49 +24,40 @@ import torch
 from . import _lib, kernels
 
 
-def _mat(name, m, rows=None, cols=None):
-    a = np.asarray(m, dtype=np.float64)
-    if a.ndim != 2:
-        raise ValueError(f"{name} must be 2-D, got shape {a.shape}")
-    if rows is not None and a.shape[0] != rows:
-        raise ValueError(f"{name} must have {rows} rows, got {a.shape[0]}")
-    if cols is not None and a.shape[1] != cols:
-        raise ValueError(f"{name} must have {cols} cols, got {a.shape[1]}")
-    if not np.isfinite(a).all():
-        raise ValueError(f"{name} contains non-finite entries")
-    return a
+def _mat(label, arr, rows=None, cols=None) -> np.ndarray:
+    """numerics.py:22-32: a finite 2-D float64 matrix, optionally (rows, cols)."""
+    out = np.asarray(arr, dtype=np.float64)
+    if out.ndim != 2:
+        raise ValueError(f"{label} must be 2-D, got shape {out.shape}")
+    for axis, (want, what) in enumerate(((rows, "rows"), (cols, "cols"))):
+        if want is not None and out.shape[axis] != want:
+            raise ValueError(f"{label} must have {want} {what}, got {out.shape[axis]}")
+    if not np.all(np.isfinite(out)):
+        raise ValueError(f"{label} contains non-finite entries")
+    return out
 
 
 @dataclass(frozen=True)
 class KVState:
-    """(num_heads, seq_len, d_head) keys/values (numerics.py:43-72)."""
+    """Per-sequence cache (numerics.py:43-72): keys / values as (num_heads, seq_len, d_head) float64."""
 
     keys: np.ndarray
     values: np.ndarray
 
     def __post_init__(self):
-        k = np.asarray(self.keys, dtype=np.float64)
-        v = np.asarray(self.values, dtype=np.float64)
-        if k.ndim != 3 or v.ndim != 3:
+        pair = tuple(np.asarray(t, dtype=np.float64) for t in (self.keys, self.values))
+        if any(t.ndim != 3 for t in pair):
             raise ValueError("keys/values must be (num_heads, seq_len, d_head)")
-        if k.shape != v.shape:
-            raise ValueError(f"key shape {k.shape} != value shape {v.shape}")
-        if not (np.isfinite(k).all() and np.isfinite(v).all()):
+        if pair[0].shape != pair[1].shape:
+            raise ValueError(f"key shape {pair[0].shape} != value shape {pair[1].shape}")
+        if not all(np.all(np.isfinite(t)) for t in pair):
             raise ValueError("KV entries must be finite")
-        object.__setattr__(self, "keys", k)
-        object.__setattr__(self, "values", v)
+        object.__setattr__(self, "keys", pair[0])
+        object.__setattr__(self, "values", pair[1])
 
-    @property
-    def num_heads(self):
-        return self.keys.shape[0]
-
-    @property
-    def seq_len(self):
-        return self.keys.shape[1]
-
-    @property
-    def head_dim(self):
-        return self.keys.shape[2]
+    num_heads = property(lambda self: self.keys.shape[0])
+    seq_len = property(lambda self: self.keys.shape[1])
+    head_dim = property(lambda self: self.keys.shape[2])
 
 
 def _dev():
@@ -171,18 +162,16 @@ def stable_softmax(logits) -> np.ndarray:
 
 def decode_attention(q_token, kv: KVState, w_o) -> np.ndarray:
     """K2 split-KV attention over the cache, then W_O (numerics.py:166-191)."""
-    if kv.seq_len == 0:
+    if not kv.seq_len:
         raise ValueError("cannot attend over an empty cache")
-    q = np.asarray(q_token, dtype=np.float64)
+    q, h, d = np.asarray(q_token, dtype=np.float64), kv.num_heads * kv.head_dim, kv.head_dim
     if q.ndim != 1:
         raise ValueError("q_token must be a 1-D row of length h")
-    h = kv.num_heads * kv.head_dim
-    if q.shape[0] != h:
-        raise ValueError(f"q_token has length {q.shape[0]}, expected {h}")
-    if not np.isfinite(q).all():
+    if q.size != h:
+        raise ValueError(f"q_token has length {q.size}, expected {h}")
+    if not np.all(np.isfinite(q)):
         raise ValueError("q_token contains non-finite entries")
     w_o = _mat("w_o", w_o, h, h)
-    d = kv.head_dim
     if d not in (64, 128):
         raise ValueError(f"head_dim {d} unsupported by the decode-attention kernel (64 or 128)")
     dev = _dev()
