@@ -145,6 +145,12 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
       }
     }
   }
+  static const int bn_env = [] {  // KVPR_K1_BN = 32..256 / 512: tile override (experiments; same bits)
+    const char* e = getenv("KVPR_K1_BN");
+    const int v = e != nullptr ? atoi(e) : 0;
+    return (v == 32 || v == 64 || v == 128 || v == 256 || v == 512) ? v : 0;
+  }();
+  if (bn_env) bn = bn_env;
   return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, bn, static_cast<cudaStream_t>(stream));
 }
 
