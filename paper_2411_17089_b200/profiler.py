@@ -5,7 +5,7 @@ reference replaces the profiler with hand-entered CSV records fed to
 ``calibrate`` (hwprofile.py:108-166); here the records are produced on the
 device with CUDA events:
 
-  h2d / d2h : pinned (cudaHostRegister'ed) host <-> HBM copies of 2^24..2^30
+  h2d / d2h : pinned host (the host stores' allocation, hostmem.py) <-> HBM copies of 2^24..2^30
               bytes on a dedicated copy stream (the runtime's transfer path,
               kvpr_copy_async);
   gemm      : the K1 recompute GEMM itself (kvpr_recompute_kv) at several
@@ -23,6 +23,7 @@ import statistics
 import torch
 
 from . import _lib, kernels
+from .hostmem import pinned_empty, unpin
 from .hwprofile import CalibrationResult, Measurement, calibrate
 
 
@@ -43,11 +44,8 @@ def _time(fn, stream: torch.cuda.Stream, reps: int, warm: int = 2) -> float:
 def probe_transfers(device=None, sizes=(1 << 24, 1 << 26, 1 << 28, 1 << 30), reps: int = 5) -> list[Measurement]:
     dev = torch.device(device or "cuda")
     big = max(sizes)
-    host = torch.empty(big, dtype=torch.uint8)
+    host = pinned_empty((big,), torch.uint8)  # the host stores' allocation (hostmem)
     host.fill_(1)
-    rc = torch.cuda.cudart().cudaHostRegister(host.data_ptr(), big, 0)
-    if int(rc) != 0:
-        raise RuntimeError(f"cudaHostRegister failed ({rc})")
     try:
         d = torch.empty(big, dtype=torch.uint8, device=dev)
         s = torch.cuda.Stream(dev)
@@ -60,7 +58,7 @@ def probe_transfers(device=None, sizes=(1 << 24, 1 << 26, 1 << 28, 1 << 30), rep
         del d
         return out
     finally:
-        torch.cuda.cudart().cudaHostUnregister(host.data_ptr())
+        unpin(host)
 
 
 def probe_recompute(hidden: int, batch: int, prefix_lens=(128, 256, 512, 1024), device=None,

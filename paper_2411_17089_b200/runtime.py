@@ -34,6 +34,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib, kernels
+from .hostmem import pinned_empty, unpin
 from .weights import OPTWeights
 
 F16 = torch.float16
@@ -46,33 +47,24 @@ def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) ->
 
 
 class HostStores:
-    """Per-layer X and KV stores in page-locked host memory (exact-size cudaHostRegister)."""
+    """Per-layer X and KV stores in page-locked host memory, exact size (hostmem.pinned_empty)."""
 
     def __init__(self, layers: int, capacity: int, batch: int, hidden: int, kv_page_bytes: int | None = None,
                  with_x: bool = True):
         self.layers, self.capacity, self.batch, self.hidden = layers, capacity, batch, hidden
-        self.x = torch.empty(layers, capacity if with_x else 0, batch, hidden, dtype=F16)
+        self.x = pinned_empty((layers, capacity if with_x else 0, batch, hidden), F16)
         if kv_page_bytes is None:  # fp16 pages [pos][2][b][h]
-            self.kv = torch.empty(layers, capacity, 2, batch, hidden, dtype=F16)
+            self.kv = pinned_empty((layers, capacity, 2, batch, hidden), F16)
         else:  # compressed pages (4-bit groupwise), kv_page_bytes each
-            self.kv = torch.empty(layers, capacity, kv_page_bytes, dtype=torch.uint8)
-        self._registered = []
-        for t in (self.x, self.kv):
-            if t.numel() == 0:
-                continue
-            rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * t.element_size(), 0)
-            if int(rc) != 0:
-                raise RuntimeError(f"cudaHostRegister failed ({rc}) for {t.numel() * t.element_size() / 2**30:.1f} GiB")
-            self._registered.append(t)
+            self.kv = pinned_empty((layers, capacity, kv_page_bytes), torch.uint8)
 
     @property
     def nbytes(self) -> int:
         return self.x.numel() * 2 + self.kv.numel() * self.kv.element_size()
 
     def close(self) -> None:
-        for t in self._registered:
-            torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
-        self._registered = []
+        unpin(self.x)
+        unpin(self.kv)
 
     def __del__(self):  # pragma: no cover - best effort
         try:

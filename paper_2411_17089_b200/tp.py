@@ -34,6 +34,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib, kernels
+from .hostmem import pinned_empty, unpin
 from .runtime import F16, F32, _copy
 from .weights import LayerWeights, OPTWeights
 
@@ -257,12 +258,8 @@ class TPRuntime:
         self.ds = torch.cuda.Stream(self.dev)
         self.comm = torch.cuda.Stream(self.dev)
         # host stores: compact X (owned blocks only) and local-head KV
-        self.store_x = torch.empty(cfg.layers, lay.compact_capacity(capacity), b, h, dtype=F16)
-        self.store_kv = torch.empty(cfg.layers, capacity, 2, b, hs, dtype=F16)
-        for t in (self.store_x, self.store_kv):
-            rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * 2, 0)
-            if int(rc) != 0:
-                raise RuntimeError(f"cudaHostRegister failed ({rc})")
+        self.store_x = pinned_empty((cfg.layers, lay.compact_capacity(capacity), b, h), F16)
+        self.store_kv = pinned_empty((cfg.layers, capacity, 2, b, hs), F16)
         z = lambda *s, dt=F16: torch.empty(*s, dtype=dt, device=self.dev)  # noqa: E731
         self.nbuf = 2
         self.kv_dev = z(2, capacity, 2, b, hs)
@@ -516,4 +513,4 @@ class TPRuntime:
             if err:
                 raise RuntimeError("fused TP all-reduce: a peer flag wait timed out (results are invalid)")
         for t in (self.store_x, self.store_kv):
-            torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+            unpin(t)

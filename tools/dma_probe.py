@@ -23,8 +23,9 @@ ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
 main = torch.cuda.Stream()
 side = torch.cuda.Stream()
 N = 1 << 30
-host = torch.empty(N, dtype=torch.uint8)
-torch.cuda.cudart().cudaHostRegister(host.data_ptr(), N, 0)
+from paper_2411_17089_b200.hostmem import mode, pinned_empty  # noqa: E402
+
+host = pinned_empty((N,), torch.uint8)  # KVPR_HOST_ALLOC=register|hostalloc (the host stores' allocation)
 dbuf = torch.empty(N, dtype=torch.uint8, device=dev)
 dbuf2 = torch.empty(N, dtype=torch.uint8, device=dev)
 
@@ -77,4 +78,5 @@ for ctas in (8, 16, 32):
                                   side.cuda_stream))
     r["pull_gbs_alone"] = round(gbs, 1)
     res[f"sm_pull_{ctas}ctas"] = r
+res["host_alloc"] = mode()
 print(json.dumps(res))
