@@ -20,6 +20,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib, kernels
+from .hostmem import pinned_empty, unpin
 from .runtime import F16, F32, HostStores, _copy, chunk_bounds
 from .weights import LayerWeights, OPTWeights
 
@@ -83,15 +84,12 @@ class StreamedRuntime:
         _lib.load()
         h, f, b, L = cfg.hidden, cfg.ffn, batch, cfg.layers
         self.layer_numel = sum(_numel(s) for s in _shapes(h, f).values())
-        # host: all layers' weights in one registered flat buffer (views per layer)
-        self.host_w = torch.empty(L, self.layer_numel, dtype=F16)
+        # host: all layers' weights in one page-locked flat buffer (views per layer)
+        self.host_w = pinned_empty((L, self.layer_numel), F16)  # page-locked like the host stores (hostmem)
         for j, lw in enumerate(weights.layers):
             hv = _views(self.host_w[j], h, f)
             for name in _FIELDS:
                 getattr(hv, name).copy_(getattr(lw, name))
-        rc = torch.cuda.cudart().cudaHostRegister(self.host_w.data_ptr(), self.host_w.numel() * 2, 0)
-        if int(rc) != 0:
-            raise RuntimeError(f"cudaHostRegister failed ({rc}) for the weight store")
         # resident: embeddings / final LN (tied LM head); device weight slots for 2 layers
         self.embed, self.pos, self.lnf_g, self.lnf_b = (t.to(self.dev) for t in
                                                          (weights.embed, weights.pos, weights.lnf_g, weights.lnf_b))
@@ -311,4 +309,4 @@ class StreamedRuntime:
     def close(self) -> None:
         for st in self.stores:
             st.close()
-        torch.cuda.cudart().cudaHostUnregister(self.host_w.data_ptr())
+        unpin(self.host_w)
