@@ -94,6 +94,11 @@ int kvpr_sm_count(int device);
 int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* kv_pages, int batch,
                       int pos_begin, int pos_end, int hidden, void* stream);
 
+/* The tile kvpr_recompute_kv uses for a launch over `positions` positions on a GPU with `sms` SMs:
+ * 512 = 256 x 256 CTA-pair tile (cta_group::2), 32..256 = 128 x BN tile on one CTA, 0 = invalid
+ * arguments.  Pure host function (no CUDA call); the bench labels its roofline line with it. */
+int kvpr_recompute_tile(int batch, int positions, int hidden, int sms);
+
 /* Fused projection: out = epilogue(A[M,K] . W[N,K]^T + bias), tcgen05 GEMM.
  * Used for the decode-token q/k/v (K3), out-proj + residual (K4), fc1+ReLU and
  * fc2 + residual (K6), LM head (K8), and the prefill that fills the host stores.

@@ -31,6 +31,7 @@ EXPORTS = (
     "kvpr_kernel_launches",
     "kvpr_sm_count",
     "kvpr_recompute_kv",
+    "kvpr_recompute_tile",
     "kvpr_linear",
     "kvpr_linear_ws",
     "kvpr_layernorm_linear_ws",
@@ -117,6 +118,7 @@ _SIGS = {
     "kvpr_kernel_launches": ([], _ll),
     "kvpr_sm_count": ([_i], _i),
     "kvpr_recompute_kv": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp], _i),
+    "kvpr_recompute_tile": ([_i, _i, _i, _i], _i),
     "kvpr_linear": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp], _i),
     "kvpr_linear_ws": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp, _sz, _vp], _i),
     "kvpr_layernorm_linear_ws": ([_vp, _ll, _vp, _vp, _f, _vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i,

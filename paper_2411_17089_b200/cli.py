@@ -57,6 +57,8 @@ class Setup:
     recompute: bool
     budget: float | None
     runtime: dict
+    weights_resident: bool = True
+    granularity: str = "coarse"
 
 
 def _only(section: str, given: dict, allowed) -> None:
@@ -117,8 +119,6 @@ def load_config(path: str) -> Setup:
             rec = rec == "on"
         if pol.get("granularity", "coarse") not in ("coarse", "fine"):
             raise ConfigError("policy.granularity must be 'coarse' or 'fine'")
-        if not pol.get("weights_resident", True):
-            raise ConfigError("policy.weights_resident=false (streamed weights) is not implemented on the B200 path")
         schedule = pol.get("schedule", "row")
         if schedule not in ("row", "column"):
             raise ConfigError("policy.schedule must be 'row' or 'column'")
@@ -128,7 +128,8 @@ def load_config(path: str) -> Setup:
         raise
     except (ValueError, TypeError) as exc:
         raise ConfigError(str(exc)) from exc
-    return Setup(spec, wl, prof, schedule, bool(rec), hw.get("gpu_mem_budget_bytes"), rt)
+    return Setup(spec, wl, prof, schedule, bool(rec), hw.get("gpu_mem_budget_bytes"), rt,
+                 bool(pol.get("weights_resident", True)), pol.get("granularity", "coarse"))
 
 
 def _plan(s: Setup, l_override: int | None) -> SplitPlan:
@@ -173,7 +174,8 @@ def cmd_profile(a) -> int:
 
 def _device_bytes(s: Setup, capacity: int) -> float:
     h, L, f, b = s.spec.hidden_dim, s.spec.num_layers, s.spec.ffn_dim, s.wl.batch_size
-    weights = L * (4 * h * h + 2 * h * f) * 2 + 2 * 50272 * h * 2
+    resident_layers = L if s.weights_resident and s.wl.num_batches == 1 else 2  # streamed: two layer slots
+    weights = resident_layers * (4 * h * h + 2 * h * f) * 2 + 2 * 50272 * h * 2
     buffers = 2 * capacity * 3 * b * h * 2 + b * 50272 * 4
     return float(weights + buffers)
 
@@ -191,6 +193,8 @@ def cmd_run(a) -> int:
             plan, pspec, pwl, _ = import_plan(json.load(fh))
         if (pspec, pwl) != (s.spec, s.wl):
             raise ConfigError("plan context does not match the config")
+        if plan.mode != s.schedule:
+            raise ConfigError(f"plan mode {plan.mode!r} does not match policy.schedule {s.schedule!r}")
     else:
         plan = _plan(s, a.l)
     cap = s.wl.prompt_len + s.wl.gen_len + 1
@@ -204,7 +208,12 @@ def cmd_run(a) -> int:
     w = OPTWeights.random(cfg, seed=int(rt_cfg.get("seed", 0)), device=dev, std=float(rt_cfg.get("weights_std", 0.02)))
     prompt = torch.randint(0, cfg.vocab, (s.wl.batch_size, s.wl.prompt_len),
                            generator=torch.Generator().manual_seed(int(rt_cfg.get("seed", 0)) + 1))
-    rt = KVPRRuntime(w, s.wl.batch_size, cap, device=dev, chunks=int(rt_cfg.get("chunks", 4)))
+    kv_bits = _kv_bits(s)
+    if not s.weights_resident or s.wl.num_batches > 1:
+        return _run_streamed(a, s, plan, w, cap, dev, need)
+    # the row schedule keeps X resident in HBM (t_act = 0 in its plan); column streams X over PCIe
+    rt = KVPRRuntime(w, s.wl.batch_size, cap, device=dev, chunks=int(rt_cfg.get("chunks", 4)),
+                     x_resident=s.schedule == "row", kv_bits=kv_bits)
     first = rt.prefill(prompt)
     tracer = tr.Tracer()
     rt.decode(plan.splits, tokens=first, trace=tracer)
@@ -221,6 +230,52 @@ def cmd_run(a) -> int:
              f"gpu_utilization={rep['gpu_util']!r}", f"peak_gpu_bytes={need!r}",
              f"splits={','.join(str(x) for x in plan.splits)}"]
     lines += [f"busy_{k}={v!r}" for k, v in sorted(rep["breakdown"].items())]
+    sys.stdout.write("\n".join(lines) + "\n")
+    return EXIT_OK
+
+
+def _kv_bits(s: Setup) -> int | None:
+    """fp16 pages for q = p (or None); 4-bit groupwise pages for q = 0.5625 (costmodel.py:109-118)."""
+    q = s.wl.kv_bytes_per_element
+    if q is None or q == s.spec.precision_bytes:
+        return None
+    if q == 0.5625:
+        return 4
+    raise ConfigError(f"workload.kv_bytes_per_element={q!r}: the B200 runtime stores fp16 pages or 4-bit "
+                      "groupwise pages (0.5625)")
+
+
+def _run_streamed(a, s: Setup, plan: SplitPlan, w, cap: int, dev, need: float) -> int:
+    """policy.weights_resident=false or num_batches > 1: the throughput-oriented column schedule with
+    layer weights streamed from host (streamed.StreamedRuntime, §8f rank 1).  Timed with CUDA events;
+    it has no per-task trace, so --trace / --metrics are rejected."""
+    import torch
+
+    from .streamed import StreamedRuntime
+
+    if s.schedule != "column":
+        raise ConfigError("streamed weights / num_batches > 1 run the column schedule (policy.schedule='column')")
+    if _kv_bits(s) is not None:
+        raise ConfigError("streamed weights run fp16 KV pages")
+    if a.trace or a.metrics:
+        raise ConfigError("--trace / --metrics need resident weights (the streamed runtime has no task trace)")
+    K = s.wl.num_batches
+    g = torch.Generator().manual_seed(int(s.runtime.get("seed", 0)) + 1)
+    prompts = [torch.randint(0, w.cfg.vocab, (s.wl.batch_size, s.wl.prompt_len), generator=g) for _ in range(K)]
+    rt = StreamedRuntime(w, s.wl.batch_size, K, cap, device=dev, granularity=s.granularity,
+                         chunks=int(s.runtime.get("chunks", 4)))
+    first = rt.prefill(prompts)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(rt.cs)
+    rt.decode(plan.splits, tokens=first)
+    e1.record(rt.cs)
+    torch.cuda.synchronize(dev)
+    rt.close()
+    makespan = e0.elapsed_time(e1) / 1e3
+    lines = [f"makespan_s={makespan!r}",
+             f"decode_throughput_tok_s={s.wl.batch_size * K * s.wl.gen_len / makespan!r}",
+             f"peak_gpu_bytes={need!r}", f"splits={','.join(str(x) for x in plan.splits)}",
+             f"weights=streamed granularity={s.granularity} num_batches={K}"]
     sys.stdout.write("\n".join(lines) + "\n")
     return EXIT_OK
 

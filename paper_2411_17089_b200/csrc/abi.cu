@@ -97,6 +97,33 @@ long long kvpr_kernel_launches(void) { return g_kernel_launches.load(std::memory
 
 int kvpr_sm_count(int device) { return sm_count(device); }
 
+// K1's tile for a launch over `positions` positions: CTA-pair 256x256 tiles (512) when they fill the
+// SM pairs; below that (small models, short chunks) the widest 1-CTA tile (BN 32..256) that still
+// gives >= sms/2 tiles.  Every shape accumulates K in the same order, so the choice never changes
+// a bit (measured: tools/decode_gemm_bench.py --k1-only).  KVPR_K1_BN overrides it (experiments).
+int kvpr_recompute_tile(int batch, int positions, int hidden, int sms) {
+  if (batch <= 0 || positions <= 0 || hidden <= 0 || sms <= 0) return 0;
+  const long long M = static_cast<long long>(positions) * batch;
+  const long long N = 2LL * hidden;
+  int bn = 512;
+  if (((M + 255) / 256) * ((N + 255) / 256) < sms / 2) {
+    const long long m_blk = (M + 127) / 128;
+    bn = 32;
+    for (int c = 256; c >= 32; c /= 2) {
+      if (m_blk * ((N + c - 1) / c) >= sms / 2) {
+        bn = c;
+        break;
+      }
+    }
+  }
+  static const int bn_env = [] {
+    const char* e = getenv("KVPR_K1_BN");
+    const int v = e != nullptr ? atoi(e) : 0;
+    return (v == 32 || v == 64 || v == 128 || v == 256 || v == 512) ? v : 0;
+  }();
+  return bn_env ? bn_env : bn;
+}
+
 int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* kv_pages, int batch, int pos_begin,
                       int pos_end, int hidden, void* stream) {
   g_err[0] = 0;
@@ -127,30 +154,9 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
   a.flags = 0;
   const __half* a_ptr = static_cast<const __half*>(x) + (long long)pos_begin * bh;
   const int M = (pos_end - pos_begin) * batch;
-  // CTA-pair 256x256 tiles when they fill the SM pairs; below that (small models, short chunks)
-  // the widest 1-CTA tile that still gives >= sms/2 tiles (every shape accumulates K in the same
-  // order, so the choice never changes a bit; measured: tools/decode_gemm_bench.py --k1-only)
   int dev = 0;
   cudaGetDevice(&dev);
-  const int sms = sm_count(dev);
-  const long long N = 2LL * hidden;
-  int bn = 512;
-  if (((M + 255) / 256) * ((N + 255) / 256) < sms / 2) {
-    const long long m_blk = (M + 127) / 128;
-    bn = 32;
-    for (int c = 256; c >= 32; c /= 2) {
-      if (m_blk * ((N + c - 1) / c) >= sms / 2) {
-        bn = c;
-        break;
-      }
-    }
-  }
-  static const int bn_env = [] {  // KVPR_K1_BN = 32..256 / 512: tile override (experiments; same bits)
-    const char* e = getenv("KVPR_K1_BN");
-    const int v = e != nullptr ? atoi(e) : 0;
-    return (v == 32 || v == 64 || v == 128 || v == 256 || v == 512) ? v : 0;
-  }();
-  if (bn_env) bn = bn_env;
+  const int bn = kvpr_recompute_tile(batch, pos_end - pos_begin, hidden, sm_count(dev));
   return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, bn, static_cast<cudaStream_t>(stream));
 }
 

@@ -219,19 +219,24 @@ int issue_k1_on(Decoder& D, const Unit& x, __half* xd, __half* kvd, cudaStream_t
 }
 
 // K1 of unit u on the recompute stream, issued one unit ahead of its layer's compute so the rebuild
-// overlaps the previous layer's tail (small models: the layer chain is latency bound).  Hazards:
-// its pages [0, l) of buffer u % nbuf were last read by K2(u - nbuf); its X rows come from the H2D
-// of u (which waited for that K2) or, X resident, from LN1 of the same layer one step back.
+// overlaps the previous layer's tail (small models: the layer chain is latency bound).  Hazards on
+// buffer u % nbuf: its pages [0, l) were last read by K2(u - nbuf) (ev_done) and by the D2H of
+// unit u - nbuf, which copies that unit's new page s_prev - 1 to the host store (ev_d2h).  When
+// u - nbuf belongs to the previous step (layer j < nbuf), s_prev - 1 = s' - 2 lies inside [0, l)
+// whenever l >= s' - 1, so K1 must not start before that copy has read the page.  The streamed-X
+// H2D of u already waits on both, and so do its chunk events, but the X-resident path has no H2D
+// and has to wait itself.  Its X rows come from the H2D of u or, X resident, from LN1 of the same
+// layer one step back (ev_qkv).
 int issue_k1(Decoder& D, int u, int base, const int* splits) {
   const kvpr_decoder_desc& d = D.d;
   const Unit x = unit_of(D, u, base, splits);
   cudaStream_t rs = static_cast<cudaStream_t>(d.recompute_stream);
-  if (d.x_resident) {
-    if (u >= d.nbuf) KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_done[(u - d.nbuf) % D.R], 0), "k1 wait buffer"));
-    if (u >= d.layers) KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_qkv[(u - d.layers) % D.R], 0), "k1 wait X row"));
-  } else if (u >= d.nbuf) {
+  if (u >= d.nbuf) {
     KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_done[(u - d.nbuf) % D.R], 0), "k1 wait buffer"));
+    KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_d2h[(u - d.nbuf) % D.R], 0), "k1 wait page store"));
   }
+  if (d.x_resident && u >= d.layers)
+    KV_TRY(ck(cudaStreamWaitEvent(rs, D.ev_qkv[(u - d.layers) % D.R], 0), "k1 wait X row"));
   const long long bh = static_cast<long long>(d.batch) * d.hidden;
   const kvpr_layer_desc& Lw = D.layer[x.j];
   __half* xd = d.x_resident ? static_cast<__half*>(Lw.dev_x)

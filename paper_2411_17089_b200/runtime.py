@@ -139,7 +139,8 @@ class KVPRRuntime:
             raise ValueError(f"capacity {capacity} exceeds the position table ({cfg.max_pos})")
         self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
         self.dev = torch.device(device) if device is not None else weights.embed.device
-        self.chunks, self.nbuf = int(os.environ.get("KVPR_CHUNKS", chunks)), nbuf  # env: A/B knob
+        # env: A/B knob; at most 16 chunks, the native executor's per-unit chunk table (executor.cu)
+        self.chunks, self.nbuf = max(1, min(16, int(os.environ.get("KVPR_CHUNKS", chunks)))), nbuf
         # a K1 chunk carries >= KVPR_CHUNK_MB (default 32) MiB of X (>= 64 positions): every extra X
         # DMA costs copy-engine time (OPT-6.7B b4: 1/2/4/8 chunks of ~30 MB of X in total -> 98.8 /
         # 97.4 / 96.0 / 94.1% of the overlap roofline, profiles/r01_chunk_ab.jsonl), so small batches
@@ -190,7 +191,7 @@ class KVPRRuntime:
         R = cfg.layers + nbuf + 2
         self._R = R
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
-        self.ev_x = [[ev() for _ in range(chunks)] for _ in range(R)]
+        self.ev_x = [[ev() for _ in range(self.chunks)] for _ in range(R)]
         self.ev_kv = [ev() for _ in range(R)]
         self.ev_qkv = [ev() for _ in range(R)]
         self.ev_d2h = [ev() for _ in range(R)]

@@ -104,3 +104,12 @@ def test_product_never_imports_oracle():
     for p in pkg.rglob("*.py"):
         text = p.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", text, flags=re.M), f"{p} imports the oracle"
+
+
+def test_recompute_tile_choice(lib):
+    """K1's tile (host-side, no GPU): the CTA pair when 256x256 tiles fill the 74 SM pairs, else the
+    widest 1-CTA tile that still covers half the SMs; the bench labels its roofline line with it."""
+    assert lib.kvpr_recompute_tile(32, 296, 4096, 148) == 512   # config 2 chunk: 37 x 32 pair tiles
+    assert lib.kvpr_recompute_tile(4, 250, 768, 148) == 128     # config 1: 8 m-blocks x 12 = 96 tiles
+    assert lib.kvpr_recompute_tile(1, 1, 256, 148) == 32
+    assert lib.kvpr_recompute_tile(0, 10, 256, 148) == 0

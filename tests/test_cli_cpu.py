@@ -58,3 +58,20 @@ def test_plan_round_trip_through_file(tmp_path, capsys):
     doc = json.loads(out.read_text())
     assert [d["seq_len"] for d in doc["decisions"]] == [9, 10]
     assert doc["mode"] == "row"
+
+
+def test_plan_accepts_streamed_weights_like_the_reference(tmp_path, capsys):
+    """policy.weights_resident=false is a valid plan config in the reference CLI (exit 0); only `run`
+    decides how to execute it (streamed.StreamedRuntime)."""
+    doc = dict(BASE, policy={"schedule": "column", "weights_resident": False, "granularity": "fine"})
+    assert cli.main(["plan", "--config", _cfg(tmp_path, doc)]) == cli.EXIT_OK
+    assert json.loads(capsys.readouterr().out)["mode"] == "column"
+
+
+def test_run_rejects_plan_of_the_other_mode(tmp_path, capsys):
+    """A plan made for the row schedule (t_act = 0) must not drive the column runtime, and vice versa."""
+    out = tmp_path / "plan.json"
+    assert cli.main(["plan", "--config", _cfg(tmp_path, BASE), "--out", str(out)]) == 0  # row (default)
+    col = dict(BASE, policy={"schedule": "column"})
+    assert cli.main(["run", "--config", _cfg(tmp_path, col), "--plan", str(out)]) == cli.EXIT_INVALID
+    assert "plan mode 'row'" in capsys.readouterr().err
