@@ -31,6 +31,83 @@ from dataclasses import dataclass
 import numpy as np
 
 
+# ---------------------------------------------------------------------------
+# float16 <-> float32 casts.  NumPy's are scalar; oracle/csrc/fp16conv.c does the same IEEE
+# conversions (exact widening, round-to-nearest-even narrowing) with F16C over OpenMP threads.
+# Bit-identical either way (tests/test_oracle_cpu.py); the C helper only makes full-depth parity
+# checks at OPT-6.7B width affordable.
+
+_FP16 = None
+
+
+def _fp16lib():
+    global _FP16
+    if _FP16 is None:
+        import ctypes
+        from pathlib import Path
+
+        p = Path(__file__).resolve().parent / "libfp16conv.so"
+        _FP16 = False
+        if p.exists():
+            lib = ctypes.CDLL(str(p))
+            for name in ("oracle_f16_to_f32", "oracle_f32_to_f16"):
+                getattr(lib, name).argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+            lib.oracle_f32_round_f16.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+            vp, lg, i = ctypes.c_void_p, ctypes.c_long, ctypes.c_int
+            lib.oracle_decode_attention.argtypes = [vp, lg, lg, lg, lg, vp, lg, vp, vp, vp, vp, i, i, i,
+                                                    ctypes.c_double, vp]
+            _FP16 = lib
+    return _FP16
+
+
+def widen(a: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+    """float16 array -> float32 (exact), into `out` (C-contiguous, same shape) when given."""
+    lib = _fp16lib()
+    if out is not None and (not lib or a.dtype != np.float16 or out.dtype != np.float32 or
+                            not out.flags.c_contiguous):
+        out[...] = a
+        return out
+    if not lib or a.dtype != np.float16:
+        return np.asarray(a, dtype=np.float32).copy() if a.dtype == np.float32 else a.astype(np.float32)
+    a = np.ascontiguousarray(a)
+    if out is None:
+        out = np.empty(a.shape, dtype=np.float32)
+    elif out.shape != a.shape or out.dtype != np.float32:
+        raise ValueError("widen: out must be float32 of the input's shape")
+    lib.oracle_f16_to_f32(a.ctypes.data, out.ctypes.data, a.size)
+    return out
+
+
+def narrow(a: np.ndarray) -> np.ndarray:
+    """float32 array -> new float16 array (round to nearest even)."""
+    lib = _fp16lib()
+    if not lib or a.dtype != np.float32:
+        return a.astype(np.float16)
+    a = np.ascontiguousarray(a)
+    out = np.empty(a.shape, dtype=np.float16)
+    lib.oracle_f32_to_f16(a.ctypes.data, out.ctypes.data, a.size)
+    return out
+
+
+def round16(a: np.ndarray) -> np.ndarray:
+    """float32 array -> new float32 array holding float(half(a))."""
+    lib = _fp16lib()
+    if not lib or a.dtype != np.float32:
+        return a.astype(np.float16).astype(a.dtype)
+    out = np.array(a, dtype=np.float32, order="C")
+    lib.oracle_f32_round_f16(out.ctypes.data, out.size)
+    return out
+
+
+def _cast(a: np.ndarray, dtype) -> np.ndarray:
+    """a.astype(dtype) through the fast helpers where they apply."""
+    if a.dtype == np.float16 and dtype == np.float32:
+        return widen(a)
+    if a.dtype == np.float32 and dtype == np.float16:
+        return narrow(a)
+    return a.astype(dtype)
+
+
 @dataclass(frozen=True)
 class OPTShape:
     hidden: int
@@ -44,6 +121,12 @@ class OPTShape:
     @property
     def head_dim(self) -> int:
         return self.hidden // self.heads
+
+
+def _mm(x, w):
+    """x[..., k] @ w[n, k]^T as ONE GEMM over the flattened leading dims (a 3-D `x @ w.T` is a stack
+    of small GEMMs in NumPy, ~3x slower at the rebuild's [l, b, h] shape); same per-row arithmetic."""
+    return (x.reshape(-1, x.shape[-1]) @ w.T).reshape(x.shape[:-1] + (w.shape[0],))
 
 
 def _ln(x, g, b, eps):
@@ -78,7 +161,40 @@ class OPTOracle:
         self.len = 0
 
     # -- helpers ------------------------------------------------------------
+    def _fast_attention(self, d) -> bool:
+        """fp16 storage / fp32 compute: attention straight from the fp16 store rows in C (same math as
+        the NumPy branch, double accumulation), which keeps full-depth OPT-6.7B checks affordable."""
+        return bool(_fp16lib()) and self.storage is np.float16 and self.compute is np.float32 and \
+            d % 8 == 0 and d <= 256
+
+    def _attention_c(self, j, q, k, v, lp, seq):
+        b, hd, H, d = self.b, self.s.hidden, self.s.heads, self.s.head_dim
+        lib = _fp16lib()
+        # rebuilt prefix in the GEMM's own layout [pos][b][K|V] (no re-layout copy)
+        kv32 = self._rebuild_rows(j, lp) if lp > 0 else np.zeros((1, b, 2 * hd), dtype=np.float32)
+        tail = self.KV[j][lp:seq - 1]
+        assert tail.flags.c_contiguous and tail.dtype == np.float16
+        q, k, v = (np.ascontiguousarray(t, dtype=np.float32) for t in (q, k, v))
+        out = np.empty((b, hd), dtype=np.float32)
+        scratch = getattr(self, "_scratch", None)
+        if scratch is None or scratch.size < b * H * seq:
+            scratch = self._scratch = np.empty(b * H * (len(self.KV[j]) + 1), dtype=np.float64)
+        lib.oracle_decode_attention(kv32.ctypes.data, lp, b * 2 * hd, 2 * hd, hd, tail.ctypes.data, seq - 1 - lp,
+                                    k.ctypes.data,
+                                    v.ctypes.data, q.ctypes.data, out.ctypes.data, b, H, d, 1.0 / np.sqrt(d),
+                                    scratch.ctypes.data)
+        return out
+
+    def _merge_buffer(self, seq):
+        cap = max(seq, len(self.KV[0]) if self.KV else seq)
+        buf = getattr(self, "_mbuf", None)
+        if buf is None or buf.shape[0] < cap:
+            buf = self._mbuf = np.empty((cap, 2, self.b, self.s.hidden), dtype=self.compute)
+        return buf
+
     def _st(self, a):
+        if self.storage is np.float16 and self.compute is np.float32:
+            return round16(np.asarray(a, dtype=np.float32))
         return a.astype(self.storage).astype(self.compute)
 
     def _kv_store(self, kv):
@@ -94,23 +210,31 @@ class OPTOracle:
 
     def _proj_qkv(self, j, x):
         h = self.s.hidden
-        y = x @ self._lw(j, "wqkv").T + self._lw(j, "bqkv")
+        y = _mm(x, self._lw(j, "wqkv")) + self._lw(j, "bqkv")
         return self._st(y[..., :h]), self._st(y[..., h:2 * h]), self._st(y[..., 2 * h:])
 
     def _rebuild(self, j, upto):
         """K, V for positions [0, upto) from the X store (numerics.py:129-133)."""
         h = self.s.hidden
-        x = self.X[j][:upto]
+        x = _cast(self.X[j][:upto], self.compute)
         wkv = self._lw(j, "wqkv")[h:]
         bkv = self._lw(j, "bqkv")[h:]
-        y = x @ wkv.T + bkv
+        y = _mm(x, wkv) + bkv
         return self._st(y[..., :h]), self._st(y[..., h:])
 
+    def _rebuild_rows(self, j, upto):
+        """_rebuild as one [upto, b, 2h] array (K then V per row), fp16-rounded in place."""
+        h = self.s.hidden
+        y = _mm(_cast(self.X[j][:upto], self.compute), self._lw(j, "wqkv")[h:])
+        y += self._lw(j, "bqkv")[h:]
+        _fp16lib().oracle_f32_round_f16(y.ctypes.data, y.size)
+        return y
+
     def _mlp_tail(self, j, h, attn):
-        h = h + attn @ self._lw(j, "wo").T + self._lw(j, "bo")
+        h = h + _mm(attn, self._lw(j, "wo")) + self._lw(j, "bo")
         y = self._st(_ln(h, self._lw(j, "ln2.g"), self._lw(j, "ln2.b"), self.s.eps))
-        f = self._st(np.maximum(y @ self._lw(j, "w1").T + self._lw(j, "b1"), 0))
-        return h + f @ self._lw(j, "w2").T + self._lw(j, "b2")
+        f = self._st(np.maximum(_mm(y, self._lw(j, "w1")) + self._lw(j, "b1"), 0))
+        return h + _mm(f, self._lw(j, "w2")) + self._lw(j, "b2")
 
     def _logits(self, h):
         z = self._st(_ln(h, self.w["lnf.g"], self.w["lnf.b"], self.s.eps))
@@ -130,8 +254,8 @@ class OPTOracle:
             q, k, v = self._proj_qkv(j, x)
             Xs = np.zeros((capacity, b, hd), dtype=self.storage)
             KVs = np.zeros((capacity, 2, b, hd), dtype=self.storage)
-            Xs[:S0] = x
-            KVs[:S0] = self._kv_store(np.stack([k, v], axis=1).astype(self.storage))
+            Xs[:S0] = _cast(x, self.storage)
+            KVs[:S0] = self._kv_store(_cast(np.stack([k, v], axis=1), self.storage))
             self.X.append(Xs)
             self.KV.append(KVs)
             qh = q.reshape(S0, b, H, d)
@@ -159,17 +283,22 @@ class OPTOracle:
         for j in range(self.s.layers):
             x = self._st(_ln(h, self._lw(j, "ln1.g"), self._lw(j, "ln1.b"), self.s.eps))
             q, k, v = self._proj_qkv(j, x)
-            K = np.empty((seq, b, hd), dtype=self.compute)
-            V = np.empty((seq, b, hd), dtype=self.compute)
-            if lp > 0:
-                K[:lp], V[:lp] = self._rebuild(j, lp)
-            K[lp:seq - 1] = self.KV[j][lp:seq - 1, 0]
-            V[lp:seq - 1] = self.KV[j][lp:seq - 1, 1]
-            K[seq - 1], V[seq - 1] = k, v
-            # store the new position (store_activation / store_cache, graph.py:340-347)
-            if write_stores:
+            if write_stores:  # store the new position (store_activation / store_cache, graph.py:340-347)
                 self.X[j][seq - 1] = x
                 self.KV[j][seq - 1] = self._kv_store(np.stack([k, v])[None].astype(self.storage))[0]
+            if self._fast_attention(d):
+                a = self._st(self._attention_c(j, q, k, v, lp, seq))
+                h = self._mlp_tail(j, h, a)
+                continue
+            # the merged cache [pos][K|V][b][h] in one buffer reused across layers and steps (first-touch
+            # page faults of fresh multi-GB temporaries dominated the oracle's time at full width)
+            buf = self._merge_buffer(seq)
+            if lp > 0:
+                buf[:lp, 0], buf[:lp, 1] = self._rebuild(j, lp)
+            if seq - 1 > lp:
+                widen(self.KV[j][lp:seq - 1], out=buf[lp:seq - 1])
+            buf[seq - 1, 0], buf[seq - 1, 1] = k, v
+            K, V = buf[:seq, 0], buf[:seq, 1]
             lg = np.einsum("sbhd,bhd->bhs", K.reshape(seq, b, H, d), q.reshape(b, H, d)) / np.sqrt(d)
             a = self._st(np.einsum("bhs,sbhd->bhd", _softmax(lg), V.reshape(seq, b, H, d)).reshape(b, hd))
             h = self._mlp_tail(j, h, a)

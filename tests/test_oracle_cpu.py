@@ -146,3 +146,37 @@ def test_opt_oracle_matches_hf_opt(criterion):
     ok = rel <= 1e-4 and all(np.array_equal(np.argmax(b, -1), toks[i]) for i, b in enumerate(hf_logits))
     criterion("O4", f"OPT oracle == transformers OPTForCausalLM (fp32, rel {rel:.1e})", ok)
     assert ok, rel
+
+
+def test_fp16_helpers_bit_identical_to_numpy():
+    """oracle/csrc/fp16conv.c's casts are NumPy's IEEE casts, bit for bit (ties to even, subnormals,
+    overflow to inf, NaN)."""
+    if not opt_ref._fp16lib():
+        pytest.skip("oracle/libfp16conv.so not built (python -m oracle.build)")
+    rng = np.random.default_rng(0)
+    f = np.concatenate([rng.standard_normal(100003).astype(np.float32) * 10.0 ** rng.integers(-9, 6, 100003),
+                        np.array([0.0, -0.0, 65504.0, 65520.0, 1e6, -1e6, np.inf, -np.inf, 5.96e-8, 2.98e-8,
+                                  1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11], dtype=np.float32)]).astype(np.float32)
+    assert np.array_equal(opt_ref.narrow(f).view(np.uint16), f.astype(np.float16).view(np.uint16))
+    assert np.array_equal(opt_ref.round16(f), f.astype(np.float16).astype(np.float32))
+    h = np.arange(65536, dtype=np.uint16).view(np.float16)
+    w = opt_ref.widen(h)
+    ref = h.astype(np.float32)
+    same = (w.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(w) & np.isnan(ref))
+    assert same.all()
+
+
+@pytest.mark.parametrize("splits", [[0, 0, 0], [21, 5, 23]])
+def test_oracle_c_attention_equals_numpy_path(splits, monkeypatch):
+    """The fp16-storage oracle's C attention (double accumulation straight from the fp16 store rows)
+    and its NumPy einsum path agree to fp32 rounding, including a rebuilt prefix."""
+    if not opt_ref._fp16lib():
+        pytest.skip("oracle/libfp16conv.so not built (python -m oracle.build)")
+    cfg, w, shape = _tiny(3)
+    prompt = np.random.default_rng(4).integers(0, cfg.vocab, (3, 20))
+    fast = opt_ref.generate(shape, w.numpy_dict(), prompt, splits)
+    monkeypatch.setattr(opt_ref, "_FP16", False)
+    slow = opt_ref.generate(shape, w.numpy_dict(), prompt, splits)
+    rel = max(float(np.abs(a - b).max() / np.abs(b).max()) for a, b in zip(fast[1], slow[1]))
+    assert rel <= 2e-5, rel
+    assert np.array_equal(fast[0], slow[0])
