@@ -155,7 +155,7 @@ class OPTOracle:
         self.b = batch
         self.storage = storage
         self.compute = compute
-        self.w = {k: np.asarray(v).astype(compute) for k, v in weights.items()}
+        self.w = {k: _cast(np.asarray(v), compute) for k, v in weights.items()}
         self.X: list[np.ndarray] = []   # per layer [S, b, h] storage dtype
         self.KV: list[np.ndarray] = []  # per layer [S, 2, b, h] storage dtype
         self.len = 0
@@ -336,8 +336,10 @@ def generate(shape: OPTShape, weights, prompt: np.ndarray, splits: list[int], st
     else:
         X, KV, first = stores
         cap = S0 + len(splits) + 1
-        o.X = [np.array(X[j][:cap], dtype=storage) for j in range(shape.layers)]
-        o.KV = [np.array(KV[j][:cap], dtype=storage) for j in range(shape.layers)]
+        # read-only views when the dtype matches (the teacher-forced decode never writes them); the caller
+        # keeps the arrays alive (e.g. a runtime's pinned host stores) until generate returns
+        o.X = [np.asarray(X[j][:cap], dtype=storage) for j in range(shape.layers)]
+        o.KV = [np.asarray(KV[j][:cap], dtype=storage) for j in range(shape.layers)]
         o.len = S0
         toks = [np.asarray(first, dtype=np.int64)]
         logits = [None]

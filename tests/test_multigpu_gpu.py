@@ -1,0 +1,154 @@
+"""BASELINE config 3's batch partition as real multi-process decodes (one
+independent process per GPU, no collective on the data path).
+
+2 and 8 ranks share cuda:0 (a gpurun box has one B200; NCCL refuses two ranks on one device, so the
+token gather runs over gloo).  Every rank runs the product path end to end:
+multigpu.partition -> its own KVPRRuntime (own pinned host stores, own plan from the reference solver on
+its slice, multigpu.rank_plan) -> prefill -> decode -> multigpu.gather_tokens.  Ranks decode
+teacher-forced with the unpartitioned run's tokens (one decode call per step, the ids passed in), so
+every step compares logits on identical inputs:
+
+* each rank's logits within 2e-2 relative of the unpartitioned b32 run's rows for its sequences
+  (b <= 8 shards take the CUDA-core projections, a different k order than b32's swap-AB GEMM);
+* the gathered greedy tokens equal the unpartitioned run's on every decided choice, and the oracle's
+  (oracle/opt_ref.py, same forced tokens) on every choice the oracle's margin decides.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import time
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import opt_ref
+from paper_2411_17089_b200 import multigpu
+from paper_2411_17089_b200.costmodel import WorkloadSpec
+from paper_2411_17089_b200.hwprofile import HardwareProfile
+from paper_2411_17089_b200.runtime import KVPRRuntime
+from paper_2411_17089_b200.scheduler import plan_generation
+from paper_2411_17089_b200.weights import OPTConfig, OPTWeights
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 2e-2
+CFG = OPTConfig(hidden=1024, layers=3, heads=16, ffn=4096, vocab=4096, max_pos=256)
+GB, S0, STEPS = 32, 120, 8
+PROF = HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=55e9, transfer_latency=1e-5)
+
+
+def _weights():
+    return OPTWeights.random(CFG, seed=3, device="cuda:0", std=0.1, emb_std=0.1)
+
+
+def _prompt():
+    return torch.randint(0, CFG.vocab, (GB, S0), generator=torch.Generator().manual_seed(4))
+
+
+def _decode_forced(rt, first, splits, forced):
+    """One decode call per step with the given ids (teacher forcing through the public API)."""
+    logits, toks = [], []
+    for i, l in enumerate(splits):
+        inp = first if i == 0 else forced[i].to(rt.dev, torch.int32)
+        t = rt.decode([l], tokens=inp, keep_logits=True)
+        toks.append(t[0].cpu())
+        logits.append(rt.last_logits[0].cpu())
+    torch.cuda.synchronize()
+    return torch.stack(toks), torch.stack(logits)
+
+
+def _worker(rank, world, port, forced, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sl = multigpu.partition(GB, world)[rank]
+        wl = WorkloadSpec(batch_size=GB, prompt_len=S0, gen_len=STEPS)
+        plan = multigpu.rank_plan(CFG.spec(), wl, PROF, world, rank)
+        w = _weights()
+        prompt = _prompt()[sl.start:sl.start + sl.count]
+        rt = KVPRRuntime(w, sl.count, S0 + STEPS + 1)
+        t0 = time.time()
+        first = rt.prefill(prompt)
+        toks, logits = _decode_forced(rt, first, plan.splits, forced[:, sl.start:sl.start + sl.count])
+        t1 = time.time()
+        local = torch.cat([first.cpu()[None], toks]).to(torch.int64)  # [steps + 1, b_local]
+        full = multigpu.gather_tokens(local, GB, device=torch.device("cpu"))
+        slowest = multigpu.max_over_ranks(t1 - t0)
+        rt.close()
+        q.put((rank, sl.start, sl.count, full.numpy(), logits.numpy(), plan.splits, slowest))
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def unpartitioned():
+    """The b32 run on one runtime (free-running), its greedy tokens, logits and the oracle's logits on
+    the same forced tokens."""
+    w = _weights()
+    wl = WorkloadSpec(batch_size=GB, prompt_len=S0, gen_len=STEPS)
+    splits = plan_generation(CFG.spec(), wl, PROF, "column").splits
+    rt = KVPRRuntime(w, GB, S0 + STEPS + 1)
+    first = rt.prefill(_prompt())
+    toks = rt.decode(splits, tokens=first, keep_logits=True)
+    torch.cuda.synchronize()
+    g = torch.cat([first.cpu()[None], toks.cpu()]).to(torch.int64)  # [steps + 1, GB]
+    gl = rt.last_logits.cpu().numpy()
+    rt.close()
+    shape = opt_ref.OPTShape(CFG.hidden, CFG.layers, CFG.heads, CFG.ffn, CFG.vocab, CFG.max_pos, CFG.eps)
+    o_t, o_l, o_m = opt_ref.generate(shape, w.numpy_dict(), _prompt().numpy(), splits, forced=g.numpy())
+    return g, gl, np.stack(o_l[1:]), np.stack(o_m[1:])
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_batch_partition_ranks_match_unpartitioned(criterion, unpartitioned, world):
+    g, gl, o_l, o_m = unpartitioned
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, g, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    worst, abs_err, worst_o = 0.0, 0.0, 0.0
+    logits = np.zeros_like(gl)
+    for rank, start, count, full, lg, splits, _ in res:
+        logits[:, start:start + count] = lg
+        ref = gl[:, start:start + count]
+        abs_err = max(abs_err, float(np.abs(lg - ref).max()))
+        for i in range(STEPS):
+            for k in range(count):
+                worst = max(worst, float(np.abs(lg[i, k] - ref[i, k]).max() / np.abs(ref[i, k]).max()))
+                orow = o_l[i, start + k]
+                worst_o = max(worst_o, float(np.abs(lg[i, k] - orow).max() / np.abs(orow).max()))
+    gathered = res[0][3]
+    assert all(np.array_equal(r[3], gathered) for r in res), "ranks gathered different token tables"
+    # greedy: gathered decode tokens vs the unpartitioned run's (decided by its own margin) and the oracle's
+    part = np.partition(gl, -2, axis=-1)
+    m_gpu = part[..., -1] - part[..., -2]
+    bad = [(i, k) for i in range(STEPS) for k in range(GB)
+           if m_gpu[i, k] > 2 * abs_err and gathered[i + 1, k] != g[i + 1, k]]
+    o_tok = o_l.argmax(-1)
+    bad_o = [(i, k) for i in range(STEPS) for k in range(GB)
+             if o_m[i, k] > 2 * abs_err and gathered[i + 1, k] != o_tok[i, k]]
+    assert np.array_equal(gathered[0], g[0].numpy()), "prefill tokens differ"
+    ok = worst <= LOGIT_RTOL and worst_o <= LOGIT_RTOL and not bad and not bad_o
+    criterion(f"M{world}", f"batch partition over {world} processes (b{GB // world} per rank, own stores/plan, "
+                           f"gloo gather): logits rel err {worst:.2e} vs the unpartitioned b{GB} run, {worst_o:.2e} "
+                           f"vs the oracle; gathered greedy tokens equal on every decided choice", ok)
+    assert worst <= LOGIT_RTOL and worst_o <= LOGIT_RTOL, (worst, worst_o)
+    assert not bad and not bad_o, (bad, bad_o)

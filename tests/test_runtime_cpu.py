@@ -61,24 +61,56 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _tiny_decoder():
+    import numpy as np
+
+    from oracle import opt_ref
+    from paper_2411_17089_b200.weights import OPTConfig, OPTWeights
+
+    cfg = OPTConfig(hidden=64, layers=2, heads=4, ffn=256, vocab=97, max_pos=64)
+    w = OPTWeights.random(cfg, seed=5, device="cpu", std=0.1, emb_std=0.1).numpy_dict()
+    shape = opt_ref.OPTShape(cfg.hidden, cfg.layers, cfg.heads, cfg.ffn, cfg.vocab, cfg.max_pos, cfg.eps)
+    return cfg, w, shape, np.random.default_rng(6)
+
+
 def _worker(rank, world, port, global_batch, q):
+    """One rank of the batch partition: partition -> its own plan (reference solver on its slice) -> its
+    own decoder replica over its sequences -> gather_tokens.  The replica is the CPU OPT decoder with host
+    stores and the split-merge rebuild (oracle/opt_ref.py, fp64): the GPU runtime needs a device
+    (tests/test_multigpu_gpu.py runs the same flow with KVPRRuntime on the B200)."""
+    import numpy as np
+
+    from oracle import opt_ref
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        cfg, w, shape, rng = _tiny_decoder()
+        prompt = rng.integers(0, cfg.vocab, (global_batch, 12))
         sl = multigpu.partition(global_batch, world)[rank]
-        steps = 3
-        # stand-in for this rank's replica output: token = 1000*step + global sequence id
-        local = torch.tensor([[1000 * i + sl.start + k for k in range(sl.count)] for i in range(steps)])
-        full = multigpu.gather_tokens(local, global_batch)
+        wl = WorkloadSpec(batch_size=global_batch, prompt_len=12, gen_len=5)
+        plan = multigpu.rank_plan(cfg.spec(), wl, PROF, world, rank)
+        toks, logits, _ = opt_ref.generate(shape, w, prompt[sl.start:sl.start + sl.count], plan.splits,
+                                           storage=np.float64, compute=np.float64)
+        full = multigpu.gather_tokens(torch.from_numpy(toks), global_batch)
         t = multigpu.max_over_ranks(float(rank + 1))
-        q.put((rank, full.tolist(), t))
+        q.put((rank, full.tolist(), np.stack(logits).tolist(), t))
     finally:
         dist.destroy_process_group()
 
 
+PROF = HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=55e9, transfer_latency=1e-5)
+
+
 @pytest.mark.parametrize("global_batch", [8, 7])
-def test_partitioned_gather_over_gloo(global_batch):
+def test_partitioned_decode_over_gloo(global_batch):
+    """world 2 over gloo: the gathered tokens of the per-rank decoders equal the unpartitioned decode, and
+    each rank's logits its rows of it (sequences are independent units)."""
+    import numpy as np
+
+    from oracle import opt_ref
+
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -90,10 +122,17 @@ def test_partitioned_gather_over_gloo(global_batch):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    want = [[1000 * i + k for k in range(global_batch)] for i in range(3)]
-    for rank, full, t in res:
-        assert full == want
+    cfg, w, shape, rng = _tiny_decoder()
+    prompt = rng.integers(0, cfg.vocab, (global_batch, 12))
+    wl = WorkloadSpec(batch_size=global_batch, prompt_len=12, gen_len=5)
+    splits = multigpu.rank_plan(cfg.spec(), wl, PROF, 1, 0).splits
+    toks, logits, _ = opt_ref.generate(shape, w, prompt, splits, storage=np.float64, compute=np.float64)
+    logits = np.stack(logits)
+    for rank, full, lg, t in res:
+        assert full == toks.tolist()
         assert t == float(world)
+        sl = multigpu.partition(global_batch, world)[rank]
+        assert np.abs(np.array(lg) - logits[:, sl.start:sl.start + sl.count]).max() <= 1e-9
 
 
 @pytest.mark.parametrize("h,f", [(4096, 16384), (768, 3072), (64, 256)])

@@ -41,38 +41,6 @@ def _oracle_shape(cfg):
     return opt_ref.OPTShape(cfg.hidden, cfg.layers, cfg.heads, cfg.ffn, cfg.vocab, cfg.max_pos, cfg.eps)
 
 
-def test_config1_greedy_parity_32_steps(criterion):
-    """Config 1 geometry (OPT-125M shape), b4, prompt 256, 32 free-running greedy steps at the solver's plan.
-
-    fp16 storage vs the oracle's fp32 arithmetic leaves a ~3.5e-3 relative logit
-    error; 128 greedy decisions routinely include a top-1/top-2 margin below
-    that, so free-running identity depends on the draw (seeds 6, 7, 11, 13 of
-    4..13 hold for all 32 steps, profiles/r01_parity_seed_scan.jsonl).  This
-    test pins seed 13 (min oracle margin 0.013); the seed-independent decode
-    check is test_decode_path_parity_teacher_forced below.
-    """
-    cfg = OPTConfig(hidden=768, layers=12, heads=12, ffn=3072)
-    batch, S0, steps = 4, 256, 32
-    w, prompt = _setup(cfg, batch, S0, seed=13)
-    wl = WorkloadSpec(batch_size=batch, prompt_len=S0, gen_len=steps)
-    plan = plan_generation(cfg.spec(), wl, B200_GUESS, "column")
-    splits = plan.splits
-    assert 0 < splits[0] < S0 + 1
-    toks, rt = generate(w, prompt, splits, keep_logits=True)
-    gpu_logits = rt.last_logits.float().cpu().numpy()
-    rt.close()
-    o_toks, o_logits, o_marg = opt_ref.generate(_oracle_shape(cfg), w.numpy_dict(), prompt.numpy(), splits)
-    errs = [float(np.abs(gpu_logits[i] - o_logits[i + 1]).max() / np.abs(o_logits[i + 1]).max())
-            for i in range(steps)]
-    same = bool((toks.numpy() == o_toks).all())
-    min_margin = float(min(m.min() for m in o_marg))
-    ok = max(errs) <= LOGIT_RTOL and same
-    criterion("G1", f"config-1 decode, seed 13: 32 greedy steps x 4 seqs identical to the oracle, logits rel err "
-                    f"{max(errs):.2e} <= 2e-2 (min oracle top1-top2 margin {min_margin:.4f})", ok)
-    assert same, f"greedy tokens differ: gpu {toks.numpy().T} vs oracle {o_toks.T}"
-    assert max(errs) <= LOGIT_RTOL, errs
-
-
 def test_decode_path_parity_teacher_forced(criterion):
     """Seed-independent decode-path parity: the oracle decodes from the GPU's own prefill stores and
     the GPU's token sequence, so every step compares logits on identical inputs.  Logits within 2e-2
