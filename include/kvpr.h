@@ -140,6 +140,15 @@ int kvpr_layernorm_linear_ws(const float* x, long long ldx, const void* gamma, c
 int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* ws, size_t ws_bytes, int batch,
                           int heads, int head_dim, int seq_len, float scale, void* stream);
 
+/* K2 over a ragged batch: the reference keeps one KVState per sequence with its own length
+ * (numerics.py:43-72).  Sequence b attends over positions [0, seq_lens[b]) of the same page
+ * layout, padded to max_seq_len positions; seq_lens is a DEVICE int32[batch] with every entry in
+ * [1, max_seq_len] (positions past a sequence's end are never read).  Same arithmetic as
+ * kvpr_decode_attention when every length equals max_seq_len. */
+int kvpr_decode_attention_ragged(const void* q, const void* kv_pages, const int* seq_lens, void* out, void* ws,
+                                 size_t ws_bytes, int batch, int heads, int head_dim, int max_seq_len, float scale,
+                                 void* stream);
+
 /* Causal attention for the prompt (prefill that populates the host stores):
  * q/out [pos][batch][hidden], kv pages as above, positions [0, seq_len). */
 int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,

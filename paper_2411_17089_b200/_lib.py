@@ -36,6 +36,7 @@ EXPORTS = (
     "kvpr_linear_ws",
     "kvpr_layernorm_linear_ws",
     "kvpr_decode_attention",
+    "kvpr_decode_attention_ragged",
     "kvpr_prefill_attention",
     "kvpr_layernorm",
     "kvpr_embed",
@@ -124,6 +125,7 @@ _SIGS = {
     "kvpr_layernorm_linear_ws": ([_vp, _ll, _vp, _vp, _f, _vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i,
                                   _vp, _sz, _vp], _i),
     "kvpr_decode_attention": ([_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
+    "kvpr_decode_attention_ragged": ([_vp, _vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
     "kvpr_prefill_attention": ([_vp, _vp, _vp, _i, _i, _i, _i, _f, _vp], _i),
     "kvpr_layernorm": ([_vp, _ll, _vp, _vp, _vp, _ll, _i, _i, _f, _vp], _i),
     "kvpr_embed": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp], _i),

@@ -28,6 +28,7 @@ from dataclasses import dataclass
 
 from .costmodel import ModelSpec, WorkloadSpec, opt_preset
 from .hwprofile import HardwareProfile, calibrate, profile_to_json, read_measurements_csv
+from .pipesim import GpuMemoryBudgetError  # the reference's class (graph.py:70), raised by the residency check
 from .scheduler import SplitPlan, constant_plan, import_plan, plan_generation, plan_to_json
 
 log = logging.getLogger("paper_2411_17089_b200")
@@ -37,10 +38,6 @@ EXIT_OK, EXIT_INVALID, EXIT_BUDGET, EXIT_VALIDATION = 0, 1, 2, 3
 
 class ConfigError(ValueError):
     """Configuration file or flag value is invalid."""
-
-
-class GpuMemoryBudgetError(RuntimeError):
-    """Device residency of the run exceeds the configured budget."""
 
 
 class _Parser(argparse.ArgumentParser):
@@ -230,6 +227,11 @@ def cmd_run(a) -> int:
              f"gpu_utilization={rep['gpu_util']!r}", f"peak_gpu_bytes={need!r}",
              f"splits={','.join(str(x) for x in plan.splits)}"]
     lines += [f"busy_{k}={v!r}" for k, v in sorted(rep["breakdown"].items())]
+    # the reference's prediction for the same plan and profile (pipesim restatement), §8f rank 2
+    cmp = tr.compare_with_model(ents, s.spec, s.wl, s.profile, plan, s.schedule)
+    lines += [f"simulated_makespan_s={cmp['makespan']['simulated_s']!r}",
+              f"measured_over_simulated={cmp['makespan']['measured_over_simulated']!r}",
+              f"replay_over_measured={cmp['makespan']['replay_over_measured']!r}"]
     sys.stdout.write("\n".join(lines) + "\n")
     return EXIT_OK
 

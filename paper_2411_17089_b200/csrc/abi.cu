@@ -241,6 +241,19 @@ int kvpr_decode_attention(const void* q, const void* kv_pages, void* out, void* 
                           seq_len, scale, static_cast<cudaStream_t>(stream));
 }
 
+int kvpr_decode_attention_ragged(const void* q, const void* kv_pages, const int* seq_lens, void* out, void* ws,
+                                 size_t ws_bytes, int batch, int heads, int head_dim, int max_seq_len, float scale,
+                                 void* stream) {
+  g_err[0] = 0;
+  if (seq_lens == nullptr) {
+    set_error("decode_attention_ragged: seq_lens is NULL (use kvpr_decode_attention for a uniform batch)");
+    return KVPR_EINVAL;
+  }
+  return decode_attention(static_cast<const __half*>(q), static_cast<const __half*>(kv_pages),
+                          static_cast<__half*>(out), static_cast<float*>(ws), ws_bytes, batch, heads, head_dim,
+                          max_seq_len, scale, static_cast<cudaStream_t>(stream), seq_lens);
+}
+
 int kvpr_decode_attention_kv4(const void* q, const void* kv_pages, const void* qpages, int q_lo, int q_hi, void* out,
                               void* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
                               void* stream) {

@@ -204,7 +204,8 @@ constexpr int kMaxClusterSplits = 8;  // portable cluster size
 template <int D, bool Q4, bool CL>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
                                                           __half* __restrict__ out, float* __restrict__ ws, int batch,
-                                                          int heads, int seq_len, int chunk, float qscale, Q4Src q4) {
+                                                          int heads, int seq_len, int chunk, float qscale, Q4Src q4,
+                                                          const int* __restrict__ seq_lens) {
   constexpr int LPP = D / 8;
   constexpr int PPW = 32 / LPP;  // positions per warp step
   constexpr int NW = 4;
@@ -220,8 +221,11 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const __half* __restri
   const int hd = bh % heads;
   const int hidden = heads * D;
   const int split = blockIdx.y;
+  // ragged batches (seq_lens != nullptr): sequence b attends over its own [0, seq_lens[b]) of the
+  // padded slab; a split past its end contributes an empty state (m = -inf), dropped by the merge
+  const int len_b = seq_lens != nullptr ? min(seq_len, __ldg(seq_lens + b)) : seq_len;
   const int p_lo = split * chunk;
-  const int p_hi = min(seq_len, p_lo + chunk);
+  const int p_hi = min(len_b, p_lo + chunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int glane = lane % LPP, grp = lane / LPP;
 
@@ -394,13 +398,14 @@ int launch_cluster(void (*kern)(KArgs...), dim3 grid, int splits, cudaStream_t s
 }  // namespace
 
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch, int heads,
-                     int head_dim, int seq_len, float scale, cudaStream_t stream) {
-  return decode_attention_q4(q, kv, nullptr, 0, 0, out, ws, ws_bytes, batch, heads, head_dim, seq_len, scale, stream);
+                     int head_dim, int seq_len, float scale, cudaStream_t stream, const int* seq_lens) {
+  return decode_attention_q4(q, kv, nullptr, 0, 0, out, ws, ws_bytes, batch, heads, head_dim, seq_len, scale, stream,
+                             seq_lens);
 }
 
 int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages, int q_lo, int q_hi, __half* out,
                         float* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const int* seq_lens) {
   const bool use_q4 = q_hi > q_lo;
   if (use_q4 && (qpages == nullptr || q_lo < 0 || q_hi > seq_len || (heads * head_dim) % 64 != 0 ||
                  (reinterpret_cast<uintptr_t>(qpages) & 3))) {
@@ -466,29 +471,29 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
   if (splits > 1 && splits <= kMaxClusterSplits && cluster_merge) {  // merge in DSMEM: one launch
     if (head_dim == 128)
       return use_q4 ? launch_cluster(decode_attn_kernel<128, true, true>, grid, splits, stream, q, kv, out, ws, batch,
-                                     heads, seq_len, chunk, qscale, q4)
+                                     heads, seq_len, chunk, qscale, q4, seq_lens)
                     : launch_cluster(decode_attn_kernel<128, false, true>, grid, splits, stream, q, kv, out, ws, batch,
-                                     heads, seq_len, chunk, qscale, q4);
+                                     heads, seq_len, chunk, qscale, q4, seq_lens);
     return use_q4 ? launch_cluster(decode_attn_kernel<64, true, true>, grid, splits, stream, q, kv, out, ws, batch,
-                                   heads, seq_len, chunk, qscale, q4)
+                                   heads, seq_len, chunk, qscale, q4, seq_lens)
                   : launch_cluster(decode_attn_kernel<64, false, true>, grid, splits, stream, q, kv, out, ws, batch,
-                                   heads, seq_len, chunk, qscale, q4);
+                                   heads, seq_len, chunk, qscale, q4, seq_lens);
   }
   int rc;
   if (head_dim == 128) {
     if (use_q4)
       rc = launch("decode_attention", decode_attn_kernel<128, true, false>, grid, 128, 0, stream, q, kv, out, ws,
-                  batch, heads, seq_len, chunk, qscale, q4);
+                  batch, heads, seq_len, chunk, qscale, q4, seq_lens);
     else
       rc = launch("decode_attention", decode_attn_kernel<128, false, false>, grid, 128, 0, stream, q, kv, out, ws,
-                  batch, heads, seq_len, chunk, qscale, q4);
+                  batch, heads, seq_len, chunk, qscale, q4, seq_lens);
   } else {
     if (use_q4)
       rc = launch("decode_attention", decode_attn_kernel<64, true, false>, grid, 128, 0, stream, q, kv, out, ws,
-                  batch, heads, seq_len, chunk, qscale, q4);
+                  batch, heads, seq_len, chunk, qscale, q4, seq_lens);
     else
       rc = launch("decode_attention", decode_attn_kernel<64, false, false>, grid, 128, 0, stream, q, kv, out, ws,
-                  batch, heads, seq_len, chunk, qscale, q4);
+                  batch, heads, seq_len, chunk, qscale, q4, seq_lens);
   }
   if (rc || splits == 1) return rc;
   if (head_dim == 128)

@@ -71,12 +71,14 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
 int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                      const GemmArgs& tp, cudaStream_t stream);
 
+// seq_lens (device int32[batch], optional): ragged batch, sequence b attends over [0, seq_lens[b])
 int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, size_t ws_bytes, int batch,
-                     int heads, int head_dim, int seq_len, float scale, cudaStream_t stream);
+                     int heads, int head_dim, int seq_len, float scale, cudaStream_t stream,
+                     const int* seq_lens = nullptr);
 
 int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages, int q_lo, int q_hi, __half* out,
                         float* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const int* seq_lens = nullptr);
 
 int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim,
                       int seq_len, float scale, cudaStream_t stream);

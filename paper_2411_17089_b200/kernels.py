@@ -96,6 +96,26 @@ def decode_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor,
     return out
 
 
+def decode_attention_ragged(q: torch.Tensor, kv_pages: torch.Tensor, seq_lens: torch.Tensor, out: torch.Tensor,
+                            ws: torch.Tensor | None, heads: int, head_dim: int, scale: float | None = None,
+                            stream=None) -> torch.Tensor:
+    """K2 over a ragged batch: sequence b attends over pages [0, seq_lens[b]) (device int32 [batch],
+    1 <= seq_lens[b] <= kv_pages.shape[0]); kv_pages [max_len][2][batch][hidden]."""
+    _need(q, torch.float16, "q")
+    _need(kv_pages, torch.float16, "kv_pages")
+    _need(seq_lens, torch.int32, "seq_lens")
+    _need(out, torch.float16, "out")
+    batch = q.shape[0]
+    if seq_lens.numel() != batch:
+        raise ValueError(f"seq_lens has {seq_lens.numel()} entries for a batch of {batch}")
+    if scale is None:
+        scale = 1.0 / math.sqrt(head_dim)
+    ws_ptr, ws_bytes = (ws.data_ptr(), ws.numel() * ws.element_size()) if ws is not None else (None, 0)
+    _lib.call("kvpr_decode_attention_ragged", q.data_ptr(), kv_pages.data_ptr(), seq_lens.data_ptr(), out.data_ptr(),
+              ws_ptr, ws_bytes, batch, heads, head_dim, int(kv_pages.shape[0]), float(scale), _stream(stream))
+    return out
+
+
 def decode_attention_kv4(q: torch.Tensor, kv_pages: torch.Tensor, qpages: torch.Tensor, q_lo: int, q_hi: int,
                          out: torch.Tensor, ws: torch.Tensor | None, batch: int, heads: int, head_dim: int,
                          seq_len: int, scale: float | None = None, stream=None) -> torch.Tensor:

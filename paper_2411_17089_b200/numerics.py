@@ -10,7 +10,12 @@ tolerance (2e-2 relative), not 1e-12; arrays come back as float64 NumPy to
 keep the reference's types.  Validation (ValueError conditions and messages)
 follows numerics.py:22-32, 121-126, 172-182.  The reference matrices are
 [in, out] (``x @ w_k``); the kernels take the torch [out, in] layout, so
-weights are transposed on upload.
+weights are transposed on upload.  Any head_dim up to 128 works (K2 reads
+64- or 128-wide heads; narrower ones are zero-padded per head, which leaves
+K q and the kept output lanes unchanged), so the reference's randomized
+validate harness (cli.py:343-377, head_dim 1..4) runs through this module.
+``decode_attention_batch`` attends several per-sequence caches of different
+lengths in one ragged K2 launch (kvpr_decode_attention_ragged).
 """
 
 from __future__ import annotations
@@ -160,30 +165,76 @@ def stable_softmax(logits) -> np.ndarray:
     return (e / e.sum()).cpu().numpy()
 
 
-def decode_attention(q_token, kv: KVState, w_o) -> np.ndarray:
-    """K2 split-KV attention over the cache, then W_O (numerics.py:166-191)."""
-    if not kv.seq_len:
-        raise ValueError("cannot attend over an empty cache")
-    q, h, d = np.asarray(q_token, dtype=np.float64), kv.num_heads * kv.head_dim, kv.head_dim
+def _check_query(q, h) -> np.ndarray:
+    q = np.asarray(q, dtype=np.float64)
     if q.ndim != 1:
         raise ValueError("q_token must be a 1-D row of length h")
     if q.size != h:
         raise ValueError(f"q_token has length {q.size}, expected {h}")
     if not np.all(np.isfinite(q)):
         raise ValueError("q_token contains non-finite entries")
-    w_o = _mat("w_o", w_o, h, h)
-    if d not in (64, 128):
-        raise ValueError(f"head_dim {d} unsupported by the decode-attention kernel (64 or 128)")
+    return q
+
+
+def _attend(qs: list[np.ndarray], kvs: list[KVState], w_o: np.ndarray) -> np.ndarray:
+    """K2 over one or more per-sequence caches (ragged lengths), then W_O, on the device.
+
+    K2 reads whole 16-byte rows of a 64- or 128-wide head; any other head_dim <= 128 is zero-padded
+    per head (zero query and key lanes add nothing to K q, zero value lanes produce output lanes that
+    are dropped), with the softmax scale of the real head_dim, 1/sqrt(d) (numerics.py:184)."""
+    heads, d = kvs[0].num_heads, kvs[0].head_dim
+    if d > 128:
+        raise ValueError(f"head_dim {d} unsupported by the decode-attention kernel (at most 128)")
+    n, h, dp = len(kvs), heads * d, (64 if d <= 64 else 128)
     dev = _dev()
-    s = kv.seq_len
-    pages = torch.empty(s, 2, 1, h, dtype=torch.float16, device=dev)
-    pages[:, 0, 0] = torch.from_numpy(kv.keys.transpose(1, 0, 2).reshape(s, h)).to(dev, torch.float16)
-    pages[:, 1, 0] = torch.from_numpy(kv.values.transpose(1, 0, 2).reshape(s, h)).to(dev, torch.float16)
-    qd = torch.from_numpy(q).to(dev, torch.float16).view(1, h)
-    att = torch.empty(1, h, dtype=torch.float16, device=dev)
-    ws = torch.empty(1 << 20, dtype=torch.uint8, device=dev)
-    kernels.decode_attention(qd, pages, att, ws, 1, kv.num_heads, d, s, scale=1.0 / math.sqrt(d))
-    wo = torch.from_numpy(w_o.T.copy()).to(dev, torch.float16)  # [out, in]
-    out = torch.empty(1, h, dtype=torch.float32, device=dev)
-    kernels.linear_simple(att, wo, None, out)
-    return out[0].double().cpu().numpy()
+    smax = max(kv.seq_len for kv in kvs)
+    pages = torch.zeros(smax, 2, n, heads, dp, dtype=torch.float16, device=dev)
+    qd = torch.zeros(n, heads, dp, dtype=torch.float16, device=dev)
+    for i, (q, kv) in enumerate(zip(qs, kvs)):
+        s = kv.seq_len
+        pages[:s, 0, i, :, :d] = torch.from_numpy(kv.keys.transpose(1, 0, 2)).to(dev, torch.float16)
+        pages[:s, 1, i, :, :d] = torch.from_numpy(kv.values.transpose(1, 0, 2)).to(dev, torch.float16)
+        qd[i, :, :d] = torch.from_numpy(q.reshape(heads, d)).to(dev, torch.float16)
+    att = torch.empty(n, heads * dp, dtype=torch.float16, device=dev)
+    ws = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)
+    scale = 1.0 / math.sqrt(d)
+    if n == 1:
+        kernels.decode_attention(qd.view(1, -1), pages.view(smax, 2, 1, -1), att, ws, 1, heads, dp, smax, scale=scale)
+    else:
+        lens = torch.tensor([kv.seq_len for kv in kvs], dtype=torch.int32, device=dev)
+        kernels.decode_attention_ragged(qd.view(n, -1), pages.view(smax, 2, n, -1), lens, att, ws, heads, dp,
+                                        scale=scale)
+    hp = _pad_to(h, 64)  # W_O GEMM: K % 8, N % 32 -> zero-padded hidden
+    a = torch.zeros(n, hp, dtype=torch.float16, device=dev)
+    a[:, :h] = att.view(n, heads, dp)[:, :, :d].reshape(n, h)
+    wo = torch.zeros(hp, hp, dtype=torch.float16, device=dev)
+    wo[:h, :h] = torch.from_numpy(w_o.T.copy()).to(dev, torch.float16)  # [out, in]
+    out = torch.empty(n, hp, dtype=torch.float32, device=dev)
+    kernels.linear_simple(a, wo, None, out)
+    return out[:, :h].double().cpu().numpy()
+
+
+def decode_attention(q_token, kv: KVState, w_o) -> np.ndarray:
+    """K2 split-KV attention over the cache, then W_O (numerics.py:166-191)."""
+    if not kv.seq_len:
+        raise ValueError("cannot attend over an empty cache")
+    h = kv.num_heads * kv.head_dim
+    q = _check_query(q_token, h)
+    return _attend([q], [kv], _mat("w_o", w_o, h, h))[0]
+
+
+def decode_attention_batch(q_tokens, kvs: list[KVState], w_o) -> np.ndarray:
+    """decode_attention for several sequences with their own caches (ragged lengths, the reference's
+    per-sequence KVState) in ONE K2 launch: row i = decode_attention(q_tokens[i], kvs[i], w_o)."""
+    if not kvs:
+        raise ValueError("need at least one sequence")
+    heads, d = kvs[0].num_heads, kvs[0].head_dim
+    if any((kv.num_heads, kv.head_dim) != (heads, d) for kv in kvs):
+        raise ValueError("all caches must share num_heads and head_dim")
+    if any(not kv.seq_len for kv in kvs):
+        raise ValueError("cannot attend over an empty cache")
+    qs = np.asarray(q_tokens, dtype=np.float64)
+    if qs.ndim != 2 or qs.shape[0] != len(kvs):
+        raise ValueError(f"q_tokens must be ({len(kvs)}, h)")
+    h = heads * d
+    return _attend([_check_query(q, h) for q in qs], kvs, _mat("w_o", w_o, h, h))

@@ -199,3 +199,68 @@ def check_invariants(entries: list[Entry], layers: int, tol: float = 2e-6) -> li
             if d and es[0].start < max(d) - tol:
                 bad.append(f"{es[0].name} starts before store_cache i{i - 1} j{j} finished")
     return bad
+
+
+# ---------------------------------------------------------------------------
+# measured vs simulated
+
+def _med(xs):
+    xs = sorted(xs)
+    return xs[len(xs) // 2] if xs else 0.0
+
+
+def compare_with_model(entries: list[Entry], spec, wl, profile, plan, schedule: str = "column") -> dict:
+    """Lay a measured decode next to the reference's prediction for the same plan and profile.
+
+    The reference predicts a run by list-scheduling its task DAG (pipesim.build_task_graph +
+    simulate, graph.py:176-355, engine.py:140-204) with durations from the profile.  Returned:
+
+    * ``kinds``: per task kind, total measured busy time vs the simulated total (ratio = measured /
+      simulated).  Transfers and the recompute are what the profile models (calibrated bandwidths,
+      the profiled K1 rate); the reference prices MHA / FFN at the GEMM FLOP rate, which a decode
+      step (HBM-bound) does not run at, so those ratios are reported, not expected to be 1;
+    * ``makespan``: measured vs simulated, and vs a *replay*: the same DAG and scheduler fed the
+      measured per-task durations.  replay / measured >= 1 means the runtime realised at least the
+      overlap the DAG allows (it pipelines X chunks under K1, which the DAG's recompute-after-all-of-X
+      edge does not);
+    * ``layer``: steady-state per-layer time (median spacing of consecutive FFN ends) both ways.
+    The DAG's token-activation loads (column mode's per-unit X row, graph.py:295-304) are modeled but
+    not executed: the runtime keeps the residual stream in HBM, so they replay as zero.
+    """
+    from . import pipesim as ps
+
+    pol = ps.Policy(schedule, True)
+    graph = ps.build_task_graph(spec, wl, profile, plan, pol)
+    tl, rep = ps.simulate(graph, profile)
+    sim_dur = ps.task_durations(graph, profile)
+    meas: dict[tuple[str, int, int], float] = {}
+    for e in entries:
+        key = (e.kind, e.step, e.layer)
+        meas[key] = meas.get(key, 0.0) + (e.end - e.start)
+    kinds: dict[str, dict] = {}
+    replay = []
+    for t in graph.tasks:
+        k = t.kind.value
+        m = meas.get((k, t.step, t.layer), 0.0)
+        replay.append(m)
+        d = kinds.setdefault(k, {"measured_s": 0.0, "simulated_s": 0.0, "tasks": 0})
+        d["measured_s"] += m
+        d["simulated_s"] += sim_dur[t.id]
+        d["tasks"] += 1
+    for d in kinds.values():
+        d["ratio"] = d["measured_s"] / d["simulated_s"] if d["simulated_s"] > 0 else None
+    _, rep_replay = ps.simulate(graph, profile, durations=replay)
+    m_span = max(e.end for e in entries) - min(e.start for e in entries)
+    m_ffn = sorted(e.end for e in entries if e.kind == "compute_ffn")
+    s_ffn = sorted(tl.entries[t.id].end for t in graph.tasks if t.kind is ps.TaskKind.COMPUTE_FFN)
+    m_layer = _med([b - a for a, b in zip(m_ffn, m_ffn[1:])])
+    s_layer = _med([b - a for a, b in zip(s_ffn, s_ffn[1:])])
+    return {
+        "kinds": kinds,
+        "makespan": {"measured_s": m_span, "simulated_s": rep.makespan, "replay_s": rep_replay.makespan,
+                     "measured_over_simulated": m_span / rep.makespan if rep.makespan > 0 else None,
+                     "replay_over_measured": rep_replay.makespan / m_span if m_span > 0 else None},
+        "layer": {"measured_s": m_layer, "simulated_s": s_layer,
+                  "measured_over_simulated": m_layer / s_layer if s_layer > 0 else None},
+        "simulated_report": {"decode_throughput": rep.decode_throughput, "gpu_utilization": rep.gpu_utilization},
+    }

@@ -10,6 +10,10 @@ Writes
                          test_acceptance.py:73-108 (seed 20260816), the BASELINE
                          configs under the paper and B200-guess profiles
                          (SURVEY.md Appendix A), plus calibrate() fits.
+  pipesim_golden.json    kvoverlap.pipesim timelines (every task's start / end) and
+                         reports for row / column, recompute on / off, resident /
+                         streamed (coarse, fine) weights, 1-3 GPU batches, with and
+                         without transfer latency (pins paper_2411_17089_b200.pipesim).
   numerics_golden.npz    fp64 split_merge_kv / decode_attention / append_token_kv
                          outputs of kvoverlap.numerics on seeded small cases
                          (pins oracle/numerics_ref.py).
@@ -137,10 +141,6 @@ def scheduler_cases():
 
     # calibrate(): the shipped sample CSV (values inlined) and a synthetic noisy set
     sample = SAMPLE
-    _unused = [("h2d", 16777216, 0.000503), ("h2d", 67108864, 0.001967), ("h2d", 268435456, 0.007826),
-              ("h2d", 1073741824, 0.031262), ("d2h", 16777216, 0.000524), ("d2h", 67108864, 0.002041),
-              ("d2h", 268435456, 0.008103), ("d2h", 1073741824, 0.032391), ("gemm", 1099511627776, 0.004405),
-              ("gemm", 4398046511104, 0.017612), ("gemm", 17592186044416, 0.070442)]
     rng = np.random.default_rng(5)
     synth = []
     for kind, rate, lat in (("h2d", 53e9, 8e-6), ("d2h", 55e9, 9e-6), ("gemm", 1.3e15, 2e-5)):
@@ -151,6 +151,50 @@ def scheduler_cases():
         res = rh.calibrate(ms)
         out["calibrate"].append({"name": name, "records": [list(r) for r in recs], "profile": res.profile.to_dict(),
                                  "residual_rms": res.residual_rms})
+    return out
+
+
+def pipesim_cases():
+    """Simulated timelines of the live reference for a grid of policies / workloads / profiles."""
+    from kvoverlap.pipesim import Policy, build_task_graph, simulate
+
+    out = []
+    rng = np.random.default_rng(17)
+    profiles = [rh.HardwareProfile(gpu_flops=312e12, h2d_bandwidth=32 * GIB, d2h_bandwidth=32 * GIB),
+                rh.HardwareProfile(gpu_flops=1391.2e12, h2d_bandwidth=55e9, d2h_bandwidth=51e9,
+                                   transfer_latency=1e-6),
+                rh.HardwareProfile(gpu_flops=2e13, h2d_bandwidth=8 * GIB, d2h_bandwidth=8 * GIB,
+                                   transfer_latency=1e-4, gpu_efficiency=0.8)]
+    for n in range(48):
+        h = int(rng.choice([256, 1024, 4096]))
+        sp = rc.ModelSpec(hidden_dim=h, num_layers=int(rng.integers(1, 4)), num_heads=8, ffn_dim=4 * h)
+        wl = rc.WorkloadSpec(batch_size=int(rng.integers(1, 33)), prompt_len=int(rng.integers(4, 300)),
+                             gen_len=int(rng.integers(1, 4)), num_batches=int(rng.integers(1, 4)),
+                             kv_bytes_per_element=[None, 0.5625][int(rng.integers(0, 2))])
+        prof = profiles[n % 3]
+        pol = Policy(("row", "column")[n % 2], bool(rng.integers(0, 4)), ("coarse", "fine")[(n // 2) % 2],
+                     bool((n // 4) % 2))
+        if n % 5 == 4:  # constant plans, including splits past the prompt (rebuilt decode positions)
+            plan = rs.constant_plan(wl, pol.schedule, int(rng.integers(0, wl.prompt_len + wl.gen_len + 1)))
+        else:
+            plan = rs.plan_generation(sp, wl, prof, pol.schedule)
+        g = build_task_graph(sp, wl, prof, plan, pol)
+        tl, rep = simulate(g, prof)
+        out.append({
+            "spec": {k: getattr(sp, k) for k in ("hidden_dim", "num_layers", "num_heads", "ffn_dim", "precision_bytes")},
+            "wl": {k: getattr(wl, k) for k in ("batch_size", "prompt_len", "gen_len", "num_batches",
+                                               "kv_bytes_per_element")},
+            "profile": prof.to_dict(), "policy": [pol.schedule, pol.recompute, pol.granularity, pol.weights_resident],
+            "splits": [d.recompute_len for d in plan.decisions],
+            "tasks": [[t.kind.value, t.cost, list(t.deps), t.step, t.layer, t.batch, t.priority, t.part]
+                      for t in g.tasks],
+            "start": [e.start for e in tl.entries], "end": [e.end for e in tl.entries],
+            "names": [e.name for e in tl.entries],
+            "report": {"makespan": rep.makespan, "decode_throughput": rep.decode_throughput,
+                       "gpu_utilization": rep.gpu_utilization, "breakdown": rep.breakdown,
+                       "utilization_timeline": [list(x) for x in rep.utilization_timeline],
+                       "peak_gpu_bytes": rep.peak_gpu_bytes},
+        })
     return out
 
 
@@ -209,6 +253,7 @@ def main():
     doc = scheduler_cases()
     doc["cli"] = cli_cases()
     (OUT / "scheduler_golden.json").write_text(json.dumps(doc, sort_keys=True) + "\n")
+    (OUT / "pipesim_golden.json").write_text(json.dumps(pipesim_cases(), sort_keys=True) + "\n")
     np.savez_compressed(OUT / "numerics_golden.npz", **numerics_cases())
     print("wrote", OUT / "scheduler_golden.json", OUT / "numerics_golden.npz")
 

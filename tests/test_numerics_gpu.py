@@ -90,3 +90,66 @@ def test_build_append_project_match_oracle(heads, d, seq):
     assert np.max(np.abs(gn.stable_softmax(z) - nr.stable_softmax(z))) <= 1e-12
     with pytest.raises(ValueError, match="width"):
         gn.append_token_kv(full, x[-1, :-1], w_k[:-1, :-1], w_v[:-1, :-1])
+
+
+def test_reference_validate_generator_through_gpu_dropin(criterion):
+    """The reference's own randomized harness (cli.py:343-377: heads in {1,2,4}, head_dim in [1,4],
+    s' in [1,32], up to 4 sequences, every split l in [0, s']) pointed at the GPU drop-in: head dims
+    below 64 are zero-padded inside numerics.decode_attention.  The reference demands 1e-12 of its
+    fp64 path; here every split agrees with the fp64 oracle within the north-star 2e-2 (fp16 storage),
+    and the GPU output is the same for every split (K1 rebuild == the transferred cache)."""
+    rng = np.random.default_rng(0)
+    worst, cases, bad_split = 0.0, 0, []
+    for case in range(6):
+        heads = int(rng.choice([1, 2, 4]))
+        d = int(rng.integers(1, 5))
+        h = heads * d
+        seq = int(rng.integers(1, 33))
+        for _ in range(int(rng.integers(1, 5))):
+            x, w_k, w_v, w_o = (rng.standard_normal(s) for s in ((seq, h), (h, h), (h, h), (h, h)))
+            q = rng.standard_normal(h)
+            full = nr.build_kv(x, w_k, w_v, heads)
+            ref = nr.decode_attention(q, full, w_o)
+            gfull = gn.build_kv(x, w_k, w_v, heads)
+            outs = []
+            for split in range(seq + 1):
+                merged = gn.split_merge_kv(x, split, w_k, w_v, gn.KVState(gfull.keys[:, split:],
+                                                                          gfull.values[:, split:]))
+                outs.append(gn.decode_attention(q, merged, w_o))
+                worst = max(worst, _rel(outs[-1], ref))
+                cases += 1
+            if not all(np.array_equal(o, outs[0]) for o in outs):
+                bad_split.append((case, h, seq))
+    ok = worst <= RTOL and not bad_split
+    criterion("N1", f"reference validate generator (head_dim 1..4, padded) through the GPU drop-in: {cases} "
+                    f"(case, split) pairs within {worst:.2e} <= 2e-2 of the fp64 oracle, split-invariant", ok)
+    assert worst <= RTOL, worst
+    assert not bad_split, bad_split
+
+
+@pytest.mark.parametrize("d", [128, 64, 48, 3])
+def test_decode_attention_batch_ragged(d):
+    """Per-sequence caches of different lengths (the reference's KVState is per sequence) in one ragged
+    K2 launch: each row equals the single-sequence call bit for bit, and the fp64 oracle within 2e-2."""
+    rng = np.random.default_rng(d)
+    heads = 2
+    h = heads * d
+    lens = [1, 37, 130, 64, 5]
+    w_o = rng.standard_normal((h, h)) / np.sqrt(h)
+    kvs, qs, refs = [], [], []
+    for s in lens:
+        k, v = rng.standard_normal((heads, s, d)), rng.standard_normal((heads, s, d))
+        kvs.append(gn.KVState(k, v))
+        qs.append(rng.standard_normal(h))
+        refs.append(nr.decode_attention(qs[-1], nr.KVState(k, v), w_o))
+    out = gn.decode_attention_batch(np.stack(qs), kvs, w_o)
+    for i in range(len(lens)):
+        single = gn.decode_attention(qs[i], kvs[i], w_o)
+        assert np.array_equal(out[i], single), i
+        assert _rel(out[i], refs[i]) <= RTOL, (i, _rel(out[i], refs[i]))
+    with pytest.raises(ValueError, match="empty"):
+        gn.decode_attention_batch(np.stack(qs[:2]), [kvs[0], gn.KVState(kvs[1].keys[:, :0], kvs[1].values[:, :0])],
+                                  w_o)
+    with pytest.raises(ValueError, match="head_dim"):
+        gn.decode_attention(np.zeros(2 * 130), gn.KVState(np.zeros((2, 3, 130)), np.zeros((2, 3, 130))),
+                            np.eye(260))
