@@ -10,11 +10,24 @@
  * INTEGRATION.md) — that is the boundary a `kvoverlap` maintainer would bind.
  *
  * Conventions
- *  - The caller (Python / torch) owns every allocation, device and pinned
- *    host.  The library borrows raw pointers; it never allocates device
- *    memory, frees, or synchronises.
- *  - Every launch goes on the caller's stream (`stream` is a cudaStream_t,
- *    NULL = legacy default stream).
+ *  - The caller (Python / torch) owns every data buffer, device and pinned
+ *    host.  The kernel entry points (K1-K8, the codec, the probes) borrow raw
+ *    pointers: they never allocate or free memory and never synchronise; each
+ *    launches on the caller's stream (`stream` is a cudaStream_t, NULL =
+ *    legacy default stream) and returns once the launch is enqueued.
+ *    The exceptions, all outside the per-step path and named here:
+ *      * kvpr_decoder_create allocates the handle (host) and its CUDA events;
+ *        kvpr_decoder_destroy frees them.  kvpr_decoder_run only enqueues.
+ *      * kvpr_decoder_kernel_stats / kvpr_decoder_timeline wait on the
+ *        timing events they read (cudaEventSynchronize), after a timed run.
+ *      * kvpr_ipc_alloc / kvpr_ipc_free own the CUDA IPC peer regions of the
+ *        TP all-reduce (cudaMalloc / cudaFree; IPC handles cannot wrap torch
+ *        allocations); kvpr_ipc_open / _close map and unmap peers' regions.
+ *      * the stream-K decode GEMM (kvpr_linear_ws, M <= 64) keeps per-tile
+ *        arrival counters in a 16 KB zeroed device block the library
+ *        allocates once per (device, stream) on first use; every call leaves
+ *        them zero.  Workspaces (`ws`) are caller scratch of arbitrary
+ *        contents; calls sharing a ws must be stream-ordered.
  *  - Return 0 on success.  KVPR_EINVAL (bad shape / pointer / range) maps to
  *    ValueError, as the reference raises ValueError for the same conditions
  *    (numerics.py:22-32, costmodel.py:31-43); KVPR_ECUDA maps to RuntimeError.
@@ -47,6 +60,7 @@ extern "C" {
 #define KVPR_EPI_RELU 1  /* max(0, .) after bias */
 #define KVPR_EPI_F32 2   /* fp32 output (default fp16) */
 #define KVPR_EPI_ACCUM 4 /* fp32 output accumulated in place: out += result (residual add) */
+#define KVPR_EPI_W_TILED 8 /* w is in kvpr_tile_weight's box-tiled layout (ldw ignored); decode GEMM, M <= 64 */
 
 /* One output column segment of kvpr_linear.  Output element (m, n) with
  * seg = n / seg_width lands at
@@ -98,6 +112,13 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
  * 512 = 256 x 256 CTA-pair tile (cta_group::2), 32..256 = 128 x BN tile on one CTA, 0 = invalid
  * arguments.  Pure host function (no CUDA call); the bench labels its roofline line with it. */
 int kvpr_recompute_tile(int batch, int positions, int hidden, int sms);
+
+/* Decode-weight layout: W [N, K] (row stride ldw) rewritten as [N/128][K/64][128][64] fp16, zero-padded
+ * to whole 128 x 64 boxes, so each box the decode GEMM streams is 16 KB contiguous in HBM and a CTA's
+ * k-range is one contiguous region (row-major boxes are 128 separate 128-byte runs, 8 KB apart).
+ * Same products, same MMA order, same bits as the row-major operand.  out: kvpr_tiled_weight_bytes. */
+size_t kvpr_tiled_weight_bytes(int N, int K);
+int kvpr_tile_weight(const void* w, long long ldw, int N, int K, void* out, void* stream);
 
 /* Fused projection: out = epilogue(A[M,K] . W[N,K]^T + bias), tcgen05 GEMM.
  * Used for the decode-token q/k/v (K3), out-proj + residual (K4), fc1+ReLU and

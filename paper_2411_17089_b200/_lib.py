@@ -23,6 +23,7 @@ KVPR_ECUDA = 2
 EPI_RELU = 1
 EPI_F32 = 2
 EPI_ACCUM = 4
+EPI_W_TILED = 8
 
 # Every symbol include/kvpr.h declares (tests check the .so exports all of them).
 EXPORTS = (
@@ -32,6 +33,8 @@ EXPORTS = (
     "kvpr_sm_count",
     "kvpr_recompute_kv",
     "kvpr_recompute_tile",
+    "kvpr_tiled_weight_bytes",
+    "kvpr_tile_weight",
     "kvpr_linear",
     "kvpr_linear_ws",
     "kvpr_layernorm_linear_ws",
@@ -120,6 +123,8 @@ _SIGS = {
     "kvpr_sm_count": ([_i], _i),
     "kvpr_recompute_kv": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_recompute_tile": ([_i, _i, _i, _i], _i),
+    "kvpr_tiled_weight_bytes": ([_i, _i], _sz),
+    "kvpr_tile_weight": ([_vp, _ll, _i, _i, _vp, _vp], _i),
     "kvpr_linear": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp], _i),
     "kvpr_linear_ws": ([_vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i, _vp, _sz, _vp], _i),
     "kvpr_layernorm_linear_ws": ([_vp, _ll, _vp, _vp, _f, _vp, _ll, _vp, _ll, _i, _i, _i, ctypes.POINTER(Epilogue), _i,

@@ -191,6 +191,13 @@ static int auto_bn(int M, int N, int K, bool has_ws) {
   return bn;
 }
 
+size_t kvpr_tiled_weight_bytes(int N, int K) { return tiled_weight_bytes(N, K); }
+
+int kvpr_tile_weight(const void* w, long long ldw, int N, int K, void* out, void* stream) {
+  g_err[0] = 0;
+  return tile_weight(w, ldw, N, K, out, static_cast<cudaStream_t>(stream));
+}
+
 int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                    const kvpr_epilogue* epi, int bn, void* ws, size_t ws_bytes, void* stream) {
   g_err[0] = 0;
@@ -198,7 +205,7 @@ int kvpr_linear_ws(const void* a, long long lda, const void* w, long long ldw, i
     set_error("linear: null pointer");
     return KVPR_EINVAL;
   }
-  if (bn == 0) bn = auto_bn(M, N, K, ws != nullptr);
+  if (bn == 0) bn = (epi->flags & KVPR_EPI_W_TILED) ? -1 : auto_bn(M, N, K, ws != nullptr);
   return gemm_f16(a, lda, w, ldw, M, N, K, to_args(epi), bn, static_cast<cudaStream_t>(stream),
                   static_cast<float*>(ws), ws_bytes);
 }
@@ -212,7 +219,7 @@ int kvpr_layernorm_linear_ws(const float* x, long long ldx, const void* gamma, c
     return KVPR_EINVAL;
   }
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (bn == 0) bn = auto_bn(M, N, K, ws != nullptr);
+  if (bn == 0) bn = (epi->flags & KVPR_EPI_W_TILED) ? -1 : auto_bn(M, N, K, ws != nullptr);
   // KVPR_LN_FUSE=1: the one-launch form.  Off by default: at config 1 it measured 0.736 vs 0.700
   // ms/step with the rows re-read per pass, and 0.7101 vs 0.7067 with the rows held in registers
   // (profiles/r01_ln_fuse_ab.jsonl) — every CTA's LN prologue sits after its PDL wait and costs

@@ -55,6 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        if os.environ.get("KVPR_GEMM_TRACE") == "1":  # tools/sk_trace.py: per-CTA timestamps in the decode GEMM
+            cmd.insert(1, "-DKVPR_GEMM_TRACE")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))

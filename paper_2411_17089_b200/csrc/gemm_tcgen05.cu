@@ -19,6 +19,10 @@
 
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "kvpr_internal.h"
 
@@ -29,6 +33,24 @@ constexpr int kBK = 64;  // one 128-byte swizzle atom of fp16 along K
 constexpr int kBnSwapAB = -1;  // gemm_f16 tile code of the swapped-operand decode GEMM
 constexpr int kBnGemv = -2;    // CUDA-core decode projection, M <= kGemvMaxM (gemv.cu)
 constexpr long long kABandBytes = 32ll << 20;
+constexpr int kSkMaxTiles = 4096;
+
+// KVPR_GEMM_TRACE (tools only): per-CTA globaltimer stamps of the swap-AB decode GEMM
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// compiled in only with -DKVPR_GEMM_TRACE: even a null check of the pointer is an L2 load on the
+// epilogue's critical path
+__device__ __forceinline__ void gstamp(int slot) {
+#ifdef KVPR_GEMM_TRACE
+  if (g_gemm_trace != nullptr) g_gemm_trace[blockIdx.x * 8 + slot] = gtimer();
+#else
+  (void)slot;
+#endif
+}  // stream-K: n tiles of 128 outputs per decode GEMM (N <= 524288)
 
 // The 1-CTA ring is sized at launch: stage = A box (a_box_rows x 128 B: 16 KB, or only the live
 // rows of a small-M decode GEMM) + B box (BN x 128 B), as many stages as fit in shared memory
@@ -552,9 +574,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 //
 // The k order per output element is the regular kernel's (k-blocks ascending, 16-wide MMA K
 // steps), so an unsplit launch reproduces it bit for bit (tested against K1: the decode-time
-// k, v of the new token must equal the K1 rebuild).  k_splits > 1 (only with a workspace, never
-// for the q/k/v projection) writes raw fp32 partials that split_k_reduce_kernel sums in slice
-// order.
+// k, v of the new token must equal the K1 rebuild).  With a workspace (never for the q/k/v
+// projection) the kernel runs stream-K: every SM streams an equal share of the k-block units, and
+// tiles shared by several CTAs are finished in-kernel by the last CTA to arrive, which sums the
+// fp32 partial slots in k order (deterministic) and applies the epilogue -- no reduce launch.
 
 constexpr uint32_t kSwWBytes = kBM * kBK * 2;  // 16 KB: 128 weight rows x 64 k
 
@@ -596,6 +619,57 @@ __device__ __forceinline__ void tmem_ld_cols<64>(uint32_t taddr, uint32_t (&r)[6
   tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
 }
 
+// Work of one CTA as a list of segments (n block, k-blocks [kb0, kb1)).
+//  * stream-K (p.sk_ctas > 0): the n_blk x num_k_blk k-block units are cut into sk_ctas equal
+//    contiguous ranges, one per CTA, so every SM streams the same number of weight bytes whatever
+//    the tile count (out-proj: 32 tiles -> 148 CTAs of 13-14 k-blocks).  A range covers the tail of
+//    one tile, whole tiles, and the head of another.
+//  * otherwise: whole tiles, grid-strided (the q/k/v projection, whose k, v must carry K1's bits, and
+//    the TP push).
+struct SegIter {
+  int u, u_end, tile, stride, n_blk_count, nkb;
+  bool sk;
+  __device__ SegIter(const GemmArgs& p) {
+    nkb = p.num_k_blk;
+    n_blk_count = p.num_n_blk;
+    sk = p.sk_ctas > 0;
+    if (sk) {
+      const long long U = static_cast<long long>(p.num_n_blk) * nkb;
+      u = static_cast<int>(U * blockIdx.x / p.sk_ctas);
+      u_end = static_cast<int>(U * (blockIdx.x + 1) / p.sk_ctas);
+    } else {
+      tile = blockIdx.x;
+      stride = gridDim.x;
+    }
+  }
+  // next segment; first = it is the CTA's first one (the partial slot convention below)
+  __device__ bool next(int& n_blk, int& kb0, int& kb1) {
+    if (sk) {
+      if (u >= u_end) return false;
+      n_blk = u / nkb;
+      kb0 = u - n_blk * nkb;
+      kb1 = min(nkb, kb0 + (u_end - u));
+      u += kb1 - kb0;
+      return true;
+    }
+    if (tile >= n_blk_count) return false;
+    n_blk = tile;
+    kb0 = 0;
+    kb1 = nkb;
+    tile += stride;
+    return true;
+  }
+};
+
+// stream-K bookkeeping for tile t: the CTAs whose unit ranges meet it are [c_first, c_last]
+// (range of CTA c = [floor(c U / G), floor((c+1) U / G))); CTA c's segment of t sits in partial slot
+// 2c if c's range starts inside t (its first segment), else 2c + 1 (its last).
+__device__ __forceinline__ int sk_cta_of_unit(long long x, long long U, int G) {
+  // largest c with floor(c U / G) <= x
+  const long long c = ((x + 1) * G - 1) / U;
+  return static_cast<int>(c < G - 1 ? c : G - 1);
+}
+
 template <int MP, int KB>
 __global__ void __launch_bounds__(256, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
@@ -611,10 +685,12 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int sk_last;  // stream-K: this CTA finishes the tile (epilogue warps only)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   pdl_trigger();
+  if (threadIdx.x == 0) gstamp(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -637,13 +713,11 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int splits = p.k_splits > 1 ? p.k_splits : 1;
-  const int num_tiles = p.num_n_blk * splits;  // tile = (n block, k slice), slices of a block adjacent
-  const int kb_per = (p.num_k_blk + splits - 1) / splits;
-
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: weights before the PDL wait, activations after ----------------
+      // pass 0 issues the first ring of WEIGHT boxes (they never depend on an earlier kernel), pass 1
+      // (after the wait) their activation boxes, pass 2 everything after
       uint32_t stage = 0, phase = 0;
       int it = 0, pre = 0;
       for (int pass = 0; pass < 3; ++pass) {
@@ -651,13 +725,15 @@ __global__ void __launch_bounds__(256, 1)
         it = 0;
         stage = 0;
         phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-          const int n_blk = tile / splits;
-          const int kb0 = (tile % splits) * kb_per;
-          const int kb1 = min(p.num_k_blk, kb0 + kb_per);
+        SegIter segs(p);
+        int n_blk, kb0, kb1;
+        bool stop = false;
+        while (!stop && segs.next(n_blk, kb0, kb1)) {
           for (int kb = kb0; kb < kb1; kb += KB, ++it) {
-            if (pass == 0 && it == STAGES) break;
-            if (pass == 1 && it == pre) break;
+            if ((pass == 0 && it == STAGES) || (pass == 1 && it == pre)) {
+              stop = true;
+              break;
+            }
             if (pass == 2 && it < pre) {
               if (++stage == STAGES) {
                 stage = 0;
@@ -669,9 +745,16 @@ __global__ void __launch_bounds__(256, 1)
             if (pass != 1) {
               mbar_wait(&empty[stage], phase ^ 1);
               mbar_arrive_expect_tx(&full[stage], nbox * (kSwWBytes + Cfg::kXBox));
-              for (int j = 0; j < nbox; ++j)
-                tma_load_2d(sW + stage * Cfg::kWStage + j * kSwWBytes, &tmap_w, &full[stage], (kb + j) * kBK,
-                            n_blk * kBM);
+              for (int j = 0; j < nbox; ++j) {
+                // tiled weights: box (n_blk, kb) is the 16 KB contiguous run of rows (n_blk * nkb + kb) * 128
+                // of a [*, 64] matrix, so a CTA streams one contiguous region (DRAM-page friendly)
+                if (p.w_tiled)
+                  tma_load_2d(sW + stage * Cfg::kWStage + j * kSwWBytes, &tmap_w, &full[stage], 0,
+                              (n_blk * p.num_k_blk + kb + j) * kBM);
+                else
+                  tma_load_2d(sW + stage * Cfg::kWStage + j * kSwWBytes, &tmap_w, &full[stage], (kb + j) * kBK,
+                              n_blk * kBM);
+              }
             }
             if (pass != 0) {
               for (int j = 0; j < nbox; ++j)
@@ -683,7 +766,6 @@ __global__ void __launch_bounds__(256, 1)
               phase ^= 1;
             }
           }
-          if ((pass == 0 && it == STAGES) || (pass == 1 && it == pre)) break;
         }
       }
     }
@@ -692,14 +774,15 @@ __global__ void __launch_bounds__(256, 1)
       // ---------------- MMA issuer: M = 128 weight rows, N = MP activation rows ----------------
       constexpr uint32_t idesc = umma_idesc_f16_f32(kBM, MP);
       uint32_t stage = 0, phase = 0, local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      SegIter segs(p);
+      int n_blk, kb0, kb1;
+      while (segs.next(n_blk, kb0, kb1)) {
         const uint32_t acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
+        ++local;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * MP;
-        const int kb0 = (tile % splits) * kb_per;
-        const int kb1 = min(p.num_k_blk, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; kb += KB) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -727,12 +810,15 @@ __global__ void __launch_bounds__(256, 1)
     pdl_wait();
     const uint32_t q = warp & 3;
     uint32_t local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int n_blk = tile / splits;
-      const int ks = tile % splits;
+    SegIter segs(p);
+    int n_blk, kb0, kb1;
+    while (segs.next(n_blk, kb0, kb1)) {
+      const bool first_seg = local == 0;
       const uint32_t acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      ++local;
       mbar_wait(&tfull[acc], acc_phase);
+      if (threadIdx.x == 128 && local <= 3) gstamp(local);
       tc_fence_after();
       uint32_t r[MP];
       tmem_ld_cols<MP>(tmem_base + ((q * 32u) << 16) + acc * MP, r);
@@ -740,7 +826,8 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator drained into registers
-      const int n = n_blk * kBM + q * 32 + lane;
+      const int col = q * 32 + lane;               // column inside the 128-wide tile
+      const int n = n_blk * kBM + col;
       if (p.tp_world > 1) {
         // fused TP all-reduce, push half (csrc/tpcomm.cu): the raw fp32 partial of this tile goes
         // straight into slot [rank] of the tile owner's receive buffer over NVLink, then the owner's
@@ -760,40 +847,122 @@ __global__ void __launch_bounds__(256, 1)
         }
         continue;
       }
+      float v[MP];
+#pragma unroll
+      for (int m = 0; m < MP; ++m) v[m] = __uint_as_float(r[m]);
+      if (kb0 != 0 || kb1 != p.num_k_blk) {
+        // stream-K partial tile.  Every contributor but the last stores its raw fp32 partial in a slot
+        // and counts itself in; the last one to arrive sums all partials in k order (deterministic:
+        // the order never depends on which CTA finishes last) and applies the epilogue.  The CTA
+        // holding a tile's first k-blocks (c_first) usually reaches it last -- the tile is its final
+        // segment, while for every later CTA it is the first -- so it checks the count before
+        // publishing: if the others are all in, it keeps its partial in registers and skips a slot
+        // store and an atomic round trip on the kernel's critical tail.
+        const long long U = static_cast<long long>(p.num_n_blk) * p.num_k_blk;
+        const int G = p.sk_ctas;
+        const int c = blockIdx.x;
+        const long long t0 = static_cast<long long>(n_blk) * p.num_k_blk;
+        const int c_first = sk_cta_of_unit(t0, U, G);
+        const int c_last = sk_cta_of_unit(t0 + p.num_k_blk - 1, U, G);
+        const unsigned others = static_cast<unsigned>(c_last - c_first);
+        unsigned* ctr = p.sk_counters + n_blk;
+        bool last = false;
+        if (c == c_first && !first_seg) {
+          if (threadIdx.x == 128) {
+            unsigned seen;
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+            sk_last = seen == others;
+            if (sk_last) *ctr = 0u;  // every other arrival of this launch is in: zero for the next call
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          last = sk_last;
+        }
+        if (!last) {
+          float* slot = p.ws + (2LL * c + (first_seg ? 0 : 1)) * MP * kBM;
+#pragma unroll
+          for (int m = 0; m < MP; ++m) slot[m * kBM + col] = v[m];
+          // publish: the CTA barrier orders the 128 threads' slot stores before thread 128's arrival,
+          // a gpu-scope acq_rel atomic (release is cumulative); the last arriver's acquire + the
+          // second barrier order every slot before the reads below
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 128) {
+            unsigned old;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+            sk_last = old == others;
+            if (sk_last) *ctr = 0u;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (!sk_last) continue;
+        }
+        const bool own_in_regs = last;  // c_first's partial never went to its slot
+        if (threadIdx.x == 128) gstamp(4);
+        // sum the slots in k order (CTA c_first's is its last segment, every later CTA's its first).
+        // When the reducer is c_first its own partial, first in the order, is still in v (0 + v == v,
+        // so both paths produce the same bits)
+        const int cc0 = own_in_regs ? c_first + 1 : c_first;
+        if (!own_in_regs) {
+#pragma unroll
+          for (int m = 0; m < MP; ++m) v[m] = 0.f;
+        }
+        // slots per batch of loads: each batch is one L2 round trip (1-3 us while the weight stream
+        // loads the L2), so as many as the registers allow (out-proj at b32 has 5-6 contributors)
+        constexpr int SL = MP >= 64 ? 2 : (MP >= 32 ? 5 : 8);
+        for (int cc = cc0; cc <= c_last; cc += SL) {
+          float a[SL][MP];
+#pragma unroll
+          for (int t = 0; t < SL; ++t) {
+            const int c2 = cc + t;
+            const float* sl = p.ws + (2LL * c2 + (c2 == c_first && U * c2 / G < t0 ? 1 : 0)) * MP * kBM + col;
+#pragma unroll
+            for (int m = 0; m < MP; ++m) a[t][m] = c2 <= c_last ? __ldcg(sl + m * kBM) : 0.f;
+          }
+#pragma unroll
+          for (int t = 0; t < SL; ++t)
+#pragma unroll
+            for (int m = 0; m < MP; ++m)
+              if (cc + t <= c_last) v[m] += a[t][m];
+        }
+        if (threadIdx.x == 128) gstamp(6);
+      }
       if (n < p.N) {
-        if (splits > 1) {
-          float* o = p.ws + static_cast<long long>(ks) * p.M * p.ws_ld + n;
+        const float bias = p.bias != nullptr ? __half2float(p.bias[n]) : 0.f;
+        const bool scaled = n < p.scale_cols;
+        const int seg = n / p.seg_width;
+        const int scol = n - seg * p.seg_width;
+        char* sp = static_cast<char*>(seg == 0 ? p.seg_ptr[0] : (seg == 1 ? p.seg_ptr[1] : p.seg_ptr[2]));
+        const long long gs = seg == 0 ? p.seg_group_stride[0] : (seg == 1 ? p.seg_group_stride[1] : p.seg_group_stride[2]);
+        const bool f32 = (p.flags & KVPR_EPI_F32) != 0, accum = f32 && (p.flags & KVPR_EPI_ACCUM);
+        // element offsets of the MP rows: one row group (the decode case, row_group >= M) is a plain
+        // stride; otherwise 32-bit div/mod (a 64-bit division per row costs ~0.1 us, 4 us per tile)
+        const int rg = p.row_group >= MP ? MP : p.row_group;  // >= MP: one row group, a plain stride
+        const long long ld = p.ld;
+#define SWAP_OFF(m) (static_cast<long long>((m) % rg) * ld + static_cast<long long>((m) / rg) * gs + scol)
+        // residual add: every old value is loaded before the first store -- interleaved
+        // load / store pairs would be serialised (possible aliasing), one L2 round trip per row
+        float old[MP];
 #pragma unroll
-          for (int m = 0; m < MP; ++m)
-            if (m < p.M) o[static_cast<long long>(m) * p.ws_ld] = __uint_as_float(r[m]);
-        } else {
-          const float bias = p.bias != nullptr ? __half2float(p.bias[n]) : 0.f;
-          const bool scaled = n < p.scale_cols;
-          const int seg = n / p.seg_width;
-          const int col = n - seg * p.seg_width;
-          char* sp = static_cast<char*>(seg == 0 ? p.seg_ptr[0] : (seg == 1 ? p.seg_ptr[1] : p.seg_ptr[2]));
-          const long long gs = seg == 0 ? p.seg_group_stride[0] : (seg == 1 ? p.seg_group_stride[1] : p.seg_group_stride[2]);
+        for (int m = 0; m < MP; ++m) old[m] = (accum && m < p.M) ? reinterpret_cast<const float*>(sp)[SWAP_OFF(m)] : 0.f;
 #pragma unroll
-          for (int m = 0; m < MP; ++m) {
-            if (m >= p.M) continue;
-            float v = __uint_as_float(r[m]) + bias;
-            if (scaled) v *= p.scale;
-            if (p.flags & KVPR_EPI_RELU) v = fmaxf(v, 0.f);
-            const long long off = (m % p.row_group) * p.ld + (m / p.row_group) * gs + col;
-            if (p.flags & KVPR_EPI_F32) {
-              float* o = reinterpret_cast<float*>(sp) + off;
-              *o = (p.flags & KVPR_EPI_ACCUM) ? *o + v : v;
-            } else {
-              reinterpret_cast<__half*>(sp)[off] = __float2half_rn(v);
-            }
+        for (int m = 0; m < MP; ++m) {
+          if (m >= p.M) continue;
+          float x = v[m] + bias;
+          if (scaled) x *= p.scale;
+          if (p.flags & KVPR_EPI_RELU) x = fmaxf(x, 0.f);
+          if (f32) {
+            reinterpret_cast<float*>(sp)[SWAP_OFF(m)] = accum ? old[m] + x : x;
+          } else {
+            reinterpret_cast<__half*>(sp)[SWAP_OFF(m)] = __float2half_rn(x);
           }
         }
+#undef SWAP_OFF
+        if (threadIdx.x == 128) gstamp(7);
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) gstamp(5);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
@@ -911,7 +1080,8 @@ static int launch_swapab(const void* a, long long lda, const void* w, long long 
                          cudaStream_t stream) {
   using Cfg = SwapCfg<MP, KB>;
   CUtensorMap tw, tx;
-  int rc = make_tmap(&tw, w, args.N, args.K, ldw, kBM);
+  const long long tiled_rows = static_cast<long long>((args.N + kBM - 1) / kBM) * ((args.K + kBK - 1) / kBK) * kBM;
+  int rc = args.w_tiled ? make_tmap(&tw, w, tiled_rows, kBK, kBK, kBM) : make_tmap(&tw, w, args.N, args.K, ldw, kBM);
   if (rc) return rc;
   rc = make_tmap(&tx, a, args.M, args.K, lda, MP);  // rows >= M of the box are zero-filled
   if (rc) return rc;
@@ -919,8 +1089,7 @@ static int launch_swapab(const void* a, long long lda, const void* w, long long 
   args.num_n_blk = (args.N + kBM - 1) / kBM;
   args.num_k_blk = (args.K + kBK - 1) / kBK;
   args.a_box_rows = MP;
-  const int splits = args.k_splits > 1 ? args.k_splits : 1;
-  const int tiles = args.num_n_blk * splits;
+  args.k_splits = 1;
   int dev = 0;
   cudaGetDevice(&dev);
   constexpr uint32_t smem = 1024 + Cfg::kStages * Cfg::kStageBytes + kBarrierBytes;
@@ -929,12 +1098,9 @@ static int launch_swapab(const void* a, long long lda, const void* w, long long 
     cudaFuncSetAttribute(gemm_swapab_kernel<MP, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_done[dev] = 1;
   }
-  const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
-  rc = launch("gemm_swapab", gemm_swapab_kernel<MP, KB>, grid, 256, smem, stream, tw, tx, args);
-  if (rc || splits == 1) return rc;
-  const long long work = static_cast<long long>(args.M) * (args.N / 32);
-  return launch("split_k_reduce", split_k_reduce_kernel, static_cast<unsigned>((work + 127) / 128), 128, 0, stream,
-                args);
+  // stream-K: one CTA per SM over equal unit ranges; otherwise whole tiles, grid-strided
+  const int grid = args.sk_ctas > 0 ? args.sk_ctas : (args.num_n_blk < sm_count(dev) ? args.num_n_blk : sm_count(dev));
+  return launch("gemm_swapab", gemm_swapab_kernel<MP, KB>, grid, 256, smem, stream, tw, tx, args);
 }
 
 static int launch_2sm(const void* a, long long lda, const void* w, long long ldw, GemmArgs args, cudaStream_t stream) {
@@ -961,6 +1127,30 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
   return launch("gemm_tcgen05_2sm", gemm_tcgen05_2sm_kernel, grid, 256, k2SmemBytes, stream, ta, tb, args);
 }
 
+// Stream-K arrival counters: one zeroed block of kSkMaxTiles counters per (device, stream), made on first
+// use.  Launches on one stream are ordered (the epilogue waits for the previous grid before touching
+// them) and the last arrival of every tile returns its counter to zero, so a block is reusable by the
+// next call; distinct streams get distinct blocks, so concurrent GEMMs never share one.
+static unsigned* sk_counters_for(int dev, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned*> blocks;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = blocks.find({dev, stream});
+  if (it != blocks.end()) return it->second;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, kSkMaxTiles * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemsetAsync(p, 0, kSkMaxTiles * sizeof(unsigned), stream) != cudaSuccess) {
+    set_error("stream-K counters: device allocation failed");
+    return nullptr;
+  }
+  blocks[{dev, stream}] = p;
+  return p;
+}
+
+extern "C" int kvpr_debug_gemm_trace(void* buf) {  // tools/sk_trace.py: 8 u64 stamps per CTA, NULL = off
+  return cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf)) == cudaSuccess ? KVPR_OK : KVPR_ECUDA;
+}
+
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws, size_t ws_bytes, const GemvLn* ln) {
   if (ln != nullptr && bn != kBnGemv) {
@@ -971,27 +1161,42 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
   args.M = M;
   args.N = N;
   args.K = K;
+  args.w_tiled = (epi.flags & KVPR_EPI_W_TILED) ? 1 : 0;
+  if (args.w_tiled) {  // only the swap-AB decode GEMM reads the box-tiled layout
+    if (M > 64 || (bn != 0 && bn != kBnSwapAB)) {
+      set_error("gemm: tiled weights (KVPR_EPI_W_TILED) need the swap-AB decode GEMM (M <= 64, bn 0 or -1)");
+      return KVPR_EINVAL;
+    }
+    bn = kBnSwapAB;
+  }
   args.k_splits = 1;
   args.ws = nullptr;
   args.ws_ld = N;
-  if (bn == kBnSwapAB && ws != nullptr) {
-    // weight-streaming decode GEMM: an SM streams ~46 GB/s, so HBM needs every SM: slice K until
-    // the 128-row weight tiles fill them (deterministic: slices summed in order by
-    // split_k_reduce_kernel).  The reduce is one more dependent launch, so only weights of
-    // >= 16 MB split, into slices of >= 16 k-blocks (measured: tools/decode_gemm_bench.py)
+  args.sk_ctas = 0;
+  args.sk_counters = nullptr;
+  if (bn == kBnSwapAB && ws != nullptr && M > 0 && M <= 64 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
+    // weight-streaming decode GEMM: HBM needs every SM streaming for the whole kernel, so stream-K
+    // spreads the n-tile x k-block units evenly over all SMs (KVPR_STREAMK=0: whole tiles instead)
+    static const bool sk_on = [] {
+      const char* e = getenv("KVPR_STREAMK");
+      return !(e != nullptr && e[0] == '0');
+    }();
     int dev = 0;
     cudaGetDevice(&dev);
-    const int n_tiles = (N + kBM - 1) / kBM;
-    const int num_kb = (K + kBK - 1) / kBK;
-    int s = sm_count(dev) / n_tiles;
-    if (s > 8) s = 8;
-    if (s > num_kb / 16) s = num_kb / 16;
-    if (static_cast<long long>(N) * K * 2 < (16ll << 20)) s = 1;
-    while (s > 1 && (num_kb + s - 1) / s * (s - 1) >= num_kb) --s;  // every slice non-empty
-    if (s > 1 && static_cast<size_t>(s) * M * N * sizeof(float) <= ws_bytes &&
-        (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
-      args.k_splits = s;
+    const long long n_tiles = (N + kBM - 1) / kBM;
+    const long long units = n_tiles * ((K + kBK - 1) / kBK);
+    const int G = static_cast<int>(units < sm_count(dev) ? units : sm_count(dev));
+    const int mp = M <= 16 ? 16 : (M <= 32 ? 32 : 64);
+    const size_t slots = 2ull * G * mp * kBM * sizeof(float);
+    // whole tiles already cover >= 3/4 of the SMs (fc1, LM head): stream-K's fixup costs more than
+    // the idle SMs (tools/decode_gemm_tiled.py: fc1 28.9 us whole tiles vs 35.6 stream-K)
+    const bool sparse = n_tiles * 4 < 3LL * sm_count(dev);
+    if (sk_on && sparse && n_tiles <= kSkMaxTiles && slots <= ws_bytes) {
+      unsigned* ctr = sk_counters_for(dev, stream);
+      if (ctr == nullptr) return KVPR_ECUDA;
+      args.sk_ctas = G;
       args.ws = ws;
+      args.sk_counters = ctr;
     }
   } else if (ws != nullptr && M <= kBM && bn > 0 && bn <= 256 && K >= 8192) {
     // only long k-loops gain: short ones are dominated by pipeline fill + the extra reduce launch
@@ -1015,7 +1220,7 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
     set_error("gemm: non-positive shape M=%d N=%d K=%d", M, N, K);
     return KVPR_EINVAL;
   }
-  if (N % 32 != 0 || K % 8 != 0 || lda % 8 != 0 || ldw % 8 != 0) {
+  if (N % 32 != 0 || K % 8 != 0 || lda % 8 != 0 || (!args.w_tiled && ldw % 8 != 0)) {
     set_error("gemm: need N%%32==0, K%%8==0, lda/ldw%%8==0 (N=%d K=%d lda=%lld ldw=%lld)", N, K, lda, ldw);
     return KVPR_EINVAL;
   }
@@ -1083,6 +1288,49 @@ int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, 
 }  // namespace kvpr
 
 namespace kvpr {
+
+// W [N, K] row-major (row stride ldw) -> box-tiled [n_blk][k_blk][128][64], zero-padded to whole boxes:
+// the layout the swap-AB decode GEMM streams as contiguous 16 KB boxes (KVPR_EPI_W_TILED).  One
+// thread per 8 consecutive k (16 bytes).
+__global__ void tile_weight_kernel(const __half* __restrict__ w, long long ldw, int N, int K, int nkb,
+                                   __half* __restrict__ out, long long total_vec) {
+  const long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= total_vec) return;
+  const long long e = v * 8;                 // element index in the tiled buffer
+  const int c = static_cast<int>(e % kBK);   // k inside the box
+  const long long rowt = e / kBK;            // row of the [*, 64] view
+  const int r = static_cast<int>(rowt % kBM);
+  const long long box = rowt / kBM;
+  const int kb = static_cast<int>(box % nkb);
+  const long long nb = box / nkb;
+  const long long n = nb * kBM + r;
+  const int k = kb * kBK + c;
+  uint4 val = make_uint4(0, 0, 0, 0);
+  if (n < N && k + 8 <= K) val = *reinterpret_cast<const uint4*>(w + n * ldw + k);
+  else if (n < N) {
+    __half h[8];
+    for (int i = 0; i < 8; ++i) h[i] = k + i < K ? w[n * ldw + k + i] : __float2half(0.f);
+    val = *reinterpret_cast<uint4*>(h);
+  }
+  *reinterpret_cast<uint4*>(out + e) = val;
+}
+
+size_t tiled_weight_bytes(int N, int K) {
+  if (N <= 0 || K <= 0) return 0;
+  return static_cast<size_t>((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK) * kBM * kBK * sizeof(__half);
+}
+
+int tile_weight(const void* w, long long ldw, int N, int K, void* out, cudaStream_t stream) {
+  if (w == nullptr || out == nullptr || N <= 0 || K <= 0 || ldw < K || (reinterpret_cast<uintptr_t>(w) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15) || ldw % 8 != 0) {
+    set_error("tile_weight: need non-null 16-byte aligned w / out, N, K > 0, ldw >= K, ldw %% 8 == 0");
+    return KVPR_EINVAL;
+  }
+  const int nkb = (K + kBK - 1) / kBK;
+  const long long total_vec = static_cast<long long>(tiled_weight_bytes(N, K) / 16);
+  return launch("tile_weight", tile_weight_kernel, static_cast<unsigned>((total_vec + 255) / 256), 256, 0, stream,
+                static_cast<const __half*>(w), ldw, N, K, nkb, static_cast<__half*>(out), total_vec);
+}
 
 // Push half of the fused TP all-reduce: the swap-AB decode GEMM whose epilogue stores raw fp32
 // partials into the tile owners' receive slots and releases their flags (csrc/tpcomm.cu).

@@ -34,6 +34,11 @@ struct GemmArgs {
   float* ws;       // split-K partials [k_splits][M][ws_ld] fp32
   int ws_ld;
   int group_m;     // rasterization band (tile_coords): > 0 m-blocks per band, < 0 n-blocks per band
+  // stream-K swap-AB decode GEMM (sk_ctas > 0): CTAs; fp32 partial slots in ws; per-tile arrival
+  // counters (library-owned, zero between calls)
+  int sk_ctas;
+  unsigned* sk_counters;
+  int w_tiled;  // swap-AB: W in the box-tiled layout of kvpr_tile_weight (each 128 x 64 box contiguous)
   // fused TP all-reduce (swap-AB kernel only; tp_world > 1): raw partials pushed to the tile owner
   int tp_rank, tp_world;
   unsigned tp_epoch;
@@ -67,6 +72,9 @@ int gemv_slices(int N, int device);
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0, const GemvLn* ln = nullptr);
+
+size_t tiled_weight_bytes(int N, int K);
+int tile_weight(const void* w, long long ldw, int N, int K, void* out, cudaStream_t stream);
 
 int gemm_tp_partials(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K,
                      const GemmArgs& tp, cudaStream_t stream);

@@ -8,6 +8,7 @@ computes on the CPU; a missing library or a non-CUDA tensor is an error.
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import torch
 
@@ -48,20 +49,48 @@ def recompute_kv(x: torch.Tensor, w_kv: torch.Tensor, b_kv: torch.Tensor | None,
     )
 
 
-def linear(a: torch.Tensor, w: torch.Tensor, epi: _lib.Epilogue, M: int | None = None, bn: int = 0,
+@dataclass(frozen=True)
+class TiledWeight:
+    """A weight W [N, K] in kvpr_tile_weight's box-tiled layout (decode GEMMs, M <= 64)."""
+
+    data: torch.Tensor
+    N: int
+    K: int
+
+    @property
+    def shape(self):
+        return (self.N, self.K)
+
+
+def linear(a: torch.Tensor, w, epi: _lib.Epilogue, M: int | None = None, bn: int = 0,
            stream=None, lda: int | None = None, ws: torch.Tensor | None = None) -> None:
-    """out = epilogue(A[M,K] . W[N,K]^T + bias) via the tcgen05 GEMM (ws enables split-K for decode GEMMs)."""
+    """out = epilogue(A[M,K] . W[N,K]^T + bias) via the tcgen05 GEMM (ws enables stream-K for decode GEMMs).
+    w: [N, K] fp16 tensor, or a TiledWeight (streams 16 KB-contiguous boxes; swap-AB decode GEMM only)."""
     _need(a, torch.float16, "a")
-    _need(w, torch.float16, "w")
-    N, K = w.shape
+    if isinstance(w, TiledWeight):
+        _need(w.data, torch.float16, "w")
+        N, K, wptr, ldw = w.N, w.K, w.data.data_ptr(), 64
+        epi.flags |= _lib.EPI_W_TILED
+    else:
+        _need(w, torch.float16, "w")
+        (N, K), wptr, ldw = w.shape, w.data_ptr(), w.stride(0)
     if M is None:
         M = a.shape[0]
     lda = K if lda is None else lda
     if ws is None:
-        _lib.call("kvpr_linear", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn, _stream(stream))
+        _lib.call("kvpr_linear", a.data_ptr(), lda, wptr, ldw, M, N, K, epi, bn, _stream(stream))
     else:
-        _lib.call("kvpr_linear_ws", a.data_ptr(), lda, w.data_ptr(), w.stride(0), M, N, K, epi, bn,
+        _lib.call("kvpr_linear_ws", a.data_ptr(), lda, wptr, ldw, M, N, K, epi, bn,
                   ws.data_ptr(), ws.numel() * ws.element_size(), _stream(stream))
+
+
+def tile_weight(w: torch.Tensor, stream=None) -> TiledWeight:
+    """W [N, K] fp16 -> its box-tiled copy for the decode GEMM (kvpr_tile_weight)."""
+    _need(w, torch.float16, "w")
+    N, K = w.shape
+    out = torch.empty(_lib.load().kvpr_tiled_weight_bytes(N, K) // 2, dtype=torch.float16, device=w.device)
+    _lib.call("kvpr_tile_weight", w.data_ptr(), w.stride(0), N, K, out.data_ptr(), _stream(stream))
+    return TiledWeight(out, N, K)
 
 
 def linear_simple(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, out: torch.Tensor,

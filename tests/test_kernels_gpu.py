@@ -532,3 +532,54 @@ def test_decode_attention_cluster_merge_equals_combine_kernel(dev, batch, heads,
         torch.cuda.synchronize()
         outs.append(o)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 4096, 4096), (32, 16384, 4096), (32, 4096, 16384), (64, 4096, 4096),
+                                   (17, 50272, 768), (1, 1024, 4096), (12, 384, 256)])
+def test_stream_k_decode_gemm(dev, M, N, K):
+    """Swap-AB decode GEMM with a workspace runs stream-K (every SM an equal share of the n-tile x
+    k-block units; shared tiles finished in-kernel by the last CTA, partials summed in k order):
+    fp32-reference accurate, equal to the unsplit kernel within fp32 reassociation, bit-identical across
+    calls even when the workspace (its counter tail included) is overwritten with garbage in between."""
+    a = _rand(M, K, scale=0.5, seed=61)
+    w = _rand(N, K, scale=0.02, seed=62)
+    bias = _rand(N, scale=0.1, seed=63)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    ref = a.float() @ w.float().T + bias.float()
+    outs = []
+    for trial in range(3):
+        ws.random_(0, 256)  # arbitrary scratch contents, counters included
+        o = torch.empty(M, N, dtype=torch.float32, device=dev)
+        kernels.linear_simple(a, w, bias, o, bn=-1, ws=ws)
+        outs.append(o)
+    plain = torch.empty(M, N, dtype=torch.float32, device=dev)
+    kernels.linear_simple(a, w, bias, plain, bn=-1)  # no workspace: whole tiles, one CTA each
+    resid = torch.randn(M, N, device=dev)
+    acc = resid.clone()
+    kernels.linear_simple(a, w, bias, acc, flags=_lib.EPI_ACCUM, bn=-1, ws=ws)
+    torch.cuda.synchronize()
+    _close(outs[0], ref, rtol=1e-3, atol=1e-3)
+    assert all(torch.equal(outs[0], x) for x in outs[1:])
+    _close(outs[0], plain, rtol=1e-4, atol=1e-4)
+    _close(acc, resid + outs[0], rtol=1e-6, atol=1e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 4096, 4096), (17, 50272, 768), (32, 12288, 4096), (5, 384, 200)])
+def test_tiled_weights_bit_identical(dev, M, N, K):
+    """Box-tiled weights (kvpr_tile_weight, each 128 x 64 box contiguous; zero-padded to whole boxes) feed
+    the same smem bytes to the same MMA sequence: bit-identical to the row-major operand, unsplit and
+    stream-K alike (the q/k/v projection relies on it to keep K1's bits)."""
+    a = _rand(M, K, scale=0.5, seed=71)
+    w = _rand(N, K, scale=0.02, seed=72)
+    bias = _rand(N, scale=0.1, seed=73)
+    wt = kernels.tile_weight(w)
+    ws = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    for use_ws in (None, ws):
+        o1 = torch.empty(M, N, dtype=torch.float32, device=dev)
+        o2 = torch.empty_like(o1)
+        kernels.linear_simple(a, w, bias, o1, bn=-1, ws=use_ws)
+        kernels.linear_simple(a, wt, bias, o2, ws=use_ws)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2)
+    with pytest.raises(ValueError, match="tiled"):
+        kernels.linear_simple(_rand(80, K, seed=74), wt, bias, torch.empty(80, N, device=dev))
