@@ -932,29 +932,38 @@ __global__ void __launch_bounds__(256, 1)
         char* sp = static_cast<char*>(seg == 0 ? p.seg_ptr[0] : (seg == 1 ? p.seg_ptr[1] : p.seg_ptr[2]));
         const long long gs = seg == 0 ? p.seg_group_stride[0] : (seg == 1 ? p.seg_group_stride[1] : p.seg_group_stride[2]);
         const bool f32 = (p.flags & KVPR_EPI_F32) != 0, accum = f32 && (p.flags & KVPR_EPI_ACCUM);
-        // element offsets of the MP rows: one row group (the decode case, row_group >= M) is a plain
-        // stride; otherwise 32-bit div/mod (a 64-bit division per row costs ~0.1 us, 4 us per tile)
-        const int rg = p.row_group >= MP ? MP : p.row_group;  // >= MP: one row group, a plain stride
-        const long long ld = p.ld;
-#define SWAP_OFF(m) (static_cast<long long>((m) % rg) * ld + static_cast<long long>((m) / rg) * gs + scol)
         // residual add: every old value is loaded before the first store -- interleaved
         // load / store pairs would be serialised (possible aliasing), one L2 round trip per row
-        float old[MP];
+        const long long ld = p.ld;
+        const int rg = p.row_group;
+        // (MP = 64 keeps the interleaved form: 64 more live registers would spill)
+        constexpr int HOIST = MP <= 32 ? MP : 1;
+        auto store_rows = [&](auto off_of) {
+          float old[HOIST];
+          if constexpr (MP <= 32) {
 #pragma unroll
-        for (int m = 0; m < MP; ++m) old[m] = (accum && m < p.M) ? reinterpret_cast<const float*>(sp)[SWAP_OFF(m)] : 0.f;
-#pragma unroll
-        for (int m = 0; m < MP; ++m) {
-          if (m >= p.M) continue;
-          float x = v[m] + bias;
-          if (scaled) x *= p.scale;
-          if (p.flags & KVPR_EPI_RELU) x = fmaxf(x, 0.f);
-          if (f32) {
-            reinterpret_cast<float*>(sp)[SWAP_OFF(m)] = accum ? old[m] + x : x;
-          } else {
-            reinterpret_cast<__half*>(sp)[SWAP_OFF(m)] = __float2half_rn(x);
+            for (int m = 0; m < MP; ++m)
+              old[m] = (accum && m < p.M) ? reinterpret_cast<const float*>(sp)[off_of(m)] : 0.f;
           }
-        }
-#undef SWAP_OFF
+#pragma unroll
+          for (int m = 0; m < MP; ++m) {
+            if (m >= p.M) continue;
+            float x = v[m] + bias;
+            if (scaled) x *= p.scale;
+            if (p.flags & KVPR_EPI_RELU) x = fmaxf(x, 0.f);
+            if (f32) {
+              float* o = reinterpret_cast<float*>(sp) + off_of(m);
+              if constexpr (MP <= 32) *o = accum ? old[m] + x : x;
+              else *o = accum ? *o + x : x;
+            } else {
+              reinterpret_cast<__half*>(sp)[off_of(m)] = __float2half_rn(x);
+            }
+          }
+        };
+        if (rg >= MP)  // one row group (every decode GEMM): a plain stride, no division per row
+          store_rows([&](int m) { return static_cast<long long>(m) * ld + scol; });
+        else
+          store_rows([&](int m) { return static_cast<long long>(m % rg) * ld + static_cast<long long>(m / rg) * gs + scol; });
         if (threadIdx.x == 128) gstamp(7);
       }
     }
