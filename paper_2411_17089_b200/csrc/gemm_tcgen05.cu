@@ -661,6 +661,19 @@ struct SegIter {
   }
 };
 
+// Barrier of the 128 epilogue threads (named barrier 1) that also ORs a predicate over them: how
+// thread 128's arrival verdict reaches the others without a shared flag (a flag rewritten for the next
+// segment could race a slow reader of the previous one; compute-sanitizer racecheck flagged it)
+__device__ __forceinline__ bool epi_bar_or(bool v) {
+  unsigned r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %1, 0;\n\tbar.red.or.pred p, 1, 128, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(static_cast<unsigned>(v))
+      : "memory");
+  return r != 0;
+}
+
 // stream-K bookkeeping for tile t: the CTAs whose unit ranges meet it are [c_first, c_last]
 // (range of CTA c = [floor(c U / G), floor((c+1) U / G))); CTA c's segment of t sits in partial slot
 // 2c if c's range starts inside t (its first segment), else 2c + 1 (its last).
@@ -685,7 +698,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ int sk_last;  // stream-K: this CTA finishes the tile (epilogue warps only)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -868,14 +880,14 @@ __global__ void __launch_bounds__(256, 1)
         unsigned* ctr = p.sk_counters + n_blk;
         bool last = false;
         if (c == c_first && !first_seg) {
+          bool seen_all = false;
           if (threadIdx.x == 128) {
             unsigned seen;
             asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
-            sk_last = seen == others;
-            if (sk_last) *ctr = 0u;  // every other arrival of this launch is in: zero for the next call
+            seen_all = seen == others;
+            if (seen_all) *ctr = 0u;  // every other arrival of this launch is in: zero for the next call
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          last = sk_last;
+          last = epi_bar_or(seen_all);  // thread 128's verdict to all 128 epilogue threads
         }
         if (!last) {
           float* slot = p.ws + (2LL * c + (first_seg ? 0 : 1)) * MP * kBM;
@@ -885,14 +897,14 @@ __global__ void __launch_bounds__(256, 1)
           // a gpu-scope acq_rel atomic (release is cumulative); the last arriver's acquire + the
           // second barrier order every slot before the reads below
           asm volatile("bar.sync 1, 128;" ::: "memory");
+          bool fin = false;
           if (threadIdx.x == 128) {
             unsigned old;
             asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-            sk_last = old == others;
-            if (sk_last) *ctr = 0u;
+            fin = old == others;
+            if (fin) *ctr = 0u;
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (!sk_last) continue;
+          if (!epi_bar_or(fin)) continue;
         }
         const bool own_in_regs = last;  // c_first's partial never went to its slot
         if (threadIdx.x == 128) gstamp(4);
