@@ -170,6 +170,56 @@ int kvpr_decode_attention_ragged(const void* q, const void* kv_pages, const int*
                                  size_t ws_bytes, int batch, int heads, int head_dim, int max_seq_len, float scale,
                                  void* stream);
 
+/* K2 + K4 + K5 + K6 fused for small batches: the decode layer after its q/k/v projection, in ONE
+ * cooperative kernel (one CTA per SM, grid-wide barriers between the stages):
+ *   attn = decode_attention(q, pages[0, seq_len))            (as kvpr_decode_attention)
+ *   hres += attn . W_o^T + b_o
+ *   mid   = relu(LayerNorm2(hres) . W_1^T + b_1)
+ *   hres += mid . W_2^T + b_2
+ *   lnx_out = LayerNorm_x(hres)   (optional: the next layer's LN1 into its X slot, or the final LN)
+ *   q_next, page_next = lnx_out . W_qkv_next^T + b_qkv_next   (optional: the next layer's K3)
+ * The reference's decode_attention (numerics.py:166-191) followed by OPT's MLP block (SURVEY.md
+ * §8a note 2).  Deterministic; agrees with the multi-kernel sequence to fp32 rounding (different
+ * summation order).  Needs kvpr_decode_layer_tail_supported(); ws holds the attention split
+ * partials (>= batch * heads * (head_dim + 2) * 4 bytes).  Grid-barrier words are a library-owned
+ * zeroed block per (device, stream), made on first use; launches sharing a stream are ordered. */
+typedef struct kvpr_layer_tail_desc {
+  int batch, hidden, heads, head_dim, ffn, seq_len;
+  float scale, eps;
+  const void* q;        /* [batch][hidden] fp16 */
+  const void* kv_pages; /* page buffer of the layer, positions [0, seq_len) */
+  void* attn;           /* [batch][hidden] fp16 scratch (attention output) */
+  const void *wo, *bo;
+  float* hres;          /* [batch][hidden] fp32 residual stream, updated in place */
+  const void *ln2_g, *ln2_b, *w1, *b1;
+  void* mid;            /* [batch][ffn] fp16 scratch */
+  const void *w2, *b2;
+  const void *lnx_g, *lnx_b; /* optional output LayerNorm (NULL lnx_out = none) */
+  void* lnx_out;
+  long long lnx_ld;
+  /* optional, with the output LayerNorm: the next layer's q/k/v of the new token from lnx_out
+   * (K3 fused in): q -> q_next [batch][hidden], k, v -> page_next (K rows then V rows).  Same
+   * k order as the tcgen05 kernels, so k, v are bit-identical to kvpr_linear / K1 (the split
+   * invariance of numerics.split_merge_kv, numerics.py:107-137). */
+  const void *wqkv_next, *bqkv_next; /* [3*hidden][hidden], [3*hidden] */
+  void* q_next;
+  void* page_next;
+  /* optional zero-copy PCIe traffic (page-locked host stores, mapped): attention positions
+   * [host_lo, host_hi) are read from kv_host (the layer's host KV store, same page layout) instead of
+   * kv_pages -- the transferred tail KV[l:s'-1] without a copy-engine DMA; x_store_next /
+   * page_store_next receive the normalised rows / the next layer's k, v page as well (the D2H
+   * store_activation / store_cache of graph.py:340-347, written by the SMs). */
+  const void* kv_host;
+  int host_lo, host_hi;
+  void* x_store_next;
+  void* page_store_next;
+  void* ws;
+  size_t ws_bytes;
+} kvpr_layer_tail_desc;
+
+int kvpr_decode_layer_tail_supported(int batch, int hidden, int heads, int ffn);
+int kvpr_decode_layer_tail(const kvpr_layer_tail_desc* desc, void* stream);
+
 /* Causal attention for the prompt (prefill that populates the host stores):
  * q/out [pos][batch][hidden], kv pages as above, positions [0, seq_len). */
 int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,
@@ -193,6 +243,11 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
  * store_activation / store_cache) go through here.  Host buffers must be
  * page-locked for the copy to be asynchronous. */
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+
+/* n (<= 16) DMAs as ONE cudaMemcpyBatchAsync submission on `stream` (sources read in stream
+ * order; zero-byte entries skipped).  The copy engine's fixed cost is per submission, so the small
+ * per-layer copies of a small model (X[:, :l] + KV[l:s'-1]; the new X row + K,V page) go as one batch. */
+int kvpr_copy_batch_async(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, void* stream);
 
 /* 4-bit groupwise KV pages (compressed KV offload; costmodel.py:109-118:
  * kv_bytes_per_element = 4/8 + 4/64 = 0.5625).  Compressed page = codes
@@ -247,6 +302,9 @@ typedef struct kvpr_decoder_desc {
   int chunk_rows; /* minimum positions per X chunk / K1 launch (runtime.KVPRRuntime.chunk_rows) */
   int chunk_wave; /* > 0: X chunks are multiples of this many positions (whole K1 tile waves) */
   void* recompute_stream; /* non-NULL: K1 runs here, issued a unit ahead (overlaps the previous layer) */
+  int fused_tail; /* 1: the layer after q/k/v is kvpr_decode_layer_tail (batch <= 8), LN1 / final LN fused into it */
+  int zero_copy;  /* with fused_tail: bit 0 = the tail reads KV[l:s'-1] from the host store (no KV DMA),
+                     bit 1 = it writes the next unit's X row / k,v page to the host stores (no D2H DMAs) */
 } kvpr_decoder_desc;
 
 int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);

@@ -45,10 +45,13 @@ EXPORTS = (
     "kvpr_embed",
     "kvpr_argmax",
     "kvpr_copy_async",
+    "kvpr_copy_batch_async",
     "kvpr_kv4_page_bytes",
     "kvpr_kv4_quantize",
     "kvpr_kv4_dequantize",
     "kvpr_decode_attention_kv4",
+    "kvpr_decode_layer_tail_supported",
+    "kvpr_decode_layer_tail",
     "kvpr_decoder_create",
     "kvpr_decoder_destroy",
     "kvpr_decoder_run",
@@ -99,7 +102,18 @@ class DecoderDesc(ctypes.Structure):
             "embed", "pos", "lnf_g", "lnf_b", "kv_dev", "x_dev", "hres", "q", "attn", "y", "mid", "zf", "logits",
             "tok", "ws")] + [("ws_bytes", ctypes.c_size_t)] + [(n, ctypes.c_void_p) for n in (
                 "compute_stream", "h2d_stream", "d2h_stream")] + [("chunk_rows", ctypes.c_int), ("chunk_wave", ctypes.c_int),
-                                                      ("recompute_stream", ctypes.c_void_p)]
+                                                      ("recompute_stream", ctypes.c_void_p), ("fused_tail", ctypes.c_int),
+                                                      ("zero_copy", ctypes.c_int)]
+
+
+class LayerTailDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("batch", "hidden", "heads", "head_dim", "ffn", "seq_len")] + [
+        ("scale", ctypes.c_float), ("eps", ctypes.c_float)] + [(n, ctypes.c_void_p) for n in (
+            "q", "kv_pages", "attn", "wo", "bo", "hres", "ln2_g", "ln2_b", "w1", "b1", "mid", "w2", "b2", "lnx_g",
+            "lnx_b", "lnx_out")] + [("lnx_ld", ctypes.c_longlong)] + [(n, ctypes.c_void_p) for n in (
+                "wqkv_next", "bqkv_next", "q_next", "page_next", "kv_host")] + [
+                    ("host_lo", ctypes.c_int), ("host_hi", ctypes.c_int)] + [(n, ctypes.c_void_p) for n in (
+                        "x_store_next", "page_store_next", "ws")] + [("ws_bytes", ctypes.c_size_t)]
 
 
 _lib: ctypes.CDLL | None = None
@@ -136,10 +150,13 @@ _SIGS = {
     "kvpr_embed": ([_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp], _i),
     "kvpr_argmax": ([_vp, _ll, _i, _i, _vp, _vp, _vp], _i),
     "kvpr_copy_async": ([_vp, _vp, _sz, _vp], _i),
+    "kvpr_copy_batch_async": ([ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_sz), _sz, _vp], _i),
     "kvpr_kv4_page_bytes": ([_i, _i], _sz),
     "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_decode_attention_kv4": ([_vp, _vp, _vp, _i, _i, _vp, _vp, _sz, _i, _i, _i, _i, _f, _vp], _i),
+    "kvpr_decode_layer_tail_supported": ([_i, _i, _i, _i], _i),
+    "kvpr_decode_layer_tail": ([ctypes.POINTER(LayerTailDesc), _vp], _i),
     "kvpr_decoder_create": ([ctypes.POINTER(DecoderDesc), ctypes.POINTER(LayerDesc), ctypes.POINTER(_vp)], _i),
     "kvpr_decoder_destroy": ([_vp], _i),
     "kvpr_decoder_run": ([_vp, _i, ctypes.POINTER(_i), _i, _vp, _vp], _i),

@@ -66,6 +66,48 @@ int sm_count(int device) {
   return n;
 }
 
+// n DMAs as one cudaMemcpyBatchAsync submission (stream-ordered sources); zero-byte entries dropped.
+// The copy engine's fixed cost is per submission: X[:, :l] + KV[l:s'-1] of a small layer take 35 us
+// batched vs 39 us as two cudaMemcpyAsync (tools/dma_small_probe.py)
+int copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, cudaStream_t stream) {
+  constexpr size_t kMax = 16;
+  void* d[kMax];
+  void* sp[kMax];
+  size_t sz[kMax];
+  size_t m = 0;
+  if (n > kMax) {
+    set_error("copy_batch: at most %zu copies per batch (got %zu)", kMax, n);
+    return KVPR_EINVAL;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    if (sizes[i] == 0) continue;
+    if (dsts[i] == nullptr || srcs[i] == nullptr) {
+      set_error("copy_batch: null pointer in copy %zu", i);
+      return KVPR_EINVAL;
+    }
+    d[m] = dsts[i];
+    sp[m] = const_cast<void*>(srcs[i]);
+    sz[m] = sizes[i];
+    ++m;
+  }
+  if (m == 0) return KVPR_OK;
+  cudaError_t e;
+  if (m == 1) {
+    e = cudaMemcpyAsync(d[0], sp[0], sz[0], cudaMemcpyDefault, stream);
+  } else {
+    cudaMemcpyAttributes attr;
+    memset(&attr, 0, sizeof(attr));
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t idx = 0, fail = 0;
+    e = cudaMemcpyBatchAsync(d, sp, sz, m, &attr, &idx, 1, &fail, stream);
+  }
+  if (e != cudaSuccess) {
+    set_error("copy_batch: %s", cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
 static GemmArgs to_args(const kvpr_epilogue* e) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -91,7 +133,7 @@ extern "C" {
 
 const char* kvpr_last_error(void) { return g_err; }
 
-int kvpr_version(void) { return 1; }
+int kvpr_version(void) { return 2; }
 
 long long kvpr_kernel_launches(void) { return g_kernel_launches.load(std::memory_order_relaxed); }
 
@@ -261,6 +303,19 @@ int kvpr_decode_attention_ragged(const void* q, const void* kv_pages, const int*
                           max_seq_len, scale, static_cast<cudaStream_t>(stream), seq_lens);
 }
 
+int kvpr_decode_layer_tail_supported(int batch, int hidden, int heads, int ffn) {
+  return layer_tail_supported(batch, hidden, heads, ffn) ? 1 : 0;
+}
+
+int kvpr_decode_layer_tail(const kvpr_layer_tail_desc* desc, void* stream) {
+  g_err[0] = 0;
+  if (desc == nullptr) {
+    set_error("decode_layer_tail: null descriptor");
+    return KVPR_EINVAL;
+  }
+  return layer_tail(*desc, static_cast<cudaStream_t>(stream));
+}
+
 int kvpr_decode_attention_kv4(const void* q, const void* kv_pages, const void* qpages, int q_lo, int q_hi, void* out,
                               void* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
                               void* stream) {
@@ -296,6 +351,11 @@ int kvpr_embed(const int* tokens, const void* tok_emb, const void* pos_emb, floa
 int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_idx, float* out_val, void* stream) {
   g_err[0] = 0;
   return argmax_rows(logits, ld, rows, cols, out_idx, out_val, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_copy_batch_async(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, void* stream) {
+  g_err[0] = 0;
+  return copy_batch(dsts, srcs, sizes, n, static_cast<cudaStream_t>(stream));
 }
 
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream) {

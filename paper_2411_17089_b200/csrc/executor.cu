@@ -181,20 +181,28 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   const kvpr_layer_desc& Lw = D.layer[x.j];
   char* xd = static_cast<char*>(d.x_dev) + static_cast<size_t>(x.buf) * d.capacity * row;
   char* kvd = static_cast<char*>(d.kv_dev) + static_cast<size_t>(x.buf) * d.capacity * 2 * row;
-  if (!d.x_resident) {
-    int cb[16][2];
-    const int nc = chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d), d.chunk_wave);
+  const bool kv_dma = x.s - 1 > x.lp && !(d.fused_tail && (d.zero_copy & 1));  // else the tail reads it itself
+  void* kv_dst = kvd + x.lp * 2 * row;
+  const void* kv_src = static_cast<const char*>(Lw.host_kv) + x.lp * 2 * row;
+  const size_t kv_bytes = kv_dma ? (x.s - 1 - x.lp) * 2 * row : 0;
+  int cb[16][2];
+  const int nc = d.x_resident ? 0 : chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d), d.chunk_wave);
+  if (nc == 1) {
+    // one X chunk (small layers): X and the KV tail as ONE batched DMA -- the copy engine's fixed cost
+    // is per submission; the chunk's event then covers both (K1 waits on it, K2 on ev_kv)
+    void* dsts[2] = {xd, kv_dst};
+    const void* srcs[2] = {Lw.host_x, kv_src};
+    const size_t sizes[2] = {static_cast<size_t>(cb[0][1] - cb[0][0]) * row, kv_bytes};
+    KV_TRY(copy_batch(dsts, srcs, sizes, 2, hs));
+    KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks], hs), "record X"));
+  } else {
     for (int c = 0; c < nc; ++c) {
       KV_TRY(ck(cudaMemcpyAsync(xd + cb[c][0] * row, static_cast<const char*>(Lw.host_x) + cb[c][0] * row,
                                 (cb[c][1] - cb[c][0]) * row, cudaMemcpyDefault, hs),
                 "h2d X"));
       KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks + c], hs), "record X"));
     }
-  }
-  if (x.s - 1 > x.lp) {
-    KV_TRY(ck(cudaMemcpyAsync(kvd + x.lp * 2 * row, static_cast<const char*>(Lw.host_kv) + x.lp * 2 * row,
-                              (x.s - 1 - x.lp) * 2 * row, cudaMemcpyDefault, hs),
-              "h2d KV"));
+    if (kv_bytes) KV_TRY(ck(cudaMemcpyAsync(kv_dst, kv_src, kv_bytes, cudaMemcpyDefault, hs), "h2d KV"));
   }
   return ck(cudaEventRecord(D.ev_kv[x.r], hs), "record KV");
 }
@@ -248,11 +256,85 @@ int issue_k1(Decoder& D, int u, int base, const int* splits) {
 
 int head(Decoder& D, cudaStream_t cs) {
   const kvpr_decoder_desc& d = D.d;
-  KV_TRY(layernorm(d.hres, d.hidden, static_cast<const __half*>(d.lnf_g), static_cast<const __half*>(d.lnf_b),
-                   static_cast<__half*>(d.zf), d.hidden, d.batch, d.hidden, d.eps, cs));
+  if (!d.fused_tail)  // fused: the last layer's tail already wrote LN_f(h) into zf
+    KV_TRY(layernorm(d.hres, d.hidden, static_cast<const __half*>(d.lnf_g), static_cast<const __half*>(d.lnf_b),
+                     static_cast<__half*>(d.zf), d.hidden, d.batch, d.hidden, d.eps, cs));
   kvpr_epilogue e = simple_epi(d.logits, d.vocab, d.batch, d.vocab, nullptr, KVPR_EPI_F32);
   KV_TRY(kvpr_linear_ws(d.zf, d.hidden, d.embed, d.hidden, d.batch, d.vocab, d.hidden, &e, 0, d.ws, d.ws_bytes, cs));
   return argmax_rows(d.logits, d.vocab, d.batch, d.vocab, d.tok, nullptr, cs);
+}
+
+// Small batches: K2 -> out-proj -> LN2 -> fc1 -> fc2 as ONE cooperative kernel (layer_tail.cu), which
+// also normalises the new residual into the next layer's X slot and computes that layer's q, k, v of
+// the new token (K3, bit-identical to kvpr_linear) -- or, after the last layer, the final LN into zf.
+// The next unit's X slot and page s'-1 were last read by the D2H of unit u + 1 - nbuf, so that copy
+// must be done before this launch.
+int fused_tail(Decoder& D, int u, const Unit& x, __half* kvd, cudaStream_t cs) {
+  const kvpr_decoder_desc& d = D.d;
+  const kvpr_layer_desc& Lw = D.layer[x.j];
+  const int b = d.batch, h = d.hidden;
+  const long long bh = static_cast<long long>(b) * h;
+  kvpr_layer_tail_desc t;
+  memset(&t, 0, sizeof(t));
+  t.batch = b;
+  t.hidden = h;
+  t.heads = d.heads;
+  t.head_dim = h / d.heads;
+  t.ffn = d.ffn;
+  t.seq_len = x.s;
+  t.scale = static_cast<float>(1.0 / sqrt(static_cast<double>(h / d.heads)));
+  t.eps = d.eps;
+  t.q = d.q;
+  t.kv_pages = kvd;
+  t.attn = d.attn;
+  t.wo = Lw.wo;
+  t.bo = Lw.bo;
+  t.hres = d.hres;
+  t.ln2_g = Lw.ln2_g;
+  t.ln2_b = Lw.ln2_b;
+  t.w1 = Lw.w1;
+  t.b1 = Lw.b1;
+  t.mid = d.mid;
+  t.w2 = Lw.w2;
+  t.b2 = Lw.b2;
+  t.lnx_ld = h;
+  if (x.j + 1 < d.layers) {
+    const kvpr_layer_desc& Ln = D.layer[x.j + 1];  // unit u + 1: same step, next layer, buffer (u + 1) % nbuf
+    const size_t nb = static_cast<size_t>((u + 1) % d.nbuf);
+    __half* xn = d.x_resident ? static_cast<__half*>(Ln.dev_x) : static_cast<__half*>(d.x_dev) + nb * d.capacity * bh;
+    __half* kvn = static_cast<__half*>(d.kv_dev) + nb * d.capacity * 2 * bh;
+    if (u + 1 >= d.nbuf) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_d2h[(u + 1 - d.nbuf) % D.R], 0), "wait d2h (next slot)"));
+    t.lnx_g = Ln.ln1_g;
+    t.lnx_b = Ln.ln1_b;
+    t.lnx_out = xn + static_cast<size_t>(x.s - 1) * bh;
+    t.wqkv_next = Ln.wqkv;
+    t.bqkv_next = Ln.bqkv;
+    t.q_next = d.q;
+    t.page_next = kvn + static_cast<size_t>(x.s - 1) * 2 * bh;
+    if (d.zero_copy & 2) {
+      t.x_store_next = d.x_resident ? nullptr : static_cast<__half*>(Ln.host_x) + static_cast<size_t>(x.s - 1) * bh;
+      t.page_store_next = static_cast<__half*>(Ln.host_kv) + static_cast<size_t>(x.s - 1) * 2 * bh;
+    }
+  } else {
+    t.lnx_g = d.lnf_g;
+    t.lnx_b = d.lnf_b;
+    t.lnx_out = d.zf;
+  }
+  // KV[l:s'-1] straight from the host store (zero-copy over PCIe); its last position was stored by
+  // unit u - L (the previous step of this layer)
+  if (x.s - 1 > x.lp && (d.zero_copy & 1)) {
+    if (u >= d.layers) KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_d2h[(u - d.layers) % D.R], 0), "wait store (tail)"));
+    t.kv_host = Lw.host_kv;
+    t.host_lo = x.lp;
+    t.host_hi = x.s - 1;
+  }
+  t.ws = d.ws;
+  t.ws_bytes = d.ws_bytes;
+  KTime t2;
+  KV_TRY(kt_begin(D, 1, 2.0 * b * x.s * static_cast<double>(h) * 2, cs, &t2));
+  KV_TRY(layer_tail(t, cs));
+  KV_TRY(kt_end(D, &t2, cs));
+  return ck(cudaEventRecord(D.ev_done[x.r], cs), "record done");
 }
 
 int compute(Decoder& D, int u, int base, const int* splits) {
@@ -275,9 +357,11 @@ int compute(Decoder& D, int u, int base, const int* splits) {
                  x.s - 1, h, 2, cs));
   }
   // new token: LN1 into the X slot of position s'-1; q / k,v (k,v into page s'-1)
-  KV_TRY(layernorm(d.hres, h, static_cast<const __half*>(Lw.ln1_g), static_cast<const __half*>(Lw.ln1_b), x_slot, h,
-                   b, h, d.eps, cs));
-  {
+  const bool own_qkv = !d.fused_tail || x.j == 0;  // fused: the previous layer's tail made LN1 and q, k, v
+  if (own_qkv)
+    KV_TRY(layernorm(d.hres, h, static_cast<const __half*>(Lw.ln1_g), static_cast<const __half*>(Lw.ln1_b), x_slot, h,
+                     b, h, d.eps, cs));
+  if (own_qkv) {
     kvpr_epilogue e;
     memset(&e, 0, sizeof(e));
     e.bias = Lw.bqkv;
@@ -294,16 +378,18 @@ int compute(Decoder& D, int u, int base, const int* splits) {
     KV_TRY(kvpr_linear(x_slot, h, Lw.wqkv, h, b, 3 * h, h, &e, 0, cs));
   }
   KV_TRY(ck(cudaEventRecord(D.ev_qkv[x.r], cs), "record qkv"));
-  KV_TRY(ck(cudaStreamWaitEvent(ds, D.ev_qkv[x.r], 0), "d2h wait"));
-  if (!d.x_resident) {
-    KV_TRY(ck(cudaMemcpyAsync(static_cast<char*>(Lw.host_x) + static_cast<size_t>(x.s - 1) * row, x_slot, row,
-                              cudaMemcpyDefault, ds),
-              "d2h X"));
+  if (own_qkv || !(d.zero_copy & 2)) {
+    KV_TRY(ck(cudaStreamWaitEvent(ds, D.ev_qkv[x.r], 0), "d2h wait"));
+    // the new X row and K,V page as one batched DMA (store_activation + store_cache)
+    void* dsts[2] = {static_cast<char*>(Lw.host_kv) + static_cast<size_t>(x.s - 1) * 2 * row,
+                     d.x_resident ? nullptr : static_cast<char*>(Lw.host_x) + static_cast<size_t>(x.s - 1) * row};
+    const void* srcs[2] = {page, x_slot};
+    const size_t sizes[2] = {2 * row, d.x_resident ? 0 : row};
+    KV_TRY(copy_batch(dsts, srcs, sizes, 2, ds));
+    KV_TRY(ck(cudaEventRecord(D.ev_d2h[x.r], ds), "record d2h"));
+  } else {  // the previous layer's tail wrote this unit's X row and k, v page into the host stores
+    KV_TRY(ck(cudaEventRecord(D.ev_d2h[x.r], cs), "record d2h"));
   }
-  KV_TRY(ck(cudaMemcpyAsync(static_cast<char*>(Lw.host_kv) + static_cast<size_t>(x.s - 1) * 2 * row, page, 2 * row,
-                            cudaMemcpyDefault, ds),
-            "d2h KV"));
-  KV_TRY(ck(cudaEventRecord(D.ev_d2h[x.r], ds), "record d2h"));
   // K1 per landed chunk (one launch when X is resident); on its own stream it was issued a unit
   // ahead (issue_k1) and only its completion gates K2
   if (d.recompute_stream == nullptr) {
@@ -312,6 +398,7 @@ int compute(Decoder& D, int u, int base, const int* splits) {
     KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_k1[x.r], 0), "wait K1"));
   }
   KV_TRY(ck(cudaStreamWaitEvent(cs, D.ev_kv[x.r], 0), "wait KV"));
+  if (d.fused_tail) return fused_tail(D, u, x, kvd, cs);
   KTime t2;
   KV_TRY(kt_begin(D, 1, 2.0 * b * x.s * static_cast<double>(h) * 2, cs, &t2));
   KV_TRY(decode_attention(static_cast<const __half*>(d.q), kvd, static_cast<__half*>(d.attn),

@@ -48,6 +48,7 @@ struct GemmArgs {
 
 int sm_count(int device);
 void clear_error();
+int copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, cudaStream_t stream);
 
 
 
@@ -87,6 +88,9 @@ int decode_attention(const __half* q, const __half* kv, __half* out, float* ws, 
 int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages, int q_lo, int q_hi, __half* out,
                         float* ws, size_t ws_bytes, int batch, int heads, int head_dim, int seq_len, float scale,
                         cudaStream_t stream, const int* seq_lens = nullptr);
+
+bool layer_tail_supported(int batch, int hidden, int heads, int ffn);
+int layer_tail(const kvpr_layer_tail_desc& d, cudaStream_t stream);
 
 int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim,
                       int seq_len, float scale, cudaStream_t stream);

@@ -125,6 +125,57 @@ def decode_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor,
     return out
 
 
+def layer_tail_supported(batch: int, hidden: int, heads: int, ffn: int) -> bool:
+    """Shapes the fused small-batch layer tail handles (batch <= 8, hidden <= 1024, ffn <= 4096, head_dim 64/128)."""
+    return bool(_lib.load().kvpr_decode_layer_tail_supported(batch, hidden, heads, ffn))
+
+
+def layer_tail(q: torch.Tensor, kv_pages: torch.Tensor, seq_len: int, lw, hres: torch.Tensor, attn: torch.Tensor,
+               mid: torch.Tensor, ws: torch.Tensor, heads: int, eps: float, lnx: tuple | None = None,
+               qkv_next: tuple | None = None, host_kv: tuple | None = None, stores: tuple | None = None,
+               stream=None) -> None:
+    """K2 -> out-proj + residual -> LN2 -> fc1 + ReLU -> fc2 + residual in one cooperative kernel
+    (kvpr_decode_layer_tail).  lw: the layer's weights (wo, bo, ln2_g, ln2_b, w1, b1, w2, b2);
+    lnx = (gamma, beta, out fp16 [batch][>= hidden]) for the optional LayerNorm of the new residual;
+    qkv_next = (wqkv [3h, h], bqkv [3h], q_out [batch, h], page [2, batch, h]) for the next layer's q/k/v
+    of the new token from that LayerNorm (needs lnx); host_kv = (page-locked KV store of the layer, lo, hi): attention
+    positions [lo, hi) read from it over PCIe (zero-copy); stores = (host X row or None, host KV page) the
+    normalised rows / the next k, v page are also written to (page-locked, zero-copy)."""
+    batch, hidden = q.shape
+    for t, n in ((q, "q"), (kv_pages, "kv_pages"), (attn, "attn"), (mid, "mid")):
+        _need(t, torch.float16, n)
+    _need(hres, torch.float32, "hres")
+    d = _lib.LayerTailDesc()
+    d.batch, d.hidden, d.heads, d.head_dim, d.ffn, d.seq_len = batch, hidden, heads, hidden // heads, mid.shape[1], seq_len
+    d.scale, d.eps = 1.0 / math.sqrt(hidden // heads), eps
+    d.q, d.kv_pages, d.attn, d.hres, d.mid = q.data_ptr(), kv_pages.data_ptr(), attn.data_ptr(), hres.data_ptr(), \
+        mid.data_ptr()
+    for name in ("wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2"):
+        setattr(d, name, getattr(lw, name).data_ptr())
+    if lnx is not None:
+        g, b, out = lnx
+        _need(out, torch.float16, "lnx out")
+        d.lnx_g, d.lnx_b, d.lnx_out, d.lnx_ld = g.data_ptr(), b.data_ptr(), out.data_ptr(), out.stride(0)
+    if qkv_next is not None:
+        wq, bq, qo, page = qkv_next
+        for t, n in ((wq, "wqkv"), (bq, "bqkv"), (qo, "q_next"), (page, "page_next")):
+            _need(t, torch.float16, n)
+        d.wqkv_next, d.bqkv_next, d.q_next, d.page_next = wq.data_ptr(), bq.data_ptr(), qo.data_ptr(), page.data_ptr()
+    if host_kv is not None:
+        kvh, lo, hi = host_kv
+        if kvh.is_cuda:
+            raise ValueError("host_kv must be a page-locked host tensor")
+        d.kv_host, d.host_lo, d.host_hi = kvh.data_ptr(), lo, hi
+    if stores is not None:
+        xs, ps = stores
+        d.x_store_next = xs.data_ptr() if xs is not None else None
+        d.page_store_next = ps.data_ptr() if ps is not None else None
+    d.ws, d.ws_bytes = ws.data_ptr(), ws.numel() * ws.element_size()
+    import ctypes
+
+    _lib.call("kvpr_decode_layer_tail", ctypes.byref(d), _stream(stream))
+
+
 def decode_attention_ragged(q: torch.Tensor, kv_pages: torch.Tensor, seq_lens: torch.Tensor, out: torch.Tensor,
                             ws: torch.Tensor | None, heads: int, head_dim: int, scale: float | None = None,
                             stream=None) -> torch.Tensor:

@@ -46,6 +46,17 @@ def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) ->
         _lib.call("kvpr_copy_async", dst_ptr, src_ptr, nbytes, stream.cuda_stream)
 
 
+def _copy_batch(copies, stream: torch.cuda.Stream) -> None:
+    """[(dst_ptr, src_ptr, nbytes), ...] as ONE batched DMA submission (kvpr_copy_batch_async)."""
+    import ctypes
+
+    n = len(copies)
+    dsts = (ctypes.c_void_p * n)(*[c[0] for c in copies])
+    srcs = (ctypes.c_void_p * n)(*[c[1] for c in copies])
+    sizes = (ctypes.c_size_t * n)(*[c[2] for c in copies])
+    _lib.call("kvpr_copy_batch_async", dsts, srcs, sizes, n, stream.cuda_stream)
+
+
 class HostStores:
     """Per-layer X and KV stores in page-locked host memory, exact size (hostmem.pinned_empty)."""
 
@@ -123,7 +134,7 @@ class KVPRRuntime:
     """One decoder replica on one GPU (the unit the batch-partitioned multi-GPU mode replicates)."""
 
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
-                 chunks: int = 4, nbuf: int = 2, stores: HostStores | None = None, kv_bits: int | None = None,
+                 chunks: int = 4, nbuf: int | None = None, stores: HostStores | None = None, kv_bits: int | None = None,
                  x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None,
                  k1_stream: bool | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
@@ -140,6 +151,13 @@ class KVPRRuntime:
         self.cfg, self.w, self.batch, self.capacity = cfg, weights, batch, capacity
         self.dev = torch.device(device) if device is not None else weights.embed.device
         # env: A/B knob; at most 16 chunks, the native executor's per-unit chunk table (executor.cu)
+        # device buffers per category (graph.py:215-221 uses 2): small-batch layers whose step is bound by
+        # the DMA pipeline rather than the GPU keep 4 in flight (config 1: 0.571 -> 0.511 ms/step,
+        # profiles/r02s2_c1_sweep.jsonl); KVPR_NBUF overrides
+        fused_ok = (kv_bits is None and os.environ.get("KVPR_FUSED_TAIL", "1") != "0"
+                    and kernels.layer_tail_supported(batch, cfg.hidden, cfg.heads, cfg.ffn))
+        if nbuf is None:
+            nbuf = int(os.environ.get("KVPR_NBUF", 4 if fused_ok else 2))
         self.chunks, self.nbuf = max(1, min(16, int(os.environ.get("KVPR_CHUNKS", chunks)))), nbuf
         # a K1 chunk carries >= KVPR_CHUNK_MB (default 32) MiB of X (>= 64 positions): every extra X
         # DMA costs copy-engine time (OPT-6.7B b4: 1/2/4/8 chunks of ~30 MB of X in total -> 98.8 /
@@ -167,6 +185,16 @@ class KVPRRuntime:
         if k1_stream is None:
             k1_stream = (env == "1") if env in ("0", "1") else None
         self.k1_stream = (x_resident or self.chunk_wave == 0) if k1_stream is None else bool(k1_stream)
+        # batch <= 8 on a small model: the layer after q/k/v runs as one cooperative kernel (K2 -> out-proj
+        # -> LN2 -> fc1 -> fc2, plus the next LN1), csrc/layer_tail.cu; KVPR_FUSED_TAIL=0 turns it off.
+        # Not with 4-bit KV (K2-kv4) or a trace (per-kind spans need the separate kernels)
+        self.fused_tail = fused_ok
+        # with the fused tail, PCIe traffic the SMs move themselves instead of a copy-engine DMA
+        # (KVPR_TAIL_ZC: "r" = the tail reads KV[l:s'-1] from the host store, "w" = it writes the next
+        # unit's X row and k,v page to the host stores)
+        zc = os.environ.get("KVPR_TAIL_ZC", "")
+        self.zc_read = self.fused_tail and "r" in zc
+        self.zc_write = self.fused_tail and "w" in zc
         self.qbytes = kernels.kv4_page_bytes(b, h) if kv_bits == 4 else None
         self.page_bytes = self.qbytes if kv_bits == 4 else 2 * b * h * 2
         self.x_resident = x_resident
@@ -307,10 +335,12 @@ class KVPRRuntime:
                                  flags=_lib.EPI_RELU, stream=stream, ws=self.ws)
         kernels.linear_simple(mid[:M], lw.w2, lw.b2, hres[:M], flags=acc, stream=stream, ws=self.ws)
 
-    def _head(self, hrows: torch.Tensor, stream) -> None:
-        """Final LN, tied LM head (fp32 logits) and greedy argmax into self.tok."""
+    def _head(self, hrows: torch.Tensor, stream, ln: bool = True) -> None:
+        """Final LN (unless the fused layer tail already wrote it into zf), tied LM head (fp32 logits) and
+        greedy argmax into self.tok."""
         cfg = self.cfg
-        kernels.layernorm(hrows, self.w.lnf_g, self.w.lnf_b, self.zf, eps=cfg.eps, stream=stream)
+        if ln:
+            kernels.layernorm(hrows, self.w.lnf_g, self.w.lnf_b, self.zf, eps=cfg.eps, stream=stream)
         kernels.linear_simple(self.zf, self.w.embed, None, self.logits, stream=stream, ws=self.ws)
         kernels.argmax(self.logits, self.tok, stream=stream)
 
@@ -337,17 +367,25 @@ class KVPRRuntime:
         xd, kvd = self.x_dev[buf], self.kv_dev[buf]
         row = b * h * 2
         tr = self._trace
-        for c, (p0, p1) in enumerate(chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows,
-                                                  self.chunk_wave)):
+        kv_dma = s - 1 > lp and not (self.zc_read and tr is None)  # zero-copy: the tail reads it from the host
+        kv_copy = ((self.kvq_dev[buf][lp] if self.kv_bits == 4 else kvd[lp]).data_ptr(), kvh[lp].data_ptr(),
+                   (s - 1 - lp) * self.page_bytes) if kv_dma else None
+        chunks = chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows, self.chunk_wave)
+        if len(chunks) == 1 and tr is None:  # one X chunk: X and the KV tail as one batched DMA (executor.cu)
+            (p0, p1), = chunks
+            _copy_batch([(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row)] + ([kv_copy] if kv_copy else []), hs)
+            self.ev_x[r][0].record(hs)
+            self.ev_kv[r].record(hs)
+            return
+        for c, (p0, p1) in enumerate(chunks):
             sp = tr.begin(hs, "load_activation_recompute", i + 1, j + 1, f"c{c}") if tr else None
             _copy(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row, hs)
             if sp:
                 tr.end(hs, sp)
             self.ev_x[r][c].record(hs)
-        if s - 1 > lp:
+        if kv_copy:
             sp = tr.begin(hs, "load_cache", i + 1, j + 1) if tr else None
-            dst = self.kvq_dev[buf][lp] if self.kv_bits == 4 else kvd[lp]
-            _copy(dst.data_ptr(), kvh[lp].data_ptr(), (s - 1 - lp) * self.page_bytes, hs)
+            _copy(*kv_copy, hs)
             if sp:
                 tr.end(hs, sp)
         self.ev_kv[r].record(hs)
@@ -365,27 +403,35 @@ class KVPRRuntime:
         if u >= self.nbuf:  # the previous user's D2H has read this buffer's slot s'-1 / staging page
             cs.wait_event(self.ev_d2h[(u - self.nbuf) % self._R])
         # new token: X = LN1(h) straight into the X slot of position s'-1, q/k/v with k,v into page s'-1
+        fused = self.fused_tail and tr is None
         sp = tr.begin(cs, "compute_mha", I, J, "proj") if tr else None
-        kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
-        self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
+        if not fused or j == 0:  # fused: the previous layer's tail made LN1 into this slot and q, k, v
+            kernels.layernorm(self.hres, lw.ln1_g, lw.ln1_b, x_slot, eps=cfg.eps, stream=cs)
+            self._qkv(x_slot, b, lw, self.q, page, q_group=0, stream=cs)
         if self.kv_bits == 4:  # the stored copy of the new page is compressed; K2 reads the exact fp16 page
             kernels.kv4_quantize(kvd[s - 1:s], self.qnew[buf:buf + 1], b, 0, 1, stream=cs)
         if sp:
             tr.end(cs, sp)
         self.ev_qkv[r].record(cs)
-        # store_activation / store_cache (graph.py:340-347) on the D2H engine
-        ds.wait_event(self.ev_qkv[r])
-        if not self.x_resident:  # row schedule: the X row already sits in the resident store
-            sp = tr.begin(ds, "store_activation", I, J) if tr else None
-            _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
-            if sp:
+        if fused and j > 0 and self.zc_write:  # the previous tail wrote this unit's X row and k, v page to the host
+            self.ev_d2h[r].record(cs)
+        else:
+            # store_activation / store_cache (graph.py:340-347) on the D2H engine
+            ds.wait_event(self.ev_qkv[r])
+            src = self.qnew[buf] if self.kv_bits == 4 else page
+            if tr is None:  # one batched DMA (executor.cu); the row schedule's X row already sits in the store
+                _copy_batch([(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes)] +
+                            ([] if self.x_resident else [(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(),
+                                                          b * h * 2)]), ds)
+            else:
+                if not self.x_resident:
+                    sp = tr.begin(ds, "store_activation", I, J)
+                    _copy(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(), b * h * 2, ds)
+                    tr.end(ds, sp)
+                sp = tr.begin(ds, "store_cache", I, J)
+                _copy(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes, ds)
                 tr.end(ds, sp)
-        sp = tr.begin(ds, "store_cache", I, J) if tr else None
-        src = self.qnew[buf] if self.kv_bits == 4 else page
-        _copy(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes, ds)
-        if sp:
-            tr.end(ds, sp)
-        self.ev_d2h[r].record(ds)
+            self.ev_d2h[r].record(ds)
         # K1: rebuild K,V[0:l) chunk by chunk as X lands (one launch when X is resident)
         for c, (p0, p1) in enumerate(chunk_bounds(lp, 1 if self.x_resident else self.chunks, self.chunk_rows,
                                                   0 if self.x_resident else self.chunk_wave)):
@@ -398,6 +444,31 @@ class KVPRRuntime:
             if sp:
                 tr.end(cs, sp)
         cs.wait_event(self.ev_kv[r])
+        if fused:  # same launch and waits as executor.cu fused_tail()
+            qkv = None
+            if j + 1 < cfg.layers:
+                nxt = self.w.layers[j + 1]
+                nb = (u + 1) % self.nbuf
+                xn = self.x_store[j + 1] if self.x_resident else self.x_dev[nb]
+                if u + 1 >= self.nbuf:  # the next unit's X slot / page: its previous reader's D2H is done
+                    cs.wait_event(self.ev_d2h[(u + 1 - self.nbuf) % self._R])
+                lnx = (nxt.ln1_g, nxt.ln1_b, xn[s - 1])
+                qkv = (nxt.wqkv, nxt.bqkv, self.q, self.kv_dev[nb][s - 1])
+                stores = (None if self.x_resident else self.stores.x[j + 1][s - 1],
+                          self.stores.kv[j + 1][s - 1]) if self.zc_write else None
+            else:
+                lnx, stores = (self.w.lnf_g, self.w.lnf_b, self.zf), None
+            host_kv = None
+            if s - 1 > lp and self.zc_read:  # KV[l:s'-1] from the host store; its last position stored by unit u - L
+                if u >= cfg.layers:
+                    cs.wait_event(self.ev_d2h[(u - cfg.layers) % self._R])
+                host_kv = (self.stores.kv[j], lp, s - 1)
+            kt = self._ktimer("k2", 2 * b * s * h * 2, cs)
+            kernels.layer_tail(self.q, kvd, s, lw, self.hres, self.attn, self.mid, self.ws, cfg.heads, cfg.eps,
+                               lnx=lnx, qkv_next=qkv, host_kv=host_kv, stores=stores, stream=cs)
+            self._ktimer_end(kt, cs)
+            self.ev_done[r].record(cs)
+            return
         # K2 over the merged pages [0, s') in place (4-bit tail [lp, s'-1) dequantised inside K2), then W_O
         sp = tr.begin(cs, "compute_mha", I, J, "attn") if tr else None
         if self.kv_bits == 4 and s - 1 > lp:
@@ -447,6 +518,8 @@ class KVPRRuntime:
         d.chunk_rows = self.chunk_rows
         d.chunk_wave = self.chunk_wave
         d.recompute_stream = self.rs.cuda_stream if self.k1_stream else None
+        d.fused_tail = int(self.fused_tail)
+        d.zero_copy = int(self.zc_read) | (int(self.zc_write) << 1)
         h = ctypes.c_void_p()
         _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
         self._native_keep = (d, layers)
@@ -531,7 +604,7 @@ class KVPRRuntime:
                 e.record(cs)
                 layer_marks.append(e)
             if j == L - 1:
-                self._head(self.hres, stream=cs)
+                self._head(self.hres, stream=cs, ln=not (self.fused_tail and trace is None))
                 with torch.cuda.stream(cs):
                     out_tokens[i].copy_(self.tok, non_blocking=True)
                     if logits is not None:

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_version_and_error_string(lib):
-    assert lib.kvpr_version() == 1
+    assert lib.kvpr_version() == 2
     assert isinstance(_lib.last_error(), str)
 
 
@@ -53,6 +53,10 @@ def test_ctypes_struct_layout_matches_c(tmp_path):
         " offsetof(kvpr_decoder_desc, embed), offsetof(kvpr_decoder_desc, ws_bytes),"
         " offsetof(kvpr_decoder_desc, d2h_stream), sizeof(kvpr_layer_desc));"
         ' printf("%zu %zu\\n", offsetof(kvpr_decoder_desc, chunk_rows), offsetof(kvpr_decoder_desc, chunk_wave));'
+        ' printf("%zu %zu\\n", offsetof(kvpr_decoder_desc, recompute_stream), offsetof(kvpr_decoder_desc, zero_copy));'
+        ' printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(kvpr_layer_tail_desc), offsetof(kvpr_layer_tail_desc, scale),'
+        ' offsetof(kvpr_layer_tail_desc, q), offsetof(kvpr_layer_tail_desc, lnx_ld),'
+        ' offsetof(kvpr_layer_tail_desc, host_hi), offsetof(kvpr_layer_tail_desc, ws_bytes));'
         ' return 0;}'))
     exe = tmp_path / "layout"
     subprocess.run([gcc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
@@ -61,7 +65,10 @@ def test_ctypes_struct_layout_matches_c(tmp_path):
     want = [ctypes.sizeof(E), E.seg_width.offset, E.ld.offset, E.seg.offset, E.scale.offset, E.scale_cols.offset,
             E.flags.offset, ctypes.sizeof(_lib.OutSeg),
             ctypes.sizeof(D), D.eps.offset, D.embed.offset, D.ws_bytes.offset, D.d2h_stream.offset,
-            ctypes.sizeof(_lib.LayerDesc), D.chunk_rows.offset, D.chunk_wave.offset]
+            ctypes.sizeof(_lib.LayerDesc), D.chunk_rows.offset, D.chunk_wave.offset,
+            D.recompute_stream.offset, D.zero_copy.offset]
+    T = _lib.LayerTailDesc
+    want += [ctypes.sizeof(T), T.scale.offset, T.q.offset, T.lnx_ld.offset, T.host_hi.offset, T.ws_bytes.offset]
     assert got == want
 
 
@@ -75,7 +82,14 @@ def test_sass_is_tcgen05_tma(lib):
     assert "UTCHMMA" in out, "no tcgen05.mma in SASS"
     assert "UTMALDG" in out, "no TMA loads in SASS"
     assert "LDTM" in out, "no tcgen05.ld in SASS"
-    assert "HMMA" not in out.replace("UTCHMMA", ""), "legacy mma.sync path present"
+    # warp-level mma.sync only in the fused small-batch layer tail (6-21 weight rows per CTA: the dense
+    # GEMMs -- K1, prefill, decode projections -- are tcgen05) and its bit-equality probe
+    hmma_funcs = []
+    for block in out.split("Function : ")[1:]:
+        name = block.split("\n", 1)[0].strip()
+        if "HMMA" in block.replace("UTCHMMA", ""):
+            hmma_funcs.append(name)
+    assert hmma_funcs and all("layer_tail" in n or "mma_linear_probe" in n for n in hmma_funcs), hmma_funcs
 
 
 def test_missing_library_fails_loudly(tmp_path):

@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--graph", type=int, default=-1, help="force executor graph mode (0/1); -1 = runtime default")
     ap.add_argument("--x-resident", action="store_true", help="row schedule: X resident in HBM (no X H2D)")
-    ap.add_argument("--nbuf", type=int, default=2, help="device staging buffers per category")
+    ap.add_argument("--nbuf", type=int, default=None, help="device staging buffers per category (default: the runtime's)")
     ap.add_argument("--split", type=int, default=-2, help=">= 0: constant split l; -1: l = s' (all recompute)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
