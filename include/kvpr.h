@@ -244,9 +244,9 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
  * page-locked for the copy to be asynchronous. */
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
-/* n (<= 16) DMAs as ONE cudaMemcpyBatchAsync submission on `stream` (sources read in stream
- * order; zero-byte entries skipped).  The copy engine's fixed cost is per submission, so the small
- * per-layer copies of a small model (X[:, :l] + KV[l:s'-1]; the new X row + K,V page) go as one batch. */
+/* n (<= 16) DMAs enqueued in order on `stream`, one cudaMemcpyAsync each (zero-byte entries
+ * skipped): the per-layer copies of a small model (X[:, :l] + KV[l:s'-1]; the new X row + K,V page)
+ * in one C call. */
 int kvpr_copy_batch_async(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, void* stream);
 
 /* 4-bit groupwise KV pages (compressed KV offload; costmodel.py:109-118:

@@ -66,44 +66,28 @@ int sm_count(int device) {
   return n;
 }
 
-// n DMAs as one cudaMemcpyBatchAsync submission (stream-ordered sources); zero-byte entries dropped.
-// The copy engine's fixed cost is per submission: X[:, :l] + KV[l:s'-1] of a small layer take 35 us
-// batched vs 39 us as two cudaMemcpyAsync (tools/dma_small_probe.py)
+// n DMAs on one stream, one cudaMemcpyAsync each, in order; zero-byte entries dropped.  (The driver's
+// batched-copy submission was measured 4 us faster per small layer, tools/dma_small_probe.py, but
+// faulted the GPU on this pool, so every copy is its own submission.)
 int copy_batch(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, cudaStream_t stream) {
   constexpr size_t kMax = 16;
-  void* d[kMax];
-  void* sp[kMax];
-  size_t sz[kMax];
-  size_t m = 0;
   if (n > kMax) {
     set_error("copy_batch: at most %zu copies per batch (got %zu)", kMax, n);
     return KVPR_EINVAL;
   }
   for (size_t i = 0; i < n; ++i) {
-    if (sizes[i] == 0) continue;
-    if (dsts[i] == nullptr || srcs[i] == nullptr) {
+    if (sizes[i] != 0 && (dsts[i] == nullptr || srcs[i] == nullptr)) {
       set_error("copy_batch: null pointer in copy %zu", i);
       return KVPR_EINVAL;
     }
-    d[m] = dsts[i];
-    sp[m] = const_cast<void*>(srcs[i]);
-    sz[m] = sizes[i];
-    ++m;
   }
-  if (m == 0) return KVPR_OK;
-  cudaError_t e;
-  if (m == 1) {
-    e = cudaMemcpyAsync(d[0], sp[0], sz[0], cudaMemcpyDefault, stream);
-  } else {
-    cudaMemcpyAttributes attr;
-    memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t idx = 0, fail = 0;
-    e = cudaMemcpyBatchAsync(d, sp, sz, m, &attr, &idx, 1, &fail, stream);
-  }
-  if (e != cudaSuccess) {
-    set_error("copy_batch: %s", cudaGetErrorString(e));
-    return KVPR_ECUDA;
+  for (size_t i = 0; i < n; ++i) {
+    if (sizes[i] == 0) continue;
+    const cudaError_t e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream);
+    if (e != cudaSuccess) {
+      set_error("copy_batch: %s", cudaGetErrorString(e));
+      return KVPR_ECUDA;
+    }
   }
   return KVPR_OK;
 }

@@ -1,6 +1,5 @@
 // K2: split-KV decode attention over the merged (recomputed + transferred)
-// KV pages, read in place; plus the causal prefill attention that fills the
-// host stores.
+// KV pages, read in place (the causal prefill attention is prefill_attn.cu).
 //
 // Reference semantics: numerics.decode_attention (numerics.py:166-191) —
 // per head, softmax(K q / sqrt(d)) V with the max-subtracted softmax of
@@ -178,37 +177,6 @@ __global__ void decode_attn_combine_kernel(const float* __restrict__ ws, __half*
   out[(long long)b * heads * D + hd * D + dd] = __float2half_rn(a / l);
 }
 
-// Causal prefill: grid (batch*heads, ceil(seq/4)), block 128: one warp per query position.
-template <int D>
-__global__ void __launch_bounds__(128) prefill_attn_kernel(const __half* __restrict__ q, const __half* __restrict__ kv,
-                                                           __half* __restrict__ out, int batch, int heads, int seq_len,
-                                                           float qscale) {
-  constexpr int LPP = D / 8;
-  constexpr int PPW = 32 / LPP;
-  const int bh = blockIdx.x;
-  const int b = bh / heads, hd = bh % heads;
-  const int hidden = heads * D;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qpos = blockIdx.y * 4 + warp;
-  if (qpos >= seq_len) return;
-  const int glane = lane % LPP, grp = lane / LPP;
-  const long long row = (long long)qpos * batch + b;
-  float q8[8];
-  load8(q + row * hidden + hd * D + glane * 8, q8);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) q8[i] *= qscale;
-  Softmax8 st;
-  st.init();
-  sweep<D, 2>(kv + (long long)b * hidden + hd * D, 2LL * batch * hidden, (long long)batch * hidden, 0, qpos + 1, PPW,
-              grp, q8, glane, st);
-  merge_in_warp<LPP>(st);
-  if (lane < LPP) {
-    __half* o = out + row * hidden + hd * D + glane * 8;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = __float2half_rn(st.acc[i] / st.l);
-  }
-}
-
 // (bh, splits) grid in clusters of (1, splits): one cluster per (sequence, head), PDL-chained
 template <typename... KArgs, typename... Args>
 int launch_cluster(void (*kern)(KArgs...), dim3 grid, int splits, cudaStream_t s, Args... args) {
@@ -340,22 +308,6 @@ int decode_attention_q4(const __half* q, const __half* kv, const uint8_t* qpages
   if (head_dim == 128)
     return launch("decode_attention_combine", decode_attn_combine_kernel<128>, bh, 128, 0, stream, ws, out, heads, splits);
   return launch("decode_attention_combine", decode_attn_combine_kernel<64>, bh, 64, 0, stream, ws, out, heads, splits);
-}
-
-int prefill_attention(const __half* q, const __half* kv, __half* out, int batch, int heads, int head_dim, int seq_len,
-                      float scale, cudaStream_t stream) {
-  if (seq_len <= 0 || batch <= 0 || heads <= 0 || (head_dim != 64 && head_dim != 128)) {
-    set_error("prefill_attention: bad shape seq=%d batch=%d heads=%d head_dim=%d", seq_len, batch, heads, head_dim);
-    return KVPR_EINVAL;
-  }
-  dim3 grid(batch * heads, (seq_len + 3) / 4);
-  const float qscale = scale * kLog2e;
-  if (head_dim == 128)
-    prefill_attn_kernel<128><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
-  else
-    prefill_attn_kernel<64><<<grid, 128, 0, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
-  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-  return check_launch("prefill_attention");
 }
 
 }  // namespace kvpr

@@ -388,7 +388,8 @@ def test_decode_attention_empty_cache_rejected(dev):
         kernels.decode_attention(q, pages, torch.empty_like(q), None, 1, 1, 64, 0)
 
 
-@pytest.mark.parametrize("batch,heads,d,seq", [(2, 4, 64, 37), (3, 2, 128, 130)])
+@pytest.mark.parametrize("batch,heads,d,seq", [(2, 4, 64, 37), (3, 2, 128, 130), (1, 3, 64, 1), (2, 2, 128, 64),
+                                               (2, 4, 128, 1000), (1, 2, 64, 513)])
 def test_prefill_attention_causal(dev, batch, heads, d, seq):
     h = heads * d
     pages = _rand(seq, 2, batch, h, seed=20)
