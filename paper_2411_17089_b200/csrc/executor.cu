@@ -188,8 +188,8 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   int cb[16][2];
   const int nc = d.x_resident ? 0 : chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d), d.chunk_wave);
   if (nc == 1) {
-    // one X chunk (small layers): X and the KV tail as ONE batched DMA -- the copy engine's fixed cost
-    // is per submission; the chunk's event then covers both (K1 waits on it, K2 on ev_kv)
+    // one X chunk (small layers): X and the KV tail back to back in one call; the chunk's event then
+    // covers both (K1 waits on it, K2 on ev_kv)
     void* dsts[2] = {xd, kv_dst};
     const void* srcs[2] = {Lw.host_x, kv_src};
     const size_t sizes[2] = {static_cast<size_t>(cb[0][1] - cb[0][0]) * row, kv_bytes};
@@ -380,7 +380,7 @@ int compute(Decoder& D, int u, int base, const int* splits) {
   KV_TRY(ck(cudaEventRecord(D.ev_qkv[x.r], cs), "record qkv"));
   if (own_qkv || !(d.zero_copy & 2)) {
     KV_TRY(ck(cudaStreamWaitEvent(ds, D.ev_qkv[x.r], 0), "d2h wait"));
-    // the new X row and K,V page as one batched DMA (store_activation + store_cache)
+    // the new X row and K,V page, two DMAs in one call (store_activation + store_cache)
     void* dsts[2] = {static_cast<char*>(Lw.host_kv) + static_cast<size_t>(x.s - 1) * 2 * row,
                      d.x_resident ? nullptr : static_cast<char*>(Lw.host_x) + static_cast<size_t>(x.s - 1) * row};
     const void* srcs[2] = {page, x_slot};

@@ -47,7 +47,7 @@ def _copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: torch.cuda.Stream) ->
 
 
 def _copy_batch(copies, stream: torch.cuda.Stream) -> None:
-    """[(dst_ptr, src_ptr, nbytes), ...] as ONE batched DMA submission (kvpr_copy_batch_async)."""
+    """[(dst_ptr, src_ptr, nbytes), ...] enqueued by one C call (kvpr_copy_batch_async; one cudaMemcpyAsync each)."""
     import ctypes
 
     n = len(copies)
@@ -136,7 +136,7 @@ class KVPRRuntime:
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
                  chunks: int = 4, nbuf: int | None = None, stores: HostStores | None = None, kv_bits: int | None = None,
                  x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None,
-                 k1_stream: bool | None = None):
+                 k1_stream: bool | None = None, fused_tail: bool | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
 
         x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
@@ -154,7 +154,9 @@ class KVPRRuntime:
         # device buffers per category (graph.py:215-221 uses 2): small-batch layers whose step is bound by
         # the DMA pipeline rather than the GPU keep 4 in flight (config 1: 0.571 -> 0.511 ms/step,
         # profiles/r02s2_c1_sweep.jsonl); KVPR_NBUF overrides
-        fused_ok = (kv_bits is None and os.environ.get("KVPR_FUSED_TAIL", "1") != "0"
+        if fused_tail is None:
+            fused_tail = os.environ.get("KVPR_FUSED_TAIL", "1") != "0"
+        fused_ok = (bool(fused_tail) and kv_bits is None
                     and kernels.layer_tail_supported(batch, cfg.hidden, cfg.heads, cfg.ffn))
         if nbuf is None:
             nbuf = int(os.environ.get("KVPR_NBUF", 4 if fused_ok else 2))
@@ -186,7 +188,8 @@ class KVPRRuntime:
             k1_stream = (env == "1") if env in ("0", "1") else None
         self.k1_stream = (x_resident or self.chunk_wave == 0) if k1_stream is None else bool(k1_stream)
         # batch <= 8 on a small model: the layer after q/k/v runs as one cooperative kernel (K2 -> out-proj
-        # -> LN2 -> fc1 -> fc2, plus the next LN1), csrc/layer_tail.cu; KVPR_FUSED_TAIL=0 turns it off.
+        # -> LN2 -> fc1 -> fc2, plus the next LN1), csrc/layer_tail.cu; fused_tail=False (or
+        # KVPR_FUSED_TAIL=0) keeps the multi-kernel chain, whose bits the streamed and TP runtimes share.
         # Not with 4-bit KV (K2-kv4) or a trace (per-kind spans need the separate kernels)
         self.fused_tail = fused_ok
         # with the fused tail, PCIe traffic the SMs move themselves instead of a copy-engine DMA
@@ -371,7 +374,7 @@ class KVPRRuntime:
         kv_copy = ((self.kvq_dev[buf][lp] if self.kv_bits == 4 else kvd[lp]).data_ptr(), kvh[lp].data_ptr(),
                    (s - 1 - lp) * self.page_bytes) if kv_dma else None
         chunks = chunk_bounds(0 if self.x_resident else lp, self.chunks, self.chunk_rows, self.chunk_wave)
-        if len(chunks) == 1 and tr is None:  # one X chunk: X and the KV tail as one batched DMA (executor.cu)
+        if len(chunks) == 1 and tr is None:  # one X chunk: X and the KV tail in one C call (executor.cu)
             (p0, p1), = chunks
             _copy_batch([(xd[p0].data_ptr(), xh[p0].data_ptr(), (p1 - p0) * row)] + ([kv_copy] if kv_copy else []), hs)
             self.ev_x[r][0].record(hs)
@@ -419,7 +422,7 @@ class KVPRRuntime:
             # store_activation / store_cache (graph.py:340-347) on the D2H engine
             ds.wait_event(self.ev_qkv[r])
             src = self.qnew[buf] if self.kv_bits == 4 else page
-            if tr is None:  # one batched DMA (executor.cu); the row schedule's X row already sits in the store
+            if tr is None:  # two DMAs in one C call (executor.cu); the row schedule's X row already sits in the store
                 _copy_batch([(self.stores.kv[j][s - 1].data_ptr(), src.data_ptr(), self.page_bytes)] +
                             ([] if self.x_resident else [(self.stores.x[j][s - 1].data_ptr(), x_slot.data_ptr(),
                                                           b * h * 2)]), ds)

@@ -52,7 +52,8 @@ def _prompt(case="small"):
 def _reference(dev="cuda:0", case="small"):
     _, b, s0, splits, _ = CASES[case]
     w = _weights(dev, case)
-    rt = KVPRRuntime(w, b, s0 + len(splits) + 1, device=dev)
+    # the TP runtime runs the multi-kernel layer chain; so does this reference (no fused small-batch tail)
+    rt = KVPRRuntime(w, b, s0 + len(splits) + 1, device=dev, fused_tail=False)
     first = rt.prefill(_prompt(case))
     toks = rt.decode(splits, tokens=first, keep_logits=True)
     torch.cuda.synchronize()

@@ -88,22 +88,22 @@ def main():
     from paper_2411_17089_b200 import _lib
 
     lib = _lib.load()
-    lib.kvpr_debug_copy_batch.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_size_t, ctypes.c_void_p]
+    lib.kvpr_copy_batch_async.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_size_t, ctypes.c_void_p]
 
-    def x_kv_batched():
+    def x_kv_one_call():
         dsts = (ctypes.c_void_p * 2)()
         srcs = (ctypes.c_void_p * 2)()
         sizes = (ctypes.c_size_t * 2)(X, KV)
         for i in range(reps):
             dsts[0], dsts[1] = dx[(i % 2) * X:].data_ptr(), dk[(i % 2) * KV:].data_ptr()
             srcs[0], srcs[1] = hx[i * X:].data_ptr(), hk[i * KV:].data_ptr()
-            rc = lib.kvpr_debug_copy_batch(dsts, srcs, sizes, 2, ctypes.c_void_p(s1.cuda_stream))
+            rc = lib.kvpr_copy_batch_async(dsts, srcs, sizes, 2, ctypes.c_void_p(s1.cuda_stream))
             if rc:
                 raise RuntimeError(_lib.last_error())
 
     for _ in range(2):
-        timed("x_kv_batched_us", x_kv_batched)
-        timed("x_kv_batched_with_d2h_us", with_d2h(x_kv_batched))
+        timed("x_kv_one_call_us", x_kv_one_call)
+        timed("x_kv_one_call_with_d2h_us", with_d2h(x_kv_one_call))
         timed("x_only_us", x_only)
         timed("kv_only_us", kv_only)
         timed("d2h_pair_only_us", d2h_only)
