@@ -244,6 +244,12 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
  * page-locked for the copy to be asynchronous. */
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
+/* One strided DMA (cudaMemcpy2DAsync): `height` rows of `width` bytes, row r from src + r*spitch to
+ * dst + r*dpitch.  The same prefix of several layers' stores (X[j][0:l] for consecutive layers j:
+ * host pitch = one layer's store, device pitch = one staging buffer) in ONE copy-engine submission. */
+int kvpr_copy_2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                       void* stream);
+
 /* n (<= 16) DMAs enqueued in order on `stream`, one cudaMemcpyAsync each (zero-byte entries
  * skipped): the per-layer copies of a small model (X[:, :l] + KV[l:s'-1]; the new X row + K,V page)
  * in one C call. */
@@ -305,6 +311,12 @@ typedef struct kvpr_decoder_desc {
   int fused_tail; /* 1: the layer after q/k/v is kvpr_decode_layer_tail (batch <= 8), LN1 / final LN fused into it */
   int zero_copy;  /* with fused_tail: bit 0 = the tail reads KV[l:s'-1] from the host store (no KV DMA),
                      bit 1 = it writes the next unit's X row / k,v page to the host stores (no D2H DMAs) */
+  int dma_group;  /* > 1: the KV-tail copies KV[l:s'-1] of dma_group consecutive layers of a step (single
+                     X chunk or X resident) go as ONE strided 2-D DMA -- the copy engine's ~4 us fixed
+                     cost per submission is paid once per group (X stays one DMA per layer, so each
+                     K1 waits only for its own rows).  Needs layers % dma_group == 0, layers >=
+                     2 * dma_group, nbuf >= 2 * dma_group, nbuf % dma_group == 0 and equally spaced
+                     per-layer host KV stores; otherwise (or <= 1) one KV DMA per layer. */
 } kvpr_decoder_desc;
 
 int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* layers, void** handle);

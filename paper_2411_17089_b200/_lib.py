@@ -46,6 +46,7 @@ EXPORTS = (
     "kvpr_argmax",
     "kvpr_copy_async",
     "kvpr_copy_batch_async",
+    "kvpr_copy_2d_async",
     "kvpr_kv4_page_bytes",
     "kvpr_kv4_quantize",
     "kvpr_kv4_dequantize",
@@ -103,7 +104,7 @@ class DecoderDesc(ctypes.Structure):
             "tok", "ws")] + [("ws_bytes", ctypes.c_size_t)] + [(n, ctypes.c_void_p) for n in (
                 "compute_stream", "h2d_stream", "d2h_stream")] + [("chunk_rows", ctypes.c_int), ("chunk_wave", ctypes.c_int),
                                                       ("recompute_stream", ctypes.c_void_p), ("fused_tail", ctypes.c_int),
-                                                      ("zero_copy", ctypes.c_int)]
+                                                      ("zero_copy", ctypes.c_int), ("dma_group", ctypes.c_int)]
 
 
 class LayerTailDesc(ctypes.Structure):
@@ -151,6 +152,7 @@ _SIGS = {
     "kvpr_argmax": ([_vp, _ll, _i, _i, _vp, _vp, _vp], _i),
     "kvpr_copy_async": ([_vp, _vp, _sz, _vp], _i),
     "kvpr_copy_batch_async": ([ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_sz), _sz, _vp], _i),
+    "kvpr_copy_2d_async": ([_vp, _sz, _vp, _sz, _sz, _sz, _vp], _i),
     "kvpr_kv4_page_bytes": ([_i, _i], _sz),
     "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),

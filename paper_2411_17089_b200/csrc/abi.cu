@@ -183,6 +183,12 @@ int kvpr_recompute_kv(const void* x, const void* w_kv, const void* b_kv, void* k
   int dev = 0;
   cudaGetDevice(&dev);
   const int bn = kvpr_recompute_tile(batch, pos_end - pos_begin, hidden, sm_count(dev));
+  // KVPR_K1_CTAS=n (A/B): K1 on at most n SMs, the rest left to a concurrent layer tail (KVPR_TAIL_CTAS)
+  static const int k1_ctas = [] {
+    const char* e = getenv("KVPR_K1_CTAS");
+    return e != nullptr && atoi(e) > 0 ? atoi(e) : 0;
+  }();
+  a.max_ctas = k1_ctas;
   return gemm_f16(a_ptr, hidden, w_kv, hidden, M, 2 * hidden, hidden, a, bn, static_cast<cudaStream_t>(stream));
 }
 
@@ -340,6 +346,23 @@ int kvpr_argmax(const float* logits, long long ld, int rows, int cols, int* out_
 int kvpr_copy_batch_async(void* const* dsts, const void* const* srcs, const size_t* sizes, size_t n, void* stream) {
   g_err[0] = 0;
   return copy_batch(dsts, srcs, sizes, n, static_cast<cudaStream_t>(stream));
+}
+
+int kvpr_copy_2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                       void* stream) {
+  g_err[0] = 0;
+  if (width == 0 || height == 0) return KVPR_OK;
+  if (dst == nullptr || src == nullptr || dpitch < width || spitch < width) {
+    set_error("copy_2d_async: null pointer or pitch < width");
+    return KVPR_EINVAL;
+  }
+  cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error("copy_2d_async: %s", cudaGetErrorString(e));
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
 }
 
 int kvpr_copy_async(void* dst, const void* src, size_t bytes, void* stream) {

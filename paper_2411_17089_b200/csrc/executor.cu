@@ -32,7 +32,7 @@ namespace kvpr {
 namespace {
 
 struct KTime {
-  int kind;  // 0 = K1 recompute GEMM, 1 = K2 decode attention
+  int kind;  // 0 = K1 recompute GEMM, 1 = K2 decode attention, 2 = one H2D DMA (units = bytes)
   double units;
   cudaEvent_t a, b;
 };
@@ -50,6 +50,8 @@ struct Decoder {
   std::vector<cudaEvent_t> layer_marks, step_marks;  // after each layer / after each step's head
 
   long long launches = 0;
+  int group = 1;                            // layers per KV-tail DMA (kvpr_decoder_desc.dma_group, validated)
+  long long host_kv_pitch = 0;              // bytes between consecutive layers' host KV stores
 };
 
 inline int pool_take(Decoder& D, cudaEvent_t* e) {
@@ -167,6 +169,18 @@ inline Unit unit_of(const Decoder& D, int u, int base, const int* splits) {
   return x;
 }
 
+// one H2D DMA on hs, bracketed by timing events in timed runs (kvpr_decoder_kernel_stats kind 2)
+int h2d(Decoder& D, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+        cudaStream_t hs, const char* what) {
+  KTime t;
+  KV_TRY(kt_begin(D, 2, static_cast<double>(width) * height, hs, &t));
+  if (height == 1)
+    KV_TRY(ck(cudaMemcpyAsync(dst, src, width, cudaMemcpyDefault, hs), what));
+  else
+    KV_TRY(ck(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, hs), what));
+  return kt_end(D, &t, hs);
+}
+
 int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   const kvpr_decoder_desc& d = D.d;
   const Unit x = unit_of(D, u, base, splits);
@@ -187,23 +201,39 @@ int issue_h2d(Decoder& D, int u, int base, const int* splits) {
   const size_t kv_bytes = kv_dma ? (x.s - 1 - x.lp) * 2 * row : 0;
   int cb[16][2];
   const int nc = d.x_resident ? 0 : chunk_bounds(x.lp, d.chunks, cb, chunk_rows(d), d.chunk_wave);
-  if (nc == 1) {
-    // one X chunk (small layers): X and the KV tail back to back in one call; the chunk's event then
-    // covers both (K1 waits on it, K2 on ev_kv)
-    void* dsts[2] = {xd, kv_dst};
-    const void* srcs[2] = {Lw.host_x, kv_src};
-    const size_t sizes[2] = {static_cast<size_t>(cb[0][1] - cb[0][0]) * row, kv_bytes};
-    KV_TRY(copy_batch(dsts, srcs, sizes, 2, hs));
-    KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks], hs), "record X"));
-  } else {
-    for (int c = 0; c < nc; ++c) {
-      KV_TRY(ck(cudaMemcpyAsync(xd + cb[c][0] * row, static_cast<const char*>(Lw.host_x) + cb[c][0] * row,
-                                (cb[c][1] - cb[c][0]) * row, cudaMemcpyDefault, hs),
-                "h2d X"));
-      KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks + c], hs), "record X"));
+  if (D.group > 1 && nc <= 1) {
+    // small layers: X per unit (K1 of unit u waits only for its own rows), the KV tails of layers
+    // [j, j + G) of this step (same s', l) as ONE strided DMA issued by the group's leader (j % G == 0)
+    // after every member's buffer-reuse and store waits -- the members' staging buffers are
+    // consecutive (nbuf % G == 0) and their host stores equally spaced.  A ~0.1 MB tail costs ~1.8 us
+    // of PCIe and ~3.7 us of copy-engine overhead on its own (profiles/r02_dma_2d_probe.json)
+    const int G = D.group;
+    if (nc == 1) {
+      KV_TRY(h2d(D, xd, 0, Lw.host_x, 0, static_cast<size_t>(cb[0][1] - cb[0][0]) * row, 1, hs, "h2d X"));
+      KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks], hs), "record X"));
     }
-    if (kv_bytes) KV_TRY(ck(cudaMemcpyAsync(kv_dst, kv_src, kv_bytes, cudaMemcpyDefault, hs), "h2d KV"));
+    if (u % G != 0) return KVPR_OK;  // KV issued (and ev_kv recorded) by the leader
+    for (int g = 1; g < G; ++g) {
+      const int v = u + g;
+      if (v >= d.nbuf) {
+        const int rp = (v - d.nbuf) % D.R;
+        KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_done[rp], 0), "wait compute"));
+        KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_d2h[rp], 0), "wait d2h"));
+      }
+      if (v >= d.layers) KV_TRY(ck(cudaStreamWaitEvent(hs, D.ev_d2h[(v - d.layers) % D.R], 0), "wait store"));
+    }
+    if (kv_bytes)
+      KV_TRY(h2d(D, kv_dst, 2 * static_cast<size_t>(d.capacity) * row, kv_src, static_cast<size_t>(D.host_kv_pitch),
+                 kv_bytes, G, hs, "h2d KV (grouped)"));
+    for (int g = 1; g < G; ++g) KV_TRY(ck(cudaEventRecord(D.ev_kv[(u + g) % D.R], hs), "record KV"));
+    return ck(cudaEventRecord(D.ev_kv[x.r], hs), "record KV");
   }
+  for (int c = 0; c < nc; ++c) {
+    KV_TRY(h2d(D, xd + cb[c][0] * row, 0, static_cast<const char*>(Lw.host_x) + cb[c][0] * row, 0,
+               (cb[c][1] - cb[c][0]) * row, 1, hs, "h2d X"));
+    KV_TRY(ck(cudaEventRecord(D.ev_x[x.r * d.chunks + c], hs), "record X"));
+  }
+  if (kv_bytes) KV_TRY(h2d(D, kv_dst, 0, kv_src, 0, kv_bytes, 1, hs, "h2d KV"));
   return ck(cudaEventRecord(D.ev_kv[x.r], hs), "record KV");
 }
 
@@ -440,6 +470,20 @@ int kvpr_decoder_create(const kvpr_decoder_desc* desc, const kvpr_layer_desc* la
   D->d = *desc;
   D->layer.assign(layers, layers + desc->layers);
   D->R = desc->layers + desc->nbuf + 2;
+  // DMA grouping (kvpr_decoder_desc.dma_group): only where every precondition holds, else per layer
+  {
+    const int G = desc->dma_group, L = desc->layers;
+    bool ok = G > 1 && L % G == 0 && L >= 2 * G && desc->nbuf >= 2 * G && desc->nbuf % G == 0;
+    if (ok) {
+      D->host_kv_pitch = static_cast<const char*>(layers[1].host_kv) - static_cast<const char*>(layers[0].host_kv);
+      const long long row = static_cast<long long>(desc->batch) * desc->hidden * 2;
+      ok = D->host_kv_pitch >= 2 * row * desc->capacity;
+      for (int j = 1; ok && j < L; ++j)
+        ok = static_cast<const char*>(layers[j].host_kv) - static_cast<const char*>(layers[j - 1].host_kv) ==
+             D->host_kv_pitch;
+    }
+    D->group = ok ? G : 1;
+  }
   auto mk = [](std::vector<cudaEvent_t>& v, int n) {
     v.resize(n);
     for (auto& e : v)

@@ -1087,7 +1087,8 @@ static int launch_bn(const void* a, long long lda, const void* w, long long ldw,
     cudaFuncSetAttribute(gemm_tcgen05_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     attr_done[dev] = 1;
   }
-  const int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
+  int grid = tiles < sm_count(dev) ? tiles : sm_count(dev);
+  if (args.max_ctas > 0 && grid > args.max_ctas) grid = args.max_ctas;
   int rc2 = launch("gemm_tcgen05", gemm_tcgen05_kernel<BN>, grid, 256, Cfg::kSmemBytes, stream, ta, tb, args);
   if (rc2 || splits == 1) return rc2;
   const long long work = static_cast<long long>(args.M) * (args.N / 32);
@@ -1143,7 +1144,8 @@ static int launch_2sm(const void* a, long long lda, const void* w, long long ldw
     cudaFuncSetAttribute(gemm_tcgen05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2SmemBytes);
     attr_done[dev] = 1;
   }
-  const int pairs = sm_count(dev) / 2;
+  int pairs = sm_count(dev) / 2;
+  if (args.max_ctas > 1 && pairs > args.max_ctas / 2) pairs = args.max_ctas / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   return launch("gemm_tcgen05_2sm", gemm_tcgen05_2sm_kernel, grid, 256, k2SmemBytes, stream, ta, tb, args);
 }

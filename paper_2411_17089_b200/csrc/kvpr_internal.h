@@ -39,6 +39,7 @@ struct GemmArgs {
   int sk_ctas;
   unsigned* sk_counters;
   int w_tiled;  // swap-AB: W in the box-tiled layout of kvpr_tile_weight (each 128 x 64 box contiguous)
+  int max_ctas;  // > 0: persistent tcgen05 GEMMs use at most this many CTAs (SMs left to a concurrent kernel)
   // fused TP all-reduce (swap-AB kernel only; tp_world > 1): raw partials pushed to the tile owner
   int tp_rank, tp_world;
   unsigned tp_epoch;

@@ -136,7 +136,7 @@ class KVPRRuntime:
     def __init__(self, weights: OPTWeights, batch: int, capacity: int, device: torch.device | str | None = None,
                  chunks: int = 4, nbuf: int | None = None, stores: HostStores | None = None, kv_bits: int | None = None,
                  x_resident: bool = False, chunk_rows: int | None = None, chunk_wave: int | None = None,
-                 k1_stream: bool | None = None, fused_tail: bool | None = None):
+                 k1_stream: bool | None = None, fused_tail: bool | None = None, dma_group: int | None = None):
         """kv_bits=4 stores/streams the KV cache as 4-bit groupwise pages (kv_bytes_per_element 0.5625).
 
         x_resident=True is the reference's *row* schedule (graph.py:16-17, scheduler.py:88-92): layer
@@ -152,14 +152,25 @@ class KVPRRuntime:
         self.dev = torch.device(device) if device is not None else weights.embed.device
         # env: A/B knob; at most 16 chunks, the native executor's per-unit chunk table (executor.cu)
         # device buffers per category (graph.py:215-221 uses 2): small-batch layers whose step is bound by
-        # the DMA pipeline rather than the GPU keep 4 in flight (config 1: 0.571 -> 0.511 ms/step,
-        # profiles/r02s2_c1_sweep.jsonl); KVPR_NBUF overrides
+        # the DMA pipeline rather than the GPU keep 4 in flight; KVPR_NBUF overrides
         if fused_tail is None:
             fused_tail = os.environ.get("KVPR_FUSED_TAIL", "1") != "0"
         fused_ok = (bool(fused_tail) and kv_bits is None
                     and kernels.layer_tail_supported(batch, cfg.hidden, cfg.heads, cfg.ffn))
         if nbuf is None:
             nbuf = int(os.environ.get("KVPR_NBUF", 4 if fused_ok else 2))
+        # small layers (a whole X store under 8 MB): the KV tails of G consecutive layers go as one strided
+        # DMA (native executor); a ~0.1 MB tail is ~1.8 us of PCIe but ~3.7 us of copy-engine overhead on
+        # its own (profiles/r02_dma_2d_probe.json).  X stays one DMA per layer.  G divides the layers
+        # (layers >= 2G), G buffers per group in flight twice over (nbuf >= 2G).  KVPR_DMA_GROUP overrides.
+        if dma_group is None:
+            dma_group = int(os.environ.get("KVPR_DMA_GROUP", -1))
+        if dma_group < 0:
+            small = capacity * batch * cfg.hidden * 2 < (8 << 20)
+            dma_group = next((g for g in (4, 3, 2) if small and cfg.layers % g == 0 and cfg.layers >= 2 * g), 1)
+        self.dma_group = max(1, dma_group)
+        if self.dma_group > 1:
+            nbuf = self.dma_group * max(2, -(-nbuf // self.dma_group))
         self.chunks, self.nbuf = max(1, min(16, int(os.environ.get("KVPR_CHUNKS", chunks)))), nbuf
         # a K1 chunk carries >= KVPR_CHUNK_MB (default 32) MiB of X (>= 64 positions): every extra X
         # DMA costs copy-engine time (OPT-6.7B b4: 1/2/4/8 chunks of ~30 MB of X in total -> 98.8 /
@@ -247,12 +258,13 @@ class KVPRRuntime:
             self.kernel_timing.append((kt[0], kt[1], kt[2], e))
 
     def kernel_stats(self) -> dict:
-        """{name: (launches, mean seconds per launch, mean algorithmic units per launch)} of the timed launches."""
+        """{name: (launches, mean seconds per launch, mean algorithmic units per launch)} of the timed launches
+        (native executor: also "h2d", every host-to-device DMA with its bytes)."""
         if getattr(self, "_native", None) is not None and not self.kernel_timing:
             import ctypes
 
             res = {}
-            for kind, name in ((0, "k1"), (1, "k2")):
+            for kind, name in ((0, "k1"), (1, "k2"), (2, "h2d")):
                 n, t, u = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
                 _lib.check(_lib.load().kvpr_decoder_kernel_stats(self._native, kind, ctypes.byref(n), ctypes.byref(t),
                                                                  ctypes.byref(u)), "kvpr_decoder_kernel_stats")
@@ -523,6 +535,7 @@ class KVPRRuntime:
         d.recompute_stream = self.rs.cuda_stream if self.k1_stream else None
         d.fused_tail = int(self.fused_tail)
         d.zero_copy = int(self.zc_read) | (int(self.zc_write) << 1)
+        d.dma_group = self.dma_group
         h = ctypes.c_void_p()
         _lib.check(_lib.load().kvpr_decoder_create(ctypes.byref(d), layers, ctypes.byref(h)), "kvpr_decoder_create")
         self._native_keep = (d, layers)

@@ -71,6 +71,31 @@ def test_issue_schedule_variants_bitwise(layers):
             assert torch.equal(a, c), variants[k]
 
 
+@pytest.mark.parametrize("x_resident", [False, True])
+def test_grouped_dmas_bitwise(x_resident):
+    """H2D copies of G consecutive layers as one strided DMA (kvpr_decoder_desc.dma_group): only the copy
+    schedule changes -- tokens, logits and host stores equal the one-DMA-per-layer run bit for bit, for
+    G = 2, 3, 4 (12 layers, fused small-batch tail), splits from 0 to s', X streamed or resident."""
+    cfg = OPTConfig(hidden=256, layers=12, heads=4, ffn=1024, vocab=1024, max_pos=256)
+    b, S0 = 4, 70
+    splits = [35, 71, 0, 73, 10, 75, 74, 1, 40]
+    w = OPTWeights.random(cfg, seed=43, device="cuda", std=0.1, emb_std=0.1)
+    prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(44))
+    outs = []
+    for g in (1, 2, 3, 4):
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1, x_resident=x_resident, dma_group=g)
+        assert rt.dma_group == g and rt.nbuf >= 2 * g
+        first = rt.prefill(prompt)
+        toks = rt.decode(splits, tokens=first, keep_logits=True)
+        torch.cuda.synchronize()
+        n = S0 + len(splits)
+        outs.append((toks.cpu(), rt.last_logits.cpu(), rt.stores.kv[:, :n].clone(), rt.stores.x[:, :n].clone()))
+        rt.close()
+    for k, o in enumerate(outs[1:], start=2):
+        for a, c in zip(outs[0], o):
+            assert torch.equal(a, c), k
+
+
 def test_native_loop_cuts_host_time():
     """Config-1 geometry is host bound under the Python loop; the executor issues a step far faster."""
     cfg = OPTConfig(hidden=768, layers=12, heads=12, ffn=3072)

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=256)
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--x-resident", action="store_true")
+    ap.add_argument("--events", type=int, default=120, help="events listed in order (events_head)")
     ap.add_argument("--trace-out", default="gpurun_out/c1_timeline_trace.json")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -75,7 +76,7 @@ def main():
            "per_name": {k: {"n": v[0], "us_total": v[1], "us_avg": v[1] / v[0]} for k, v in
                         sorted(by_name.items(), key=lambda kv: -kv[1][1])}}
     out["events_head"] = [[e["name"].split("(")[0][:50], e.get("args", {}).get("stream"), round(e["ts"] - t0, 2),
-                           round(e["ts"] + e["dur"] - t0, 2)] for e in gpu[:120]]
+                           round(e["ts"] + e["dur"] - t0, 2)] for e in gpu[:args.events]]
     rt.close()
     print(json.dumps(out))
 
