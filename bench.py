@@ -837,6 +837,15 @@ def run_kvpr(args):
                  "note": "frac_vs_dma_ceiling: vs single launches of the same K2 timed with a concurrent H2D "
                          "(the in-step condition)"})
 
+    copy_stream = None
+    if "h2d" in kstats:  # every H2D DMA of the timed-kernels run, bracketed by events on the copy stream
+        n, t, by = kstats["h2d"]
+        tl = sum(tim.step_ms) / 1e3
+        copy_stream = {"dmas": n, "mb_per_dma": by / 1e6, "us_per_dma": t * 1e6, "gbs_in_copy": by / t / 1e9,
+                       "gbs_vs_peak": by / t / bw_peak, "busy_frac": (n * t / tl) if tl > 0 else None,
+                       "note": "H2D copy engine: bytes / time inside each DMA (events on the copy stream, in the "
+                               "separate timed-kernels run); busy_frac = summed DMA time / that run's step time"}
+
     if rank == 0:
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
@@ -851,7 +860,7 @@ def run_kvpr(args):
             "overlap_roofline": {
                 "bound": "pcie", "achieved": achieved_gbs, "peak": bw_peak / 1e9, "unit": "GB/s",
                 "frac": troof / elapsed, "traffic": None,
-                "achieved_vs_gen5_x16_nominal": achieved_gbs / 64.0,
+                "achieved_vs_gen5_x16_nominal": achieved_gbs / 64.0, "copy_stream": copy_stream,
                 "note": "north-star per-layer overlap roofline max(H2D(X[:, :l'] + KV[l':s'-1]) / measured pinned "
                         "H2D peak, 4 b l' h^2 / sustained bf16 peak), l' = min(l, s'-1): exactly the bytes the "
                         "runtime ships; frac = T_roof / T_measured over the timed steps",
