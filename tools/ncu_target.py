@@ -3,6 +3,7 @@
     ncu --set full -k regex:gemm_tcgen05 -c 1 python tools/ncu_target.py k1
     ncu --set full -k regex:decode_attn -c 1 python tools/ncu_target.py k2
     ncu --set full -k regex:gemm_tcgen05_kernel -c 1 python tools/ncu_target.py c1   # config-1 shapes
+    ncu --set full -k regex:prefill_fa -c 1 python tools/ncu_target.py prefill
 """
 import sys
 
@@ -13,6 +14,16 @@ from paper_2411_17089_b200 import kernels
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 dev = torch.device("cuda:0")
+if which == "prefill":  # causal prefill attention at the config-2 prompt (b32, 32 heads, d128, S = 1024)
+    b, heads, d, S = 32, 32, 128, 1024
+    pages = torch.randn(S, 2, b, heads * d, device=dev).half()
+    q = torch.randn(S, b, heads * d, device=dev).half()
+    o = torch.empty_like(q)
+    for _ in range(2):
+        kernels.prefill_attention(q, pages, o, b, heads, d, S)
+    torch.cuda.synchronize()
+    print("ok")
+    sys.exit(0)
 if which == "c1":  # config 1 (OPT-125M shape, b4, s' = 260, l = 252): K1, q/k/v, the CUDA-core projections, K2
     b, h, l, s = 4, 768, 252, 260
     pages = torch.randn(272, 2, b, h, device=dev).half()
