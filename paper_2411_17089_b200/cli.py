@@ -5,13 +5,16 @@ cli.py:73-164), plan JSON on stdout or --out, exit codes 0 ok, 1 invalid
 input, 2 GPU memory budget exceeded, 3 validation failure (cli.py:45-48).
 
     python -m paper_2411_17089_b200 plan      --config cfg.json [--l N] [--out plan.json]
+    python -m paper_2411_17089_b200 simulate  --config cfg.json [--plan p.json | --l N] [--trace t.json] [--metrics m.csv]
+    python -m paper_2411_17089_b200 sweep     --config cfg.json --vary AXIS=V1,V2 [--policies naive,kvpr:column]
     python -m paper_2411_17089_b200 calibrate --measurements m.csv
     python -m paper_2411_17089_b200 profile   [--hidden 4096 --batch 32] [--out m.csv]   (GPU)
     python -m paper_2411_17089_b200 run       --config cfg.json [--plan plan.json] [--trace t.json] (GPU)
     python -m paper_2411_17089_b200 validate  [--cases N] [--seed S]                       (GPU)
 
-`plan` / `calibrate` print byte-identical documents to the reference's for
-the same config.  `run` executes the plan on the B200 (random-init weights,
+`plan` / `calibrate` / `simulate` / `sweep` print byte-identical documents to
+the reference's for the same config (simulate / sweep through the pipesim
+restatement; its --trace / --metrics files are byte-identical too).  `run` executes the plan on the B200 (random-init weights,
 synthetic prompt) instead of simulating it and prints the reference's
 `key=value` report style with measured numbers.  An optional "runtime"
 section adds {"seed", "weights_std", "chunks", "device"}.
@@ -20,9 +23,11 @@ section adds {"seed", "weights_std", "chunks", "device"}.
 from __future__ import annotations
 
 import argparse
+import copy
 import json
 import logging
 import os
+import re
 import sys
 from dataclasses import dataclass
 
@@ -74,7 +79,11 @@ def _sec(doc, name, required):
     return doc[name]
 
 
-def load_config(path: str) -> Setup:
+_WORKLOAD_AXES = ("batch_size", "num_batches", "prompt_len", "gen_len", "kv_bytes_per_element")
+_HARDWARE_AXES = ("gpu_flops", "h2d_bw", "d2h_bw", "transfer_latency_s", "gpu_efficiency")
+
+
+def load_config_doc(path: str) -> dict:
     try:
         with open(path) as fh:
             doc = json.load(fh)
@@ -83,6 +92,14 @@ def load_config(path: str) -> Setup:
     if not isinstance(doc, dict):
         raise ConfigError(f"{path}: config must be a JSON object")
     _only("config", doc, ("model", "workload", "hardware", "policy", "runtime"))
+    return doc
+
+
+def load_config(path: str) -> Setup:
+    return setup_from_doc(load_config_doc(path))
+
+
+def setup_from_doc(doc: dict) -> Setup:
     try:
         m = _sec(doc, "model", True)
         fields = ("hidden_dim", "num_layers", "num_heads", "ffn_dim", "precision_bytes")
@@ -96,11 +113,10 @@ def load_config(path: str) -> Setup:
                 raise ConfigError(f"model section missing: {', '.join(missing)}")
             spec = ModelSpec(**m)
         w = _sec(doc, "workload", True)
-        _only("workload", w, ("batch_size", "num_batches", "prompt_len", "gen_len", "kv_bytes_per_element"))
+        _only("workload", w, _WORKLOAD_AXES)
         wl = WorkloadSpec(**w)
         hw = _sec(doc, "hardware", True)
-        _only("hardware", hw, ("gpu_flops", "h2d_bw", "d2h_bw", "transfer_latency_s", "gpu_efficiency",
-                               "gpu_mem_budget_bytes"))
+        _only("hardware", hw, _HARDWARE_AXES + ("gpu_mem_budget_bytes",))
         for k in ("gpu_flops", "h2d_bw", "d2h_bw"):
             if k not in hw:
                 raise ConfigError(f"hardware section missing {k!r}")
@@ -150,6 +166,122 @@ def _out(text: str, path: str | None) -> None:
 def cmd_plan(a) -> int:
     s = load_config(a.config)
     _out(plan_to_json(_plan(s, a.l), s.spec, s.wl, s.profile) + "\n", a.out)
+    return EXIT_OK
+
+
+def _sim_policy(s: Setup):
+    from .pipesim import Policy
+
+    return Policy(schedule=s.schedule, recompute=s.recompute, granularity=s.granularity,
+                  weights_resident=s.weights_resident)
+
+
+def _import_plan_for(s: Setup, path: str) -> SplitPlan:
+    with open(path) as fh:
+        doc = json.load(fh)
+    plan, spec, wl, prof = import_plan(doc)
+    if (spec, wl, prof) != (s.spec, s.wl, s.profile):
+        raise ConfigError("--plan document does not match the config")
+    return plan
+
+
+def cmd_simulate(a) -> int:
+    """The reference's prediction for one policy (cli.py:195-230): task DAG + list scheduler
+    (pipesim restatement), `key=value` report, optional Chrome trace and metrics CSV."""
+    from . import pipesim
+
+    s = load_config(a.config)
+    if a.l is not None:
+        plan = _plan(s, a.l)
+    elif a.plan:
+        plan = _import_plan_for(s, a.plan)
+    else:
+        plan = _plan(s, None)
+    policy = _sim_policy(s)
+    graph = pipesim.build_task_graph(s.spec, s.wl, s.profile, plan, policy, s.budget)
+    timeline, rep = pipesim.simulate(graph, s.profile)
+    label = "kvpr" if policy.recompute else "naive"
+    lines = [f"policy={label} schedule={policy.schedule} granularity={policy.granularity} "
+             f"recompute={'on' if policy.recompute else 'off'} weights_resident={policy.weights_resident}",
+             f"tasks={len(graph)}", f"makespan_s={rep.makespan!r}", f"throughput_tok_s={rep.decode_throughput!r}",
+             f"gpu_utilization={rep.gpu_utilization!r}", f"peak_gpu_bytes={rep.peak_gpu_bytes!r}"]
+    lines += [f"breakdown.{k}={v!r}" for k, v in rep.breakdown.items()]
+    _out("".join(x + "\n" for x in lines), a.out)
+    if a.trace:
+        pipesim.write_trace(timeline, a.trace)
+    if a.metrics:
+        with open(a.metrics, "w") as fh:
+            pipesim.write_metrics_csv([pipesim.metrics_row(label, policy, rep)], fh)
+    return EXIT_OK
+
+
+_POLICY_MODIFIERS = {"row": ("schedule", "row"), "column": ("schedule", "column"),
+                     "coarse": ("granularity", "coarse"), "fine": ("granularity", "fine"),
+                     "resident": ("weights_resident", True), "offloaded": ("weights_resident", False)}
+
+
+def parse_policy_token(token: str, base):
+    """'naive' / 'kvpr' plus ':'-separated modifiers over the config's policy (cli.py:243-262)."""
+    from .pipesim import Policy
+
+    head, *mods = token.strip().split(":")
+    if head not in ("naive", "kvpr"):
+        raise ConfigError(f"unknown policy {head!r} (use naive or kvpr)")
+    values = {"recompute": head == "kvpr", "schedule": base.schedule, "granularity": base.granularity,
+              "weights_resident": base.weights_resident}
+    for mod in mods:
+        if mod not in _POLICY_MODIFIERS:
+            raise ConfigError(f"unknown policy modifier {mod!r}")
+        field_, value = _POLICY_MODIFIERS[mod]
+        values[field_] = value
+    return token.strip(), Policy(**values)
+
+
+def _number(text: str):
+    if re.fullmatch(r"[+-]?\d+", text):
+        return int(text)
+    try:
+        return float(text)
+    except ValueError as exc:
+        raise ConfigError(f"not a number: {text!r}") from exc
+
+
+def parse_axis(vary: str):
+    if "=" not in vary:
+        raise ConfigError("--vary expects AXIS=V1,V2,...")
+    axis, _, rest = vary.partition("=")
+    axis = axis.strip()
+    values = [v for v in (x.strip() for x in rest.split(",")) if v]
+    if not values:
+        raise ConfigError("--vary axis has no values")
+    if axis not in _WORKLOAD_AXES and axis not in _HARDWARE_AXES:
+        raise ConfigError(f"unknown sweep axis {axis!r}; known: {', '.join(_WORKLOAD_AXES + _HARDWARE_AXES)}")
+    return axis, [_number(v) for v in values]
+
+
+_SWEEP_COLS = ("policy", "schedule", "granularity", "recompute", "makespan_s", "throughput_tok_s", "gpu_util",
+               "peak_gpu_bytes", "speedup_vs_first")
+
+
+def cmd_sweep(a) -> int:
+    """One axis across policies, one CSV row per (value, policy) (cli.py:287-318)."""
+    from . import pipesim
+
+    doc = load_config_doc(a.config)
+    base = _sim_policy(setup_from_doc(doc))
+    axis, values = parse_axis(a.vary)
+    policies = [parse_policy_token(t, base) for t in a.policies.split(",") if t.strip()]
+    if not policies:
+        raise ConfigError("--policies is empty")
+    section = "workload" if axis in _WORKLOAD_AXES else "hardware"
+    rows = [",".join(pipesim.cell(c) for c in ("axis", "value") + _SWEEP_COLS)]
+    for value in values:
+        point = copy.deepcopy(doc)
+        point.setdefault(section, {})[axis] = value
+        s = setup_from_doc(point)
+        for row in pipesim.compare(s.spec, s.wl, s.profile, policies, s.budget):
+            rows.append(",".join(pipesim.cell(c) for c in [axis, value] + [row[k] for k in _SWEEP_COLS]))
+    _out("".join(r + "\n" for r in rows), a.out)
     return EXIT_OK
 
 
@@ -345,6 +477,20 @@ def build_parser() -> argparse.ArgumentParser:
     sp.add_argument("--l", type=int, default=None)
     sp.add_argument("--out")
     sp.set_defaults(fn=cmd_plan)
+    sp = sub.add_parser("simulate")
+    sp.add_argument("--config", required=True)
+    sp.add_argument("--plan")
+    sp.add_argument("--out")
+    sp.add_argument("--trace")
+    sp.add_argument("--metrics")
+    sp.add_argument("--l", type=int, default=None)
+    sp.set_defaults(fn=cmd_simulate)
+    sp = sub.add_parser("sweep")
+    sp.add_argument("--config", required=True)
+    sp.add_argument("--vary", required=True)
+    sp.add_argument("--policies", default="naive,kvpr")
+    sp.add_argument("--out")
+    sp.set_defaults(fn=cmd_sweep)
     sp = sub.add_parser("calibrate")
     sp.add_argument("--measurements", required=True)
     sp.add_argument("--out")

@@ -12,7 +12,9 @@ test_acceptance.py:150-183, is the template).
 Same API and results as the reference, bit for bit (tests/test_pipesim_cpu.py
 against timelines produced by the live reference, tests/golden/pipesim_golden.json):
 ``Policy``, ``build_task_graph``, ``estimate_peak_gpu_bytes``, ``task_durations``,
-``run_schedule``, ``simulate`` -> (``Timeline``, ``SimReport``).  Only the pure
+``run_schedule``, ``simulate`` -> (``Timeline``, ``SimReport``), and the exporters / policy table
+of pipesim/trace.py (``export_trace``, ``write_trace``, ``metrics_row``, ``write_metrics_csv``,
+``plan_for_policy``, ``compare``) behind the CLI's ``simulate`` and ``sweep``.  Only the pure
 Python engine is restated (the Cython twin computes identical schedules).
 
 Per unit the graph holds up to eight tasks (graph.py:1-28):
@@ -27,7 +29,9 @@ first), double buffering as a dependency on the consumer two loads back.
 
 from __future__ import annotations
 
+import csv
 import heapq
+import json
 import math
 from dataclasses import dataclass, field
 from enum import Enum
@@ -36,7 +40,7 @@ from .costmodel import (ModelSpec, WorkloadSpec, activation_bytes, decode_step_f
                         mha_matrix_bytes, mha_weight_bytes, recompute_flops, token_activation_bytes,
                         token_kv_store_bytes)
 from .hwprofile import HardwareProfile, compute_time, transfer_time
-from .scheduler import SCHEDULE_MODES, SplitPlan
+from .scheduler import SCHEDULE_MODES, SplitPlan, constant_plan, plan_generation
 
 
 class TaskKind(str, Enum):
@@ -455,3 +459,67 @@ def check_schedule(graph: TaskGraph, start, end) -> None:
         for d in t.deps:
             if start[t.id] < end[d]:
                 raise AssertionError(f"dependency violated: task {t.id} starts before dep {d} ends")
+
+
+# ---------------------------------------------------------------------------
+# exporters and the policy comparison table (pipesim/trace.py:17-110)
+
+TRACE_LANES = {"h2d": 0, "gpu": 1, "d2h": 2}
+METRICS_COLUMNS = ("policy", "schedule", "granularity", "recompute", "makespan_s", "throughput_tok_s", "gpu_util",
+                   "peak_gpu_bytes")
+
+
+def export_trace(timeline: Timeline) -> list[dict]:
+    """Chrome trace events, one complete ("X") event per task, lanes h2d 0 / gpu 1 / d2h 2 (trace.py:30-43)."""
+    return [{"name": e.name, "cat": e.kind, "ph": "X", "ts": e.start * 1e6, "dur": (e.end - e.start) * 1e6,
+             "pid": 0, "tid": TRACE_LANES[e.resource]} for e in timeline.entries]
+
+
+def write_trace(timeline: Timeline, path: str) -> None:
+    """Compact, key-sorted JSON plus a newline: the reference's bytes (trace.py:46-49)."""
+    with open(path, "w") as fh:
+        json.dump(export_trace(timeline), fh, sort_keys=True, separators=(",", ":"))
+        fh.write("\n")
+
+
+def metrics_row(label: str, policy: Policy, report: SimReport) -> dict:
+    return {"policy": label, "schedule": policy.schedule, "granularity": policy.granularity,
+            "recompute": "on" if policy.recompute else "off", "makespan_s": report.makespan,
+            "throughput_tok_s": report.decode_throughput, "gpu_util": report.gpu_utilization,
+            "peak_gpu_bytes": report.peak_gpu_bytes}
+
+
+def cell(value) -> str:
+    """Floats by repr (round-trip exact), everything else by str (trace.py:73-76)."""
+    return repr(value) if isinstance(value, float) else str(value)
+
+
+def write_metrics_csv(rows, fh) -> None:
+    """Fixed-schema metrics table; extra row keys are ignored (trace.py:65-70)."""
+    w = csv.writer(fh, lineterminator="\n")
+    w.writerow(METRICS_COLUMNS)
+    for row in rows:
+        w.writerow([cell(row[c]) for c in METRICS_COLUMNS])
+
+
+def plan_for_policy(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile, policy: Policy) -> SplitPlan:
+    """The solver's plan when recomputing, the all-zero plan for the naive baseline (trace.py:79-85)."""
+    if policy.recompute:
+        return plan_generation(spec, wl, profile, policy.schedule)
+    return constant_plan(wl, policy.schedule, 0)
+
+
+def compare(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile, policies, gpu_mem_budget=None) -> list[dict]:
+    """Simulate each (label, Policy) on one config; rows carry speedup_vs_first (trace.py:88-110)."""
+    if not policies:
+        raise ValueError("need at least one policy")
+    rows, base = [], None
+    for label, policy in policies:
+        plan = plan_for_policy(spec, wl, profile, policy)
+        _, rep = simulate(build_task_graph(spec, wl, profile, plan, policy, gpu_mem_budget), profile)
+        row = metrics_row(label, policy, rep)
+        if base is None:
+            base = rep.makespan
+        row["speedup_vs_first"] = base / rep.makespan if rep.makespan > 0 else 0.0
+        rows.append(row)
+    return rows

@@ -14,6 +14,7 @@ Writes
                          reports for row / column, recompute on / off, resident /
                          streamed (coarse, fine) weights, 1-3 GPU batches, with and
                          without transfer latency (pins paper_2411_17089_b200.pipesim).
+  cli_small.json         a small streamed-weights config for the CLI cases (simulate --trace/--metrics, sweep)
   numerics_golden.npz    fp64 split_merge_kv / decode_attention / append_token_kv
                          outputs of kvoverlap.numerics on seeded small cases
                          (pins oracle/numerics_ref.py).
@@ -225,25 +226,53 @@ def numerics_cases():
     return arrs
 
 
+CLI_SMALL = {"model": {"hidden_dim": 768, "num_layers": 4, "num_heads": 12, "ffn_dim": 3072}, "workload": {"batch_size": 4, "prompt_len": 64, "gen_len": 2,
+                                                          "num_batches": 2},
+             "hardware": {"gpu_flops": 1.19e15, "h2d_bw": 55.3e9, "d2h_bw": 55.3e9, "transfer_latency_s": 2e-6},
+             "policy": {"schedule": "column", "granularity": "fine", "weights_resident": False}}
+
+
 def cli_cases():
-    """stdout of the reference CLI (`kvoverlap plan|calibrate`) for configs shipped with this repo."""
+    """stdout (and --trace / --metrics files) of the reference CLI (`kvoverlap plan | calibrate |
+    simulate | sweep`) for configs shipped with this repo."""
     import contextlib
+    import hashlib
     import io
+    import tempfile
 
     from kvoverlap import cli as rcli
 
     root = OUT.parents[1]
+    (OUT / "cli_small.json").write_text(json.dumps(CLI_SMALL, sort_keys=True) + "\n")
+    big = str(root / "configs" / "opt6.7b_b32_s1024.json")
+    small = str(OUT / "cli_small.json")
+    tmp = Path(tempfile.mkdtemp())
     out = {}
     for name, argv in (
-        ("plan_opt6.7b", ["plan", "--config", str(root / "configs" / "opt6.7b_b32_s1024.json")]),
-        ("plan_opt6.7b_l500", ["plan", "--config", str(root / "configs" / "opt6.7b_b32_s1024.json"), "--l", "500"]),
+        ("plan_opt6.7b", ["plan", "--config", big]),
+        ("plan_opt6.7b_l500", ["plan", "--config", big, "--l", "500"]),
         ("calibrate_sample", ["calibrate", "--measurements", str(OUT / "measurements_sample.csv")]),
+        ("simulate_opt6.7b", ["simulate", "--config", big]),
+        ("simulate_opt6.7b_l500", ["simulate", "--config", big, "--l", "500"]),
+        ("simulate_small_files", ["simulate", "--config", small, "--trace", "@TMP/t.json", "--metrics", "@TMP/m.csv"]),
+        ("sweep_prompt", ["sweep", "--config", big, "--vary", "prompt_len=512,2048",
+                          "--policies", "naive,kvpr,kvpr:row,kvpr:fine:offloaded"]),
+        ("sweep_h2d_bw", ["sweep", "--config", big, "--vary", "h2d_bw=25e9,64e9"]),
+        ("sweep_small_batches", ["sweep", "--config", small, "--vary", "num_batches=1,3",
+                                 "--policies", "kvpr,kvpr:coarse,naive:row:resident"]),
     ):
         buf = io.StringIO()
+        real = [a.replace("@TMP", str(tmp)) for a in argv]
         with contextlib.redirect_stdout(buf):
-            rc = rcli.main(argv)
-        out[name] = {"argv": argv[:1] + [a.replace(str(root) + "/", "") for a in argv[1:]], "rc": rc,
-                     "stdout": buf.getvalue()}
+            rc = rcli.main(real)
+        case = {"argv": argv[:1] + [a.replace(str(root) + "/", "") for a in argv[1:]], "rc": rc,
+                "stdout": buf.getvalue()}
+        assert rc == 0, (name, rc)
+        if "--trace" in argv:
+            data = (tmp / "t.json").read_bytes()
+            case["trace_sha256"], case["trace_bytes"] = hashlib.sha256(data).hexdigest(), len(data)
+            case["metrics"] = (tmp / "m.csv").read_text()
+        out[name] = case
     return out
 
 

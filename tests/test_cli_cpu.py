@@ -1,10 +1,11 @@
-"""CLI contract (no GPU): byte-identical plan / calibrate documents vs the
+"""CLI contract (no GPU): byte-identical plan / calibrate / simulate / sweep documents vs the
 reference CLI's stdout (tests/golden/scheduler_golden.json["cli"], produced by
 running `kvoverlap plan|calibrate` on the same files), config validation and
 the exit-code contract of pkg/src/kvoverlap/cli.py:45-48."""
 
 from __future__ import annotations
 
+import hashlib
 import json
 
 import pytest
@@ -17,13 +18,32 @@ G = json.loads((GOLDEN / "scheduler_golden.json").read_text())["cli"]
 
 
 @pytest.mark.parametrize("name", sorted(G))
-def test_cli_output_identical_to_reference(name, capsys, monkeypatch):
+def test_cli_output_identical_to_reference(name, capsys, monkeypatch, tmp_path):
+    """plan / calibrate / simulate / sweep: stdout byte-identical to the reference CLI's, and simulate's
+    --trace (sha256) and --metrics files too."""
     monkeypatch.chdir(ROOT)
     case = G[name]
-    rc = cli.main(case["argv"])
+    rc = cli.main([a.replace("@TMP", str(tmp_path)) for a in case["argv"]])
     out = capsys.readouterr().out
     assert rc == case["rc"] == 0
     assert out == case["stdout"]
+    if "trace_sha256" in case:
+        data = (tmp_path / "t.json").read_bytes()
+        assert (len(data), hashlib.sha256(data).hexdigest()) == (case["trace_bytes"], case["trace_sha256"])
+        assert (tmp_path / "m.csv").read_text() == case["metrics"]
+
+
+def test_sweep_and_simulate_errors(tmp_path, capsys):
+    cfg = _cfg(tmp_path, BASE)
+    assert cli.main(["sweep", "--config", cfg, "--vary", "nope=1,2"]) == cli.EXIT_INVALID
+    assert cli.main(["sweep", "--config", cfg, "--vary", "prompt_len"]) == cli.EXIT_INVALID
+    assert cli.main(["sweep", "--config", cfg, "--vary", "prompt_len=8", "--policies", "kvpr:sideways"]) == \
+        cli.EXIT_INVALID
+    assert cli.main(["sweep", "--config", cfg, "--vary", "prompt_len=8", "--policies", "greedy"]) == cli.EXIT_INVALID
+    assert cli.main(["sweep", "--config", cfg, "--vary", "prompt_len=x"]) == cli.EXIT_INVALID
+    tight = dict(BASE, hardware=dict(BASE["hardware"], gpu_mem_budget_bytes=1e6))
+    assert cli.main(["simulate", "--config", _cfg(tmp_path, tight)]) == cli.EXIT_BUDGET
+    capsys.readouterr()
 
 
 def _cfg(tmp_path, doc):
