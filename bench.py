@@ -403,10 +403,11 @@ def run_config1(args, dev, peaks):
             "profile": {"h2d_bandwidth": prof.h2d_bandwidth, "gpu_flops": prof.gpu_flops, "bw_peak": bw}}
 
 
-def run_config5(args, dev, peaks, prof, bw, prompts=(512, 2048, 8192), layers=2, steps=3):
+def run_config5(args, dev, peaks, prof, bw, prompts=(512, 1024, 2048, 4096, 8192), layers=2, steps=3, grid=8):
     """BASELINE config 5: OPT-6.7B layer shapes, b32, per-layer decode latency at prompts 512..8192 for
-    l = 0 (naive offload), the reference solver's l (column, live profile) and l = s'; reports T_roof
-    fractions and the measured argmin (scheduler-chosen l vs measured optimum).  Per-layer latency is
+    l = 0 (naive offload), the reference solver's l (column, live profile), l = s' and a forced-l grid
+    (steps of max(64, s'/grid) over [0, s']); reports T_roof fractions and the measured argmin over all
+    points (scheduler-chosen l vs measured optimum).  Per-layer latency is
     what is compared, so `layers` of the 32 identical layers bound the host stores (6.4 GB per layer at
     prompt 8192)."""
     import statistics
@@ -431,7 +432,9 @@ def run_config5(args, dev, peaks, prof, bw, prompts=(512, 2048, 8192), layers=2,
         wl = WorkloadSpec(batch_size=b, prompt_len=P, gen_len=steps)
         l_sched = solve_split(spec, wl, prof, s1, "column").recompute_len
         pts = []
-        for name, l in (("naive", 0), ("solver", l_sched), ("full", s1)):
+        step_l = max(64, -(-s1 // grid // 64) * 64)
+        forced = [("grid", l) for l in range(step_l, s1, step_l) if l != l_sched]
+        for name, l in [("naive", 0), ("solver", l_sched), ("full", s1)] + forced:
             rt.reset(P)
             tim = DecodeTiming()
             rt.decode([min(l, P + 1 + i) for i in range(steps)], tokens=first, timing=tim)
@@ -443,8 +446,8 @@ def run_config5(args, dev, peaks, prof, bw, prompts=(512, 2048, 8192), layers=2,
                         "ref_pred_column_ms": layer_time(spec, wl, prof, s1, l, "column").total * 1e3})
         best = min(pts, key=lambda r: r["layer_ms"])
         sched = next(r for r in pts if r["plan"] == "solver")
-        out.append({"prompt": P, "l_sched": l_sched, "points": pts, "measured_argmin_l": best["l"],
-                    "sched_vs_measured_opt": best["layer_ms"] / sched["layer_ms"]})
+        out.append({"prompt": P, "l_sched": l_sched, "l_grid_step": step_l, "points": pts,
+                    "measured_argmin_l": best["l"], "sched_vs_measured_opt": best["layer_ms"] / sched["layer_ms"]})
         rt.close()
         del rt, w
         torch.cuda.empty_cache()
