@@ -228,10 +228,12 @@ template <int D>
 int launch_prefill(const __half* q, const __half* kv, __half* out, int batch, int heads, int seq_len, float qscale,
                    cudaStream_t stream) {
   constexpr size_t smem = (size_t)(kBM + 4 * kBN) * D * 2;
-  static bool attr_set = false;
-  if (!attr_set) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int attr_done[64] = {0};  // the attribute is per device
+  if (dev >= 64 || !attr_done[dev]) {
     cudaFuncSetAttribute(prefill_fa_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+    if (dev < 64) attr_done[dev] = 1;
   }
   dim3 grid((seq_len + kBM - 1) / kBM, batch * heads);
   prefill_fa_kernel<D><<<grid, 128, smem, stream>>>(q, kv, out, batch, heads, seq_len, qscale);
