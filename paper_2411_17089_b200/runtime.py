@@ -190,14 +190,16 @@ class KVPRRuntime:
             self.hs = torch.cuda.Stream(self.dev)              # H2D copy engine
             self.ds = torch.cuda.Stream(self.dev)              # D2H copy engine
             self.rs = torch.cuda.Stream(self.dev)              # K1 issued a unit ahead (native executor)
-        # native executor: K1 on its own stream, issued a unit ahead, where the layer chain is GPU-bound
-        # (X resident = the row schedule, or small models whose K1 never fills a wave).  A PCIe-bound
-        # column schedule hides K1 anyway and keeps it on the compute stream, uncontended.
+        # native executor: K1 on its own stream, issued a unit ahead, for small models whose K1 never
+        # fills a wave (the layer chain is latency-bound and K1 overlaps it).  At full width K1 stays on
+        # the compute stream: a PCIe-bound column schedule hides it anyway, and in the row schedule a K1
+        # holding SMs under the next layer's stream-K projections costs more than the overlap gains
+        # (config 2 row, same box: 536 vs 514 tok/s, profiles/r02_row_k1_stream.jsonl).
         # KVPR_K1_STREAM=0/1 forces it.
         env = os.environ.get("KVPR_K1_STREAM")
         if k1_stream is None:
             k1_stream = (env == "1") if env in ("0", "1") else None
-        self.k1_stream = (x_resident or self.chunk_wave == 0) if k1_stream is None else bool(k1_stream)
+        self.k1_stream = (self.chunk_wave == 0) if k1_stream is None else bool(k1_stream)
         # batch <= 8 on a small model: the layer after q/k/v runs as one cooperative kernel (K2 -> out-proj
         # -> LN2 -> fc1 -> fc2, plus the next LN1), csrc/layer_tail.cu; fused_tail=False (or
         # KVPR_FUSED_TAIL=0) keeps the multi-kernel chain, whose bits the streamed and TP runtimes share.
