@@ -584,3 +584,35 @@ def test_tiled_weights_bit_identical(dev, M, N, K):
         assert torch.equal(o1, o2)
     with pytest.raises(ValueError, match="tiled"):
         kernels.linear_simple(_rand(80, K, seed=74), wt, bias, torch.empty(80, N, device=dev))
+
+
+def test_copy_entry_points(dev):
+    """kvpr_copy_async / kvpr_copy_batch_async / kvpr_copy_2d_async (the schedule's DMAs): bytes land
+    where the pitches say, zero-byte entries are skipped, a pitch below the width is rejected."""
+    import ctypes
+
+    from paper_2411_17089_b200 import _lib, hostmem
+
+    lib = _lib.load()
+    s = torch.cuda.current_stream()
+    host = hostmem.pinned_empty((4, 1000), torch.uint8)
+    host.copy_(torch.randint(0, 255, (4, 1000), dtype=torch.uint8))
+    dst = torch.zeros(4, 600, dtype=torch.uint8, device=dev)
+    # 2-D: 4 rows of 300 bytes from host pitch 1000 (offset 100) into device pitch 600 (offset 50)
+    _lib.call("kvpr_copy_2d_async", dst.data_ptr() + 50, 600, host.data_ptr() + 100, 1000, 300, 4, s.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, 50:350].cpu(), host[:, 100:400])
+    assert int(dst[:, :50].sum()) == 0 and int(dst[:, 350:].sum()) == 0
+    with pytest.raises(ValueError):
+        _lib.call("kvpr_copy_2d_async", dst.data_ptr(), 100, host.data_ptr(), 1000, 300, 2, s.cuda_stream)
+    # batch: two copies and a zero-byte entry, one call
+    out = torch.zeros(3, 256, dtype=torch.uint8, device=dev)
+    dsts = (ctypes.c_void_p * 3)(out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr())
+    srcs = (ctypes.c_void_p * 3)(host[0].data_ptr(), host[1].data_ptr(), host[2].data_ptr())
+    sizes = (ctypes.c_size_t * 3)(256, 0, 128)
+    _lib.call("kvpr_copy_batch_async", dsts, srcs, sizes, 3, s.cuda_stream)
+    _lib.call("kvpr_copy_async", out[1].data_ptr() + 10, host[3].data_ptr(), 20, s.cuda_stream)
+    torch.cuda.synchronize()
+    o = out.cpu()
+    assert torch.equal(o[0], host[0, :256]) and torch.equal(o[2, :128], host[2, :128]) and int(o[2, 128:].sum()) == 0
+    assert torch.equal(o[1, 10:30], host[3, :20]) and int(o[1, :10].sum()) == 0
