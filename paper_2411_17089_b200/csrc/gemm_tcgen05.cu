@@ -1033,6 +1033,33 @@ static int make_tmap(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t 
   return KVPR_OK;
 }
 
+// fp16 tensor [dims[rank-1]]...[dims[0]] with byte strides of dims 1.. (strides[rank-1]) -> boxes `box`
+// with the 128-byte swizzle, zero fill out of bounds (prefill_attn.cu's 3-D views of the page layout)
+int make_tmap_nd(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  if (enc == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return KVPR_ECUDA;
+  }
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], estr[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    estr[i] = 1;
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(ptr), d, st, bx, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) for a rank-%d map", int(r), rank);
+    return KVPR_ECUDA;
+  }
+  return KVPR_OK;
+}
+
 // 64-wide k-boxes per ring stage of the swap-AB decode GEMM: KVPR_SWAP_KBOX = 1, 2 or 4 overrides
 // the shape-based default (0)
 static int swap_kbox() {

@@ -2,6 +2,7 @@
 // the extern "C" boundary in abi.cu.  Nothing here crosses the C-ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -71,6 +72,10 @@ struct GemvLn {  // LayerNorm prologue of the fused decode projection (A = LN(x)
 int gemv_f16(const void* a, long long lda, const void* w, long long ldw, const GemmArgs& args, cudaStream_t stream,
              const GemvLn* ln = nullptr);
 int gemv_slices(int N, int device);
+
+// rank-2..5 fp16 tensor map with the 128-byte swizzle (gemm_tcgen05.cu); strides in bytes for dims 1..
+int make_tmap_nd(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box);
 
 int gemm_f16(const void* a, long long lda, const void* w, long long ldw, int M, int N, int K, const GemmArgs& epi,
              int bn, cudaStream_t stream, float* ws = nullptr, size_t ws_bytes = 0, const GemvLn* ln = nullptr);

@@ -83,14 +83,14 @@ def test_sass_is_tcgen05_tma(lib):
     assert "UTMALDG" in out, "no TMA loads in SASS"
     assert "LDTM" in out, "no tcgen05.ld in SASS"
     # warp-level mma.sync only in the fused small-batch layer tail (6-21 weight rows per CTA: the dense
-    # GEMMs -- K1, prefill projections, decode projections -- are tcgen05), its bit-equality probe, and
-    # the causal prefill attention (off the timed decode path)
+    # GEMMs -- K1, prefill projections and attention, decode projections -- are tcgen05) and its
+    # bit-equality probe
     hmma_funcs = []
     for block in out.split("Function : ")[1:]:
         name = block.split("\n", 1)[0].strip()
         if "HMMA" in block.replace("UTCHMMA", ""):
             hmma_funcs.append(name)
-    assert hmma_funcs and all("layer_tail" in n or "mma_linear_probe" in n or "prefill_fa" in n for n in hmma_funcs), hmma_funcs
+    assert hmma_funcs and all("layer_tail" in n or "mma_linear_probe" in n for n in hmma_funcs), hmma_funcs
 
 
 def test_missing_library_fails_loudly(tmp_path):

@@ -34,7 +34,7 @@ def short(name):
 
 def main(path):
     seq = load(path)
-    last_prefill = max((i for i, (n, _) in enumerate(seq) if "prefill_attn" in n or "prefill_fa" in n), default=-1)
+    last_prefill = max((i for i, (n, _) in enumerate(seq) if "prefill_attn" in n or "prefill_fa" in n or "prefill_tc" in n), default=-1)
     regions = {"prefill+setup": seq[: last_prefill + 1], "decode": seq[last_prefill + 1:]}
     for name, part in regions.items():
         tot = defaultdict(float)

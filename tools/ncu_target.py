@@ -3,7 +3,7 @@
     ncu --set full -k regex:gemm_tcgen05 -c 1 python tools/ncu_target.py k1
     ncu --set full -k regex:decode_attn -c 1 python tools/ncu_target.py k2
     ncu --set full -k regex:gemm_tcgen05_kernel -c 1 python tools/ncu_target.py c1   # config-1 shapes
-    ncu --set full -k regex:prefill_fa -c 1 python tools/ncu_target.py prefill
+    ncu --set full -k regex:prefill_tc -c 1 python tools/ncu_target.py prefill
 """
 import sys
 
