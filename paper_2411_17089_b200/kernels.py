@@ -218,6 +218,16 @@ def decode_attention_kv4(q: torch.Tensor, kv_pages: torch.Tensor, qpages: torch.
 
 def prefill_attention(q: torch.Tensor, kv_pages: torch.Tensor, out: torch.Tensor, batch: int, heads: int,
                       head_dim: int, seq_len: int, scale: float | None = None, stream=None) -> torch.Tensor:
+    """Causal attention of positions [0, seq_len): q / out [pos][batch][heads * head_dim] and the pages
+    [pos][2][batch][heads * head_dim], all contiguous fp16 (the kernel's TMA maps assume those strides)."""
+    for t, name in ((q, "q"), (kv_pages, "kv_pages"), (out, "out")):
+        _need(t, torch.float16, name)
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    h = heads * head_dim
+    if q.numel() < seq_len * batch * h or out.numel() < seq_len * batch * h or kv_pages.numel() < seq_len * 2 * batch * h:
+        raise ValueError("prefill_attention: q / out need seq_len x batch x hidden and kv_pages seq_len x 2 x batch x "
+                         "hidden elements")
     if scale is None:
         scale = 1.0 / math.sqrt(head_dim)
     _lib.call(
