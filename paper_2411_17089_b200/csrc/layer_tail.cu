@@ -4,9 +4,10 @@
 // At batch <= 8 on a small model (BASELINE config 1: OPT-125M shape, b4) a decode layer moves
 // ~14 MB of weights and ~3 MB of KV: every kernel of the chain is a few microseconds of launch,
 // ramp and drain around well under a microsecond of streaming, and the chain of dependent launches,
-// not PCIe, sets the step time (profiles/r02s2_c1_sweep.jsonl: with no PCIe on the path at all the
-// layer still takes ~40 us).  Here the steps after the q/k/v projection run as stages of one grid
-// (one CTA per SM) separated by grid-wide barriers (~1 us each) instead of kernel boundaries:
+// not PCIe, set the step time (round-2 sweep: with no PCIe on the path at all the multi-kernel layer
+// still took ~40 us; profiles/r02_c1_modes.jsonl has the unfused chain beside this kernel).  Here the
+// steps after the q/k/v projection run as stages of one grid (one CTA per SM) separated by grid-wide
+// barriers (~1 us each) instead of kernel boundaries:
 //
 //   entry  each CTA bulk-copies ITS weight rows of all three projections (CTA c owns output columns
 //          [cN/G, (c+1)N/G) of each) into shared memory, so the weight stream runs under stage A
