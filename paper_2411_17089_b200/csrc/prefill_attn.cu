@@ -208,9 +208,13 @@ __global__ void __launch_bounds__(256, 1) prefill_tc_kernel(const __grid_constan
         for (int c = 0; c < kRows; ++c)
           if (j * kRows + c > row) s[c] = -INFINITY;
       }
-      float mx = m;
+      float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kRows; ++c) mx = fmaxf(mx, s[c]);  // finite: key j*128 <= row on every tile
+      for (int c = 0; c < kRows; ++c) mx = fmaxf(mx, s[c]);
+      // lazy rescaling: keep the running max unless this tile exceeds it by more than 2^8 (P <= 256
+      // stays exact enough in fp16 and O / l absorb the common factor), so most tiles after the first
+      // skip the O correction; the first tile always sets it (finite: key j*128 <= row on every tile)
+      mx = (mx > m + 8.f) ? mx : m;
       const float alpha = exp2f(m - mx);
       float sum = 0.f;
 #pragma unroll
