@@ -96,6 +96,37 @@ def test_grouped_dmas_bitwise(x_resident):
             assert torch.equal(a, c), k
 
 
+def test_decode_split_over_calls_bitwise():
+    """Nine steps as one decode() call, as 5 + 4 calls, and as nine single-step calls (the e2e path)
+    give the same tokens, logits and host stores: the executor's event rings, grouped KV copies and
+    staging buffers carry no state across calls that changes the result (12 layers, fused tail,
+    KV tails in groups of 4)."""
+    cfg = OPTConfig(hidden=256, layers=12, heads=4, ffn=1024, vocab=1024, max_pos=256)
+    b, S0 = 4, 70
+    splits = [35, 71, 0, 73, 10, 75, 74, 1, 40]
+    w = OPTWeights.random(cfg, seed=45, device="cuda", std=0.1, emb_std=0.1)
+    prompt = torch.randint(0, cfg.vocab, (b, S0), generator=torch.Generator().manual_seed(46))
+    outs = []
+    for parts in ([9], [5, 4], [1] * 9):
+        rt = KVPRRuntime(w, b, S0 + len(splits) + 1)
+        assert rt.fused_tail and rt.dma_group == 4
+        tok = rt.prefill(prompt)
+        toks, logits, i = [], [], 0
+        for n in parts:
+            t = rt.decode(splits[i:i + n], tokens=tok, keep_logits=True)
+            toks.append(t)
+            logits.append(rt.last_logits[-1].clone())  # [steps, batch, vocab] of this call: its last step
+            tok = t[-1]
+            i += n
+        torch.cuda.synchronize()
+        n = S0 + len(splits)
+        outs.append((torch.cat(toks).cpu(), logits[-1].cpu(), rt.stores.kv[:, :n].clone(), rt.stores.x[:, :n].clone()))
+        rt.close()
+    for k, o in enumerate(outs[1:], start=1):
+        for a, c in zip(outs[0], o):
+            assert torch.equal(a, c), k
+
+
 def test_native_loop_cuts_host_time():
     """Config-1 geometry is host bound under the Python loop; the executor issues a step far faster."""
     cfg = OPTConfig(hidden=768, layers=12, heads=12, ffn=3072)
