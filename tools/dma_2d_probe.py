@@ -76,7 +76,18 @@ def main():
         torch.cuda.synchronize()
         out[name] = round(e0.elapsed_time(e1) * 1e3 / (reps * L), 3)
 
+    def split_rows(rows):  # one layer's X as ONE 2-D submission of `rows` contiguous rows (pitch = width)
+        w = X // rows
+
+        def body():
+            for j in range(L):
+                _lib.call("kvpr_copy_2d_async", dx.data_ptr() + j * DP, w, hx.data_ptr() + j * HP, w, w, rows,
+                          s.cuda_stream)
+        return body
+
     for _ in range(2):
+        for rows in (1, 4, 16, 64):
+            timed(f"x_rows{rows}_us", split_rows(rows))
         timed2("x_2streams_us", two_streams(X, 0))
         timed2("x_kv_2streams_us", two_streams(X, KV))
         for g in (1, 2, 3, 4, 6, 12):
