@@ -11,7 +11,7 @@ timeout 900 $CS --tool racecheck --print-limit 20 python -m pytest tests/test_nu
 echo "## synccheck: stream-K decode GEMM"
 timeout 900 $CS --tool synccheck --print-limit 20 python -m pytest tests/test_kernels_gpu.py -q -k "stream_k" 2>&1 | tail -6
 echo "## memcheck: executor + runtime (decode pipeline, full-size tests excluded)"
-timeout 1500 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_executor_gpu.py tests/test_runtime_gpu.py -q -k "not full_size" 2>&1 | tail -6
+timeout 1500 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_executor_gpu.py tests/test_runtime_gpu.py -q -k "not full_size and not host_time" 2>&1 | tail -6
 echo "## racecheck + memcheck: tensor-core prefill attention, fused layer tail"
 timeout 900 $CS --tool racecheck --print-limit 20 python -m pytest tests/test_kernels_gpu.py -q -k "prefill" 2>&1 | tail -4
 timeout 900 $CS --tool memcheck --print-limit 20 python -m pytest tests/test_kernels_gpu.py -q -k "prefill" 2>&1 | tail -4
