@@ -33,7 +33,10 @@ import csv
 import heapq
 import json
 import math
+import os
 from dataclasses import dataclass, field
+
+import numpy as np
 from enum import Enum
 
 from .costmodel import (ModelSpec, WorkloadSpec, activation_bytes, decode_step_flops, kv_remainder_bytes,
@@ -350,7 +353,7 @@ def task_durations(graph: TaskGraph, profile: HardwareProfile) -> list[float]:
     return out
 
 
-def run_schedule(resource, duration, priority, deps, n_resources: int = 3) -> tuple[list[float], list[float]]:
+def _list_schedule(resource, duration, priority, deps, n_resources: int = 3) -> tuple[list[float], list[float]]:
     """Non-preemptive list scheduling (_engine_py.py:18-90): whenever a lane is idle it starts the ready
     task with the smallest (priority, id); all lanes finishing at the same instant complete before the
     next dispatch.  deps[i] = task ids task i waits for.  Returns (start, end) per task."""
@@ -396,6 +399,49 @@ def run_schedule(resource, duration, priority, deps, n_resources: int = 3) -> tu
     return start, end
 
 
+# engine selection (engine.py:45-76): only the pure-Python engine is restated, which the reference keeps
+# identical to its compiled twin; KVOVERLAP_ENGINE / engine= behave as in a reference build without the
+# extension ("c" is an error)
+_ENGINE_ENV = "KVOVERLAP_ENGINE"
+
+
+def available_engines() -> tuple[str, ...]:
+    return ("py",)
+
+
+def active_engine() -> str:
+    forced = os.environ.get(_ENGINE_ENV, "").strip().lower()
+    if forced:
+        if forced not in ("py", "c"):
+            raise ValueError(f"{_ENGINE_ENV} must be 'py' or 'c', got {forced!r}")
+        if forced == "c":
+            raise RuntimeError("KVOVERLAP_ENGINE=c but the compiled engine is not built")
+        return forced
+    return "py"
+
+
+def _engine(engine: str | None) -> None:
+    name = engine if engine is not None else active_engine()
+    if name == "c":
+        raise RuntimeError("compiled engine requested but not built")
+    if name != "py":
+        raise ValueError(f"unknown engine {name!r}")
+
+
+def run_schedule(resource, duration, priority, dep_indptr, dep_indices, n_resources: int, engine: str | None = None):
+    """The reference's engine entry point (engine.py:61-76, _engine_py.py:18-90): dependencies as CSR
+    (task i waits for dep_indices[dep_indptr[i]:dep_indptr[i+1]]); returns (start, end) float64 arrays."""
+    _engine(engine)
+    n = len(resource)
+    indptr = np.asarray(dep_indptr, dtype=np.int64).tolist()
+    indices = np.asarray(dep_indices, dtype=np.int64).tolist()
+    deps = [indices[indptr[i]:indptr[i + 1]] for i in range(n)]
+    start, end = _list_schedule(np.asarray(resource, dtype=np.int64).tolist(),
+                                np.asarray(duration, dtype=np.float64).tolist(),
+                                np.asarray(priority, dtype=np.int64).tolist(), deps, n_resources)
+    return np.asarray(start, dtype=np.float64), np.asarray(end, dtype=np.float64)
+
+
 def _bins(spans, makespan: float, bins: int) -> tuple[tuple[float, float], ...]:
     """GPU-lane busy fraction per equal-width bin (engine.py:122-137)."""
     if makespan <= 0 or not math.isfinite(makespan) or bins <= 0:
@@ -411,14 +457,15 @@ def _bins(spans, makespan: float, bins: int) -> tuple[tuple[float, float], ...]:
     return tuple(((b + 0.5) * width, min(1.0, busy[b] / width)) for b in range(bins))
 
 
-def simulate(graph: TaskGraph, profile: HardwareProfile, *, bins: int = 100, check: bool = True,
-             durations: list[float] | None = None) -> tuple[Timeline, SimReport]:
+def simulate(graph: TaskGraph, profile: HardwareProfile, *, engine: str | None = None, bins: int = 100,
+             check: bool = True, durations: list[float] | None = None) -> tuple[Timeline, SimReport]:
     """(Timeline, SimReport) of the graph under the profile (engine.py:140-204).  ``durations``
     overrides the profile's per-task durations (e.g. measured ones: replaying a measured run through
     the same DAG and scheduler)."""
+    _engine(engine)
     tasks = graph.tasks
     dur = list(durations) if durations is not None else task_durations(graph, profile)
-    start, end = run_schedule([RESOURCE_INDEX[t.resource] for t in tasks], dur, [t.priority for t in tasks],
+    start, end = _list_schedule([RESOURCE_INDEX[t.resource] for t in tasks], dur, [t.priority for t in tasks],
                               [t.deps for t in tasks])
     if check:
         check_schedule(graph, start, end)
@@ -509,14 +556,15 @@ def plan_for_policy(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile,
     return constant_plan(wl, policy.schedule, 0)
 
 
-def compare(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile, policies, gpu_mem_budget=None) -> list[dict]:
+def compare(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile, policies, gpu_mem_budget=None,
+            engine: str | None = None) -> list[dict]:
     """Simulate each (label, Policy) on one config; rows carry speedup_vs_first (trace.py:88-110)."""
     if not policies:
         raise ValueError("need at least one policy")
     rows, base = [], None
     for label, policy in policies:
         plan = plan_for_policy(spec, wl, profile, policy)
-        _, rep = simulate(build_task_graph(spec, wl, profile, plan, policy, gpu_mem_budget), profile)
+        _, rep = simulate(build_task_graph(spec, wl, profile, plan, policy, gpu_mem_budget), profile, engine=engine)
         row = metrics_row(label, policy, rep)
         if base is None:
             base = rep.makespan

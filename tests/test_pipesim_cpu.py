@@ -137,5 +137,9 @@ def test_errors_match_reference():
         ps.build_task_graph(spec, wl, prof, plan, ps.Policy("row"), gpu_mem_budget=1.0)
     with pytest.raises(ValueError):
         ps.Policy("diagonal")
-    with pytest.raises(ps.DependencyCycleError):
-        ps.run_schedule([0, 0], [1.0, 1.0], [0, 0], [(1,), (0,)])
+    with pytest.raises(ps.DependencyCycleError):  # the reference's CSR form: task 0 waits for 1, 1 for 0
+        ps.run_schedule([0, 0], [1.0, 1.0], [0, 0], [0, 1, 2], [1, 0], 3)
+    with pytest.raises(RuntimeError):
+        ps.simulate(ps.build_task_graph(spec, wl, prof, constant_plan(wl, "row", 0), ps.Policy("row")), prof,
+                    engine="c")
+    assert ps.available_engines() == ("py",) and ps.active_engine() == "py"
