@@ -55,6 +55,7 @@ extern "C" {
 #define KVPR_OK 0
 #define KVPR_EINVAL 1
 #define KVPR_ECUDA 2
+#define KVPR_ECYCLE 3 /* kvpr_list_schedule: the dependency graph has a cycle */
 
 /* epilogue flags for kvpr_linear */
 #define KVPR_EPI_RELU 1  /* max(0, .) after bias */
@@ -337,6 +338,14 @@ int kvpr_decoder_kernel_stats(void* handle, int kind, int* launches, double* mea
 int kvpr_decoder_timeline(void* handle, float* layer_ms, int layer_cap, float* step_ms, int step_cap);
 /* Kernel launches (ABI-level) the executor has issued so far. */
 long long kvpr_decoder_launches(void* handle);
+
+/* Compiled engine of the pipeline simulator (kvoverlap.pipesim's _engine.pyx, engine.py:45-76): list
+ * scheduling of n tasks onto n_resources exclusive lanes, dependencies as CSR (task i waits for
+ * dep_indices[dep_indptr[i] .. dep_indptr[i+1])); fills start / end.  Host code, no GPU.  Returns
+ * KVPR_ECYCLE when some tasks never become ready. */
+int kvpr_list_schedule(long long n, const long long* resource, const double* duration, const long long* priority,
+                       const long long* dep_indptr, const long long* dep_indices, int n_resources, double* start,
+                       double* end);
 
 /* ---------------------------------------------------------------------------------------------
  * Fused tensor-parallel projection + all-reduce over peer memory (config 4: head-sharded OPT-30B;

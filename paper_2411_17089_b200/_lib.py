@@ -19,6 +19,7 @@ LIB_PATH = _PKG / "libkvpr.so"
 KVPR_OK = 0
 KVPR_EINVAL = 1
 KVPR_ECUDA = 2
+KVPR_ECYCLE = 3
 
 EPI_RELU = 1
 EPI_F32 = 2
@@ -47,6 +48,7 @@ EXPORTS = (
     "kvpr_copy_async",
     "kvpr_copy_batch_async",
     "kvpr_copy_2d_async",
+    "kvpr_list_schedule",
     "kvpr_kv4_page_bytes",
     "kvpr_kv4_quantize",
     "kvpr_kv4_dequantize",
@@ -153,6 +155,7 @@ _SIGS = {
     "kvpr_copy_async": ([_vp, _vp, _sz, _vp], _i),
     "kvpr_copy_batch_async": ([ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_sz), _sz, _vp], _i),
     "kvpr_copy_2d_async": ([_vp, _sz, _vp, _sz, _sz, _sz, _vp], _i),
+    "kvpr_list_schedule": ([ctypes.c_longlong] + [_vp] * 5 + [_i, _vp, _vp], _i),
     "kvpr_kv4_page_bytes": ([_i, _i], _sz),
     "kvpr_kv4_quantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),
     "kvpr_kv4_dequantize": ([_vp, _vp, _i, _i, _i, _i, _vp], _i),

@@ -17,7 +17,7 @@ CSRC = Path(__file__).resolve().parent
 PKG = CSRC.parent
 ROOT = PKG.parent
 LIB = PKG / "libkvpr.so"
-SOURCES = ["abi.cu", "gemm_tcgen05.cu", "attention.cu", "elementwise.cu", "kvquant.cu", "executor.cu", "tpcomm.cu", "gemv.cu", "layer_tail.cu", "prefill_attn.cu"]
+SOURCES = ["abi.cu", "gemm_tcgen05.cu", "attention.cu", "elementwise.cu", "kvquant.cu", "executor.cu", "tpcomm.cu", "gemv.cu", "layer_tail.cu", "prefill_attn.cu", "sched_engine.cu"]
 HEADERS = ["common.cuh", "kvpr_internal.h", "attn_common.cuh"]
 
 NVCC_FLAGS = [

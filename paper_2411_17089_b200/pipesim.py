@@ -399,39 +399,74 @@ def _list_schedule(resource, duration, priority, deps, n_resources: int = 3) -> 
     return start, end
 
 
-# engine selection (engine.py:45-76): only the pure-Python engine is restated, which the reference keeps
-# identical to its compiled twin; KVOVERLAP_ENGINE / engine= behave as in a reference build without the
-# extension ("c" is an error)
+# engine selection (engine.py:45-76): the pure-Python engine (`_list_schedule`) and the compiled one,
+# `kvpr_list_schedule` in libkvpr (csrc/sched_engine.cu, the counterpart of the reference's _engine.pyx;
+# identical schedules).  As in the reference: "c" when the library loads, KVOVERLAP_ENGINE=py|c forces one
+# side, forcing "c" without it is an error.
 _ENGINE_ENV = "KVOVERLAP_ENGINE"
 
 
+def _c_available() -> bool:
+    try:
+        from . import _lib
+
+        _lib.load()
+        return True
+    except (OSError, RuntimeError):
+        return False
+
+
 def available_engines() -> tuple[str, ...]:
-    return ("py",)
+    return ("py", "c") if _c_available() else ("py",)
 
 
 def active_engine() -> str:
+    """Engine simulate() uses right now, honouring the environment override."""
     forced = os.environ.get(_ENGINE_ENV, "").strip().lower()
     if forced:
         if forced not in ("py", "c"):
             raise ValueError(f"{_ENGINE_ENV} must be 'py' or 'c', got {forced!r}")
-        if forced == "c":
+        if forced == "c" and not _c_available():
             raise RuntimeError("KVOVERLAP_ENGINE=c but the compiled engine is not built")
         return forced
-    return "py"
+    return "c" if _c_available() else "py"
 
 
-def _engine(engine: str | None) -> None:
+def _engine(engine: str | None) -> str:
     name = engine if engine is not None else active_engine()
-    if name == "c":
+    if name == "c" and not _c_available():
         raise RuntimeError("compiled engine requested but not built")
-    if name != "py":
+    if name not in ("py", "c"):
         raise ValueError(f"unknown engine {name!r}")
+    return name
+
+
+def _run_c(resource, duration, priority, indptr, indices, n_resources: int):
+    import ctypes
+
+    from . import _lib
+
+    res = np.ascontiguousarray(resource, dtype=np.int64)
+    dur = np.ascontiguousarray(duration, dtype=np.float64)
+    pri = np.ascontiguousarray(priority, dtype=np.int64)
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int64)
+    n = len(res)
+    start, end = np.zeros(n, dtype=np.float64), np.zeros(n, dtype=np.float64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p) if a.size else None  # noqa: E731
+    rc = _lib.load().kvpr_list_schedule(n, ptr(res), ptr(dur), ptr(pri), ptr(ip), ptr(ix), int(n_resources),
+                                        ptr(start), ptr(end))
+    if rc == _lib.KVPR_ECYCLE:
+        raise DependencyCycleError(_lib.last_error())
+    _lib.check(rc, "kvpr_list_schedule")
+    return start, end
 
 
 def run_schedule(resource, duration, priority, dep_indptr, dep_indices, n_resources: int, engine: str | None = None):
     """The reference's engine entry point (engine.py:61-76, _engine_py.py:18-90): dependencies as CSR
     (task i waits for dep_indices[dep_indptr[i]:dep_indptr[i+1]]); returns (start, end) float64 arrays."""
-    _engine(engine)
+    if _engine(engine) == "c":
+        return _run_c(resource, duration, priority, dep_indptr, dep_indices, n_resources)
     n = len(resource)
     indptr = np.asarray(dep_indptr, dtype=np.int64).tolist()
     indices = np.asarray(dep_indices, dtype=np.int64).tolist()
@@ -462,11 +497,18 @@ def simulate(graph: TaskGraph, profile: HardwareProfile, *, engine: str | None =
     """(Timeline, SimReport) of the graph under the profile (engine.py:140-204).  ``durations``
     overrides the profile's per-task durations (e.g. measured ones: replaying a measured run through
     the same DAG and scheduler)."""
-    _engine(engine)
+    name = _engine(engine)
     tasks = graph.tasks
     dur = list(durations) if durations is not None else task_durations(graph, profile)
-    start, end = _list_schedule([RESOURCE_INDEX[t.resource] for t in tasks], dur, [t.priority for t in tasks],
-                              [t.deps for t in tasks])
+    res, pri = [RESOURCE_INDEX[t.resource] for t in tasks], [t.priority for t in tasks]
+    if name == "c":
+        indptr = np.zeros(len(tasks) + 1, dtype=np.int64)
+        indptr[1:] = np.cumsum([len(t.deps) for t in tasks])
+        indices = np.fromiter((d for t in tasks for d in t.deps), dtype=np.int64, count=int(indptr[-1]))
+        s_arr, e_arr = _run_c(res, dur, pri, indptr, indices, len(RESOURCE_INDEX))
+        start, end = s_arr.tolist(), e_arr.tolist()
+    else:
+        start, end = _list_schedule(res, dur, pri, [t.deps for t in tasks])
     if check:
         check_schedule(graph, start, end)
     n = len(tasks)

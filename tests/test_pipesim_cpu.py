@@ -137,9 +137,33 @@ def test_errors_match_reference():
         ps.build_task_graph(spec, wl, prof, plan, ps.Policy("row"), gpu_mem_budget=1.0)
     with pytest.raises(ValueError):
         ps.Policy("diagonal")
-    with pytest.raises(ps.DependencyCycleError):  # the reference's CSR form: task 0 waits for 1, 1 for 0
-        ps.run_schedule([0, 0], [1.0, 1.0], [0, 0], [0, 1, 2], [1, 0], 3)
-    with pytest.raises(RuntimeError):
+    for engine in ps.available_engines():  # the reference's CSR form: task 0 waits for 1, 1 for 0
+        with pytest.raises(ps.DependencyCycleError):
+            ps.run_schedule([0, 0], [1.0, 1.0], [0, 0], [0, 1, 2], [1, 0], 3, engine=engine)
+    with pytest.raises(ValueError):
         ps.simulate(ps.build_task_graph(spec, wl, prof, constant_plan(wl, "row", 0), ps.Policy("row")), prof,
-                    engine="c")
-    assert ps.available_engines() == ("py",) and ps.active_engine() == "py"
+                    engine="fortran")
+
+
+def test_compiled_engine_bit_identical():
+    """The compiled engine (kvpr_list_schedule, csrc/sched_engine.cu) schedules exactly like the Python one:
+    every golden case's timeline and report, and 200 random DAGs with tied priorities and durations."""
+    assert ps.available_engines() == ("py", "c") and ps.active_engine() == "c"
+    for c in CASES:
+        spec, wl, prof, pol, plan = _plan(c)
+        g = ps.build_task_graph(spec, wl, prof, plan, pol)
+        assert ps.simulate(g, prof, engine="py") == ps.simulate(g, prof, engine="c")
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n = int(rng.integers(0, 150))
+        res = rng.integers(0, 3, size=n)
+        dur = rng.integers(0, 4, size=n) * 0.25  # ties in completion times
+        pri = rng.integers(0, 10, size=n)        # ties in priority: id breaks them
+        deps = [rng.choice(i, size=int(rng.integers(0, min(i, 4) + 1)), replace=False) if i else np.empty(0, int)
+                for i in range(n)]
+        indptr = np.zeros(n + 1, dtype=np.int64)
+        indptr[1:] = np.cumsum([len(d) for d in deps])
+        idx = np.concatenate(deps).astype(np.int64) if n else np.empty(0, np.int64)
+        a = ps.run_schedule(res, dur, pri, indptr, idx, 3, engine="py")
+        b = ps.run_schedule(res, dur, pri, indptr, idx, 3, engine="c")
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
