@@ -28,8 +28,8 @@ int kvpr_list_schedule(long long n, const long long* resource, const double* dur
     return KVPR_EINVAL;
   }
   if (n == 0) return KVPR_OK;
-  std::vector<long long> indeg(n);
-  std::vector<std::vector<long long>> children(n);
+  // children of every task as CSR (two passes, no per-task allocation)
+  std::vector<long long> indeg(n), child_ptr(n + 1, 0);
   for (long long i = 0; i < n; ++i) {
     if (resource[i] < 0 || resource[i] >= n_resources || dep_indptr[i + 1] < dep_indptr[i]) {
       kvpr::set_error("list_schedule: task %lld has resource %lld or a bad dependency range", i, resource[i]);
@@ -42,48 +42,68 @@ int kvpr_list_schedule(long long n, const long long* resource, const double* dur
         kvpr::set_error("list_schedule: task %lld depends on %lld (out of range)", i, d);
         return KVPR_EINVAL;
       }
-      children[d].push_back(i);
+      ++child_ptr[d + 1];
     }
   }
-  using Key = std::pair<long long, long long>;  // (priority, id): Python's heapq order on tuples
-  std::vector<std::priority_queue<Key, std::vector<Key>, std::greater<Key>>> ready(n_resources);
+  for (long long i = 0; i < n; ++i) child_ptr[i + 1] += child_ptr[i];
+  std::vector<long long> child(child_ptr[n]), fill(child_ptr.begin(), child_ptr.end() - 1);
   for (long long i = 0; i < n; ++i)
-    if (indeg[i] == 0) ready[resource[i]].push({priority[i], i});
-  std::vector<long long> running_id(n_resources, -1);
+    for (long long p = dep_indptr[i]; p < dep_indptr[i + 1]; ++p) child[fill[dep_indices[p]]++] = i;
+  // ready queues ordered by (priority, id): one packed int64 key priority * n + id when the priorities
+  // fit (as the reference's compiled engine does), else (priority, id) pairs -- the same order
+  long long pmin = priority[0], pmax = priority[0];
+  for (long long i = 1; i < n; ++i) {
+    pmin = priority[i] < pmin ? priority[i] : pmin;
+    pmax = priority[i] > pmax ? priority[i] : pmax;
+  }
+  const bool packed = pmin >= 0 && pmax <= (1LL << 62) / n;
   std::vector<double> running_end(n_resources, 0.0);
+  std::vector<long long> running_id(n_resources, -1);
   long long completed = 0;
-  auto dispatch = [&](double now) {
-    for (int r = 0; r < n_resources; ++r) {
-      if (running_id[r] < 0 && !ready[r].empty()) {
-        const long long i = ready[r].top().second;
-        ready[r].pop();
-        start[i] = now;
-        end[i] = now + duration[i];
-        running_id[r] = i;
-        running_end[r] = end[i];
+  auto run = [&](auto& ready, auto key, auto id_of) {
+    for (long long i = 0; i < n; ++i)
+      if (indeg[i] == 0) ready[resource[i]].push(key(i));
+    auto dispatch = [&](double now) {
+      for (int r = 0; r < n_resources; ++r) {
+        if (running_id[r] < 0 && !ready[r].empty()) {
+          const long long i = id_of(ready[r].top());
+          ready[r].pop();
+          start[i] = now;
+          end[i] = now + duration[i];
+          running_id[r] = i;
+          running_end[r] = end[i];
+        }
       }
+    };
+    dispatch(0.0);
+    for (;;) {
+      bool any = false;
+      double t = 0.0;
+      for (int r = 0; r < n_resources; ++r)
+        if (running_id[r] >= 0 && (!any || running_end[r] < t)) {
+          t = running_end[r];
+          any = true;
+        }
+      if (!any) break;
+      for (int r = 0; r < n_resources; ++r) {
+        if (running_id[r] >= 0 && running_end[r] == t) {
+          const long long i = running_id[r];
+          running_id[r] = -1;
+          ++completed;
+          for (long long p = child_ptr[i]; p < child_ptr[i + 1]; ++p)
+            if (--indeg[child[p]] == 0) ready[resource[child[p]]].push(key(child[p]));
+        }
+      }
+      dispatch(t);
     }
   };
-  dispatch(0.0);
-  for (;;) {
-    bool any = false;
-    double t = 0.0;
-    for (int r = 0; r < n_resources; ++r)
-      if (running_id[r] >= 0 && (!any || running_end[r] < t)) {
-        t = running_end[r];
-        any = true;
-      }
-    if (!any) break;
-    for (int r = 0; r < n_resources; ++r) {
-      if (running_id[r] >= 0 && running_end[r] == t) {
-        const long long i = running_id[r];
-        running_id[r] = -1;
-        ++completed;
-        for (long long c : children[i])
-          if (--indeg[c] == 0) ready[resource[c]].push({priority[c], c});
-      }
-    }
-    dispatch(t);
+  if (packed) {
+    std::vector<std::priority_queue<long long, std::vector<long long>, std::greater<long long>>> ready(n_resources);
+    run(ready, [&](long long i) { return priority[i] * n + i; }, [&](long long k) { return k % n; });
+  } else {
+    using Key = std::pair<long long, long long>;
+    std::vector<std::priority_queue<Key, std::vector<Key>, std::greater<Key>>> ready(n_resources);
+    run(ready, [&](long long i) { return Key(priority[i], i); }, [](const Key& k) { return k.second; });
   }
   if (completed != n) {
     kvpr::set_error("%lld of %lld tasks never became ready", n - completed, n);

@@ -341,15 +341,15 @@ def build_task_graph(spec: ModelSpec, wl: WorkloadSpec, profile: HardwareProfile
 # ---------------------------------------------------------------------------
 # engine
 
-def task_durations(graph: TaskGraph, profile: HardwareProfile) -> list[float]:
-    """Seconds per task: FLOPs / effective rate on the gpu lane, latency + bytes / bandwidth on the
-    copy lanes (engine.py:81-90)."""
-    out = []
+def task_durations(graph: TaskGraph, profile: HardwareProfile) -> np.ndarray:
+    """Seconds per task (float64 array, as the reference returns): FLOPs / effective rate on the gpu lane,
+    latency + bytes / bandwidth on the copy lanes (engine.py:79-90)."""
+    out = np.empty(len(graph), dtype=np.float64)
     for tk in graph.tasks:
         if tk.resource is Resource.GPU:
-            out.append(compute_time(profile, tk.cost))
+            out[tk.id] = compute_time(profile, tk.cost)
         else:
-            out.append(transfer_time(profile, tk.cost, tk.resource.value))
+            out[tk.id] = transfer_time(profile, tk.cost, tk.resource.value)
     return out
 
 
@@ -441,6 +441,14 @@ def _engine(engine: str | None) -> str:
     return name
 
 
+def _dep_csr(graph: TaskGraph) -> tuple[np.ndarray, np.ndarray]:
+    """The graph's dependencies as CSR arrays (engine.py:92-100)."""
+    indptr = np.zeros(len(graph) + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum([len(t.deps) for t in graph.tasks])
+    indices = np.fromiter((d for t in graph.tasks for d in t.deps), dtype=np.int64, count=int(indptr[-1]))
+    return indptr, indices
+
+
 def _run_c(resource, duration, priority, indptr, indices, n_resources: int):
     import ctypes
 
@@ -499,13 +507,10 @@ def simulate(graph: TaskGraph, profile: HardwareProfile, *, engine: str | None =
     the same DAG and scheduler)."""
     name = _engine(engine)
     tasks = graph.tasks
-    dur = list(durations) if durations is not None else task_durations(graph, profile)
+    dur = list(durations) if durations is not None else task_durations(graph, profile).tolist()
     res, pri = [RESOURCE_INDEX[t.resource] for t in tasks], [t.priority for t in tasks]
     if name == "c":
-        indptr = np.zeros(len(tasks) + 1, dtype=np.int64)
-        indptr[1:] = np.cumsum([len(t.deps) for t in tasks])
-        indices = np.fromiter((d for t in tasks for d in t.deps), dtype=np.int64, count=int(indptr[-1]))
-        s_arr, e_arr = _run_c(res, dur, pri, indptr, indices, len(RESOURCE_INDEX))
+        s_arr, e_arr = _run_c(res, dur, pri, *_dep_csr(graph), len(RESOURCE_INDEX))
         start, end = s_arr.tolist(), e_arr.tolist()
     else:
         start, end = _list_schedule(res, dur, pri, [t.deps for t in tasks])

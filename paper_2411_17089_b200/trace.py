@@ -232,7 +232,7 @@ def compare_with_model(entries: list[Entry], spec, wl, profile, plan, schedule: 
     pol = ps.Policy(schedule, True)
     graph = ps.build_task_graph(spec, wl, profile, plan, pol)
     tl, rep = ps.simulate(graph, profile)
-    sim_dur = ps.task_durations(graph, profile)
+    sim_dur = ps.task_durations(graph, profile).tolist()
     meas: dict[tuple[str, int, int], float] = {}
     for e in entries:
         key = (e.kind, e.step, e.layer)
