@@ -1,0 +1,4 @@
+from paper_2411_17089_b200.scheduler import *  # noqa: F401,F403
+from paper_2411_17089_b200 import scheduler as _m
+
+globals().update({k: v for k, v in vars(_m).items() if not k.startswith("__")})

@@ -42,3 +42,22 @@ def test_reference_suite_passes_against_this_package(criterion):
     ok = out.returncode == 0 and "failed" not in tail and passed >= 145
     assert criterion("R1", f"the reference's own tests ({', '.join(FILES)}) against this package: {tail}", ok), \
         out.stdout[-3000:]
+
+
+@pytest.mark.skipif(not REF_TESTS.is_dir(), reason="reference test suite not present (GPU box)")
+def test_reference_numerics_tests_pin_the_oracle(criterion):
+    """The reference's own fp64 numerics tests (test_numerics.py, acceptance criterion 07: split rebuild
+    exact within 1e-12 over 1008 randomized checks) run against oracle/numerics_ref.py through
+    tests/refshim_oracle -- the oracle every GPU parity test is judged against passes the reference's
+    own exactness tests, beside the npz goldens (tests/test_oracle_cpu.py)."""
+    shim = ROOT / "tests" / "refshim_oracle"
+    env = dict(os.environ, PYTHONPATH=f"{shim}{os.pathsep}{ROOT}")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                          str(REF_TESTS / "test_numerics.py"),
+                          str(REF_TESTS / "test_acceptance.py") + "::test_criterion_07_split_rebuild_is_exact"],
+                         capture_output=True, text=True, env=env, cwd=ROOT, timeout=600)
+    tail = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-500:]
+    m = re.search(r"(\d+) passed", tail)
+    ok = out.returncode == 0 and "failed" not in tail and m is not None and int(m.group(1)) >= 15
+    assert criterion("R2", f"the reference's numerics tests (test_numerics.py + criterion 07) against the oracle: "
+                           f"{tail}", ok), out.stdout[-3000:]
