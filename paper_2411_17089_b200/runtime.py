@@ -162,12 +162,15 @@ class KVPRRuntime:
         # small layers (a whole X store under 8 MB): the KV tails of G consecutive layers go as one strided
         # DMA (native executor); a ~0.1 MB tail is ~1.8 us of PCIe but ~3.7 us of copy-engine overhead on
         # its own (profiles/r02_dma_2d_probe.json).  X stays one DMA per layer.  G divides the layers
-        # (layers >= 2G), G buffers per group in flight twice over (nbuf >= 2G).  KVPR_DMA_GROUP overrides.
+        # (layers >= 2G), G buffers per group in flight twice over (nbuf >= 2G); the smallest G wins (config
+        # 1, medians of 5: G 1 / 2 / 3 / 4 = 0.511 / 0.473 / 0.477 / 0.483 ms per step,
+        # profiles/r02_c1_dma_group.jsonl: larger groups hold the first layer's K2 for the group's copy).
+        # KVPR_DMA_GROUP overrides.
         if dma_group is None:
             dma_group = int(os.environ.get("KVPR_DMA_GROUP", -1))
         if dma_group < 0:
             small = capacity * batch * cfg.hidden * 2 < (8 << 20)
-            dma_group = next((g for g in (4, 3, 2) if small and cfg.layers % g == 0 and cfg.layers >= 2 * g), 1)
+            dma_group = next((g for g in (2, 3, 4) if small and cfg.layers % g == 0 and cfg.layers >= 2 * g), 1)
         self.dma_group = max(1, dma_group)
         if self.dma_group > 1:
             nbuf = self.dma_group * max(2, -(-nbuf // self.dma_group))

@@ -100,7 +100,7 @@ def test_decode_split_over_calls_bitwise():
     """Nine steps as one decode() call, as 5 + 4 calls, and as nine single-step calls (the e2e path)
     give the same tokens, logits and host stores: the executor's event rings, grouped KV copies and
     staging buffers carry no state across calls that changes the result (12 layers, fused tail,
-    KV tails in groups of 4)."""
+    KV tails in groups of 2)."""
     cfg = OPTConfig(hidden=256, layers=12, heads=4, ffn=1024, vocab=1024, max_pos=256)
     b, S0 = 4, 70
     splits = [35, 71, 0, 73, 10, 75, 74, 1, 40]
@@ -109,7 +109,7 @@ def test_decode_split_over_calls_bitwise():
     outs = []
     for parts in ([9], [5, 4], [1] * 9):
         rt = KVPRRuntime(w, b, S0 + len(splits) + 1)
-        assert rt.fused_tail and rt.dma_group == 4
+        assert rt.fused_tail and rt.dma_group == 2
         tok = rt.prefill(prompt)
         toks, logits, i = [], [], 0
         for n in parts:
