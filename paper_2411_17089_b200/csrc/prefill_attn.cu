@@ -6,15 +6,15 @@
 // numerics.decode_attention (numerics.py:166-191) applies per position.  Off the timed decode path
 // (the reference prices it nowhere: pipesim models decode layers only), but it gates long-prompt
 // runs (config 5, prompt 8192): the CUDA-core kernel of round 1 spent 36 ms per OPT-6.7B layer at
-// b32 s1024, a warp-MMA (mma.sync) flash kernel 1.27 ms, this one 0.67 ms
-// (profiles/r02_prefill_bench.jsonl).
+// b32 s1024, a warp-MMA (mma.sync) flash kernel 1.27 ms, a one-query-tile tcgen05 version 0.67 ms, this
+// two-tile ping-pong 0.50 ms (profiles/r02_prefill_bench.jsonl).
 //
 // Layout (runtime.py prefill): q rows [pos][b][hidden]; KV pages [pos][2][b][hidden] -- one
 // (sequence, head) row of K or V is head_dim contiguous halves, rows of consecutive positions are
 // b*hidden (q) or 2*b*hidden (K, V) halves apart: 3-D TMA maps (h, b or 2b, pos) cut 64-column x
 // 128-position boxes straight out of them.  The output goes to [pos][b][hidden] like q.
 //
-// One CTA per (128-query tile, sequence, head), heaviest (last) query tiles first.
+// One CTA per (pair of 128-query tiles, sequence, head), heaviest (last) pairs first.
 #include <math.h>
 #include <stdlib.h>
 
@@ -24,30 +24,36 @@
 namespace kvpr {
 namespace {
 
-// Warp roles (256 threads): w0 = TMA producer, w1 = MMA issuer (one elected lane), w2 = TMEM
-// allocator, w4..w7 = softmax / O correction / epilogue with thread t <-> TMEM lane t <-> query row
-// q0 + t (a whole S row per thread: max and sum need no shuffles).  Per key tile j:
-//   MMA    S_j = Q K_j^T -> TMEM S[j % 2]                      (commit sfull[j % 2])
-//          after P_{j-1} is in smem: O += P_{j-1} V_{j-1}      (commit pvdone, kvempty)
-//   softmax  S_j -> registers, scale, causal mask, row max m', p = exp2(s - m'), row sum;
-//          after pvdone(j-1): O *= exp2(m - m') in TMEM if the max moved, P_j -> smem (fp16,
-//          K-major SW128) -> arrive pfull
-// so S_{j+1} runs on the tensor core while the softmax of S_j runs, and P V of tile j while the
-// softmax of tile j+1 computes its row statistics.  Q, K, V by TMA (3-D maps over the [pos][b][h]
-// and [pos][2][b][h] layouts, 128-row boxes, zero fill past seq_len); V is read MN-major (the
-// instruction's B-transpose bit), P V's A operand is P in shared memory.
+// Two query tiles per CTA, ping-ponged (384 threads): w0 = TMA producer of Q and K, w1 = MMA issuer
+// (one elected lane; the warp allocates TMEM), w2 = TMA producer of V, w4..w7 = softmax / O correction /
+// epilogue of query tile A, w8..w11 the same for tile B, thread t of a group <-> TMEM lane t <-> query
+// row q0 + t (a whole S row per thread: max and sum need no shuffles).  TMEM: S_A, S_B, O_A, O_B.
+// Per key tile j and tile T in {A, B}:
+//   MMA      once P_T(j-1) is in smem: S_T(j) = Q_T K_j^T (commit s_full[T]),
+//            O_T += P_T(j-1) V_{j-1} (commit pv_done[T]); K_j / V_{j-1} released after tile B's use
+//   softmax  pass 1: S_T(j) -> row max (8 independent chains); wait pv_done[T](j-1), O_T *= exp2(m - m')
+//            in TMEM if the max moved; pass 2: S_T(j) again -> p = exp2(s - m'), row sum, P_T -> smem
+//            (fp16, K-major SW128) -> arrive p_full[T]
+// While one group runs its softmax (MUFU / FMA latency-bound: one warp per sub-partition and group) the
+// tensor core works on the other group's S and P V, so the two chains hide each other.  The pair is
+// two adjacent query tiles (2p, 2p+1): tile B needs one more key tile than A, heaviest pairs first.
+// Q, K, V by TMA (3-D maps over the [pos][b][h] and [pos][2][b][h] layouts, 128-row boxes, zero fill past
+// seq_len); V is read MN-major (the instruction's B-transpose bit), P V's A operand is P in shared memory.
 namespace tc {
 
-constexpr int kRows = 128;  // queries per CTA and keys per tile
+constexpr int kRows = 128;  // queries per tile and keys per tile
+constexpr int kKS = 2;      // K stages
 
 template <int D>
 struct Cfg {
+  static constexpr int kVS = D == 64 ? 2 : 1;          // V stages (D = 128: 224 KB of the 227 KB)
   static constexpr uint32_t kBox = kRows * 64 * 2;      // one 64-column box: 16 KB
   static constexpr uint32_t kTile = kRows * D * 2;      // Q, K or V tile
-  static constexpr uint32_t kQ = 0, kK = kTile, kV = 3 * kTile, kP = 5 * kTile;
-  static constexpr uint32_t kBar = kP + kRows * kRows * 2;
+  static constexpr uint32_t kP1 = kRows * kRows * 2;    // one P tile: 32 KB
+  static constexpr uint32_t kQ = 0, kK = 2 * kTile, kV = kK + kKS * kTile, kP = kV + kVS * kTile;
+  static constexpr uint32_t kBar = kP + 2 * kP1;
   static constexpr uint32_t kSmem = kBar + 256 + 1024;  // barriers, 1024-B alignment slack
-  static constexpr uint32_t kO = 2 * kRows;              // TMEM column of O (S[0] at 0, S[1] at 128)
+  static constexpr uint32_t kO = 2 * kRows;              // TMEM column of O_A (S_A at 0, S_B at 128)
 };
 
 // bounded wait: a schedule bug traps (a launch error) instead of hanging the GPU; `code` / `j` name the
@@ -69,6 +75,100 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, flush-to-zero (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// y = x * a + c on a pair of floats in one FFMA2 (the sm_100 paired fp32 pipe)
+__device__ __forceinline__ void ffma2(float& y0, float& y1, float x0, float x1, float a, float c) {
+  uint64_t x, av, cv, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(cv) : "f"(c));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(x), "l"(av), "l"(cv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(y0), "=f"(y1) : "l"(y));
+}
+
+// (s0, s1) += (x0, x1) in one FADD2
+__device__ __forceinline__ void fadd2(float& s0, float& s1, float x0, float x1) {
+  uint64_t sv, xv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(s0), "f"(s1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xv) : "f"(x0), "f"(x1));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(sv) : "l"(xv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(sv));
+}
+
+// pass 1 of a 128-key tile: the row max of the raw scores, 8 independent chains of 3-input max
+// (FMNMX3); kMask: keys past `lim` (within the tile) are masked -- the diagonal tile only
+template <bool kMask>
+__device__ __forceinline__ float tile_row_max(uint32_t s_col, int lim) {
+  float mp[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mp[i] = -INFINITY;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {  // two 64-column halves, one TMEM-load wait each
+    uint32_t r[64];
+    tmem_ld_32x32b_x32(s_col + hh * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld_32x32b_x32(s_col + hh * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
+      if (kMask) {
+        v0 = hh * 64 + i > lim ? -INFINITY : v0;
+        v1 = hh * 64 + i + 1 > lim ? -INFINITY : v1;
+      }
+      mp[(i >> 1) & 7] = fmaxf(mp[(i >> 1) & 7], fmaxf(v0, v1));
+    }
+  }
+  return fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+}
+
+// pass 2: p = exp2(s * scale - m') (FFMA2 + MUFU.EX2), the row sum (FADD2), P row tt -> shared memory,
+// K-major with the 128-byte swizzle (16-byte unit u of row tt at u ^ (tt & 7)); returns the row sum
+template <bool kMask>
+__device__ __forceinline__ float tile_exp_store(uint32_t s_col, int lim, float qscale, float mx, uint32_t p_base,
+                                                int tt, uint32_t box_bytes) {
+  float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (kMask) asm volatile("mov.b32 %0, %0;" : "+r"(lim));  // opaque: pass 1's mask bits are not kept live
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    uint32_t r[64];
+    tmem_ld_32x32b_x32(s_col + hh * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld_32x32b_x32(s_col + hh * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
+      if (kMask) {
+        v0 = hh * 64 + i > lim ? -INFINITY : v0;
+        v1 = hh * 64 + i + 1 > lim ? -INFINITY : v1;
+      }
+      ffma2(v0, v1, v0, v1, qscale, -mx);
+      v0 = ex2_approx(v0);  // masked: ex2(-inf) = 0
+      v1 = ex2_approx(v1);
+      fadd2(sp[(i >> 1) & 3], sp[((i >> 1) & 3) + 4], v0, v1);
+      r[i] = __float_as_uint(v0);
+      r[i + 1] = __float_as_uint(v1);
+    }
+#pragma unroll
+    for (int uu = 0; uu < 8; ++uu) {
+      const int u = hh * 8 + uu;
+      const uint32_t addr = p_base + (u >> 3) * box_bytes + tt * 128 + (((u & 7) ^ (tt & 7)) << 4);
+      const uint32_t* w = r + uu * 8;
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                   "r"(pack_half2(__uint_as_float(w[0]), __uint_as_float(w[1]))),
+                   "r"(pack_half2(__uint_as_float(w[2]), __uint_as_float(w[3]))),
+                   "r"(pack_half2(__uint_as_float(w[4]), __uint_as_float(w[5]))),
+                   "r"(pack_half2(__uint_as_float(w[6]), __uint_as_float(w[7])))
+                   : "memory");
+    }
+  }
+  return ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
 }
 
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -96,58 +196,73 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 1) prefill_tc_kernel(const __grid_constant__ CUtensorMap tq,
+__global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                            const __grid_constant__ CUtensorMap tkv,
                                                            __half* __restrict__ out, int batch, int heads,
                                                            int seq_len, float qscale) {
   using C = Cfg<D>;
+  constexpr int VS = C::kVS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t base = smem_u32(sm);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::kBar);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
-  uint64_t* s_full = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_full = bars;             // [1]
+  uint64_t* k_full = bars + 1;         // [kKS]
+  uint64_t* k_empty = bars + 3;        // [kKS]
+  uint64_t* v_full = bars + 5;         // [VS]
+  uint64_t* v_empty = bars + 7;        // [VS]
+  uint64_t* s_full = bars + 9;         // [2] per query tile
+  uint64_t* p_full = bars + 11;        // [2]
+  uint64_t* pv_done = bars + 13;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-  const int qt = gridDim.x - 1 - blockIdx.x;  // long (late) query tiles first
+  // long (late) pairs first within each (sequence, head); the pairs of one (sequence, head) are adjacent in
+  // launch order so they share its K / V in L2 (pair-major order measured 3-12% slower)
+  const int pair = gridDim.x - 1 - blockIdx.x;
   const int b = blockIdx.y / heads, hd = blockIdx.y % heads;
-  const int q0 = qt * kRows, ntiles = qt + 1;
+  const int ktot = (seq_len + kRows - 1) / kRows;
+  const int nt_a = 2 * pair + 1, ntk = min(2 * pair + 2, ktot);  // key tiles of A and of B (ntk >= nt_a)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tkv);
-  }
-  if (warp == 1 && lane == 0) {
-    for (int i = 0; i < 9; ++i) mbar_init(bars + i, 1);
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
+    for (int i = 0; i < 11; ++i) mbar_init(bars + i, 1);
+    mbar_init(&p_full[0], 128);
+    mbar_init(&p_full[1], 128);
+    mbar_init(&pv_done[0], 1);
+    mbar_init(&pv_done[1], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer ----------------
-      mbar_arrive_expect_tx(q_full, C::kTile);
-      for (int c = 0; c < D / 64; ++c) tma_load_3d(base + C::kQ + c * C::kBox, &tq, q_full, hd * D + c * 64, b, q0);
-      for (int j = 0; j < ntiles; ++j) {
-        const int buf = j & 1;
-        if (j >= 2) wait_bar(&kv_empty[buf], ((j - 2) >> 1) & 1, 1, j);
-        mbar_arrive_expect_tx(&k_full[buf], C::kTile);
+    if (lane == 0) {  // ---------------- TMA: Q_A, Q_B, then the K ring ----------------
+      mbar_arrive_expect_tx(q_full, 2 * C::kTile);
+      for (int t = 0; t < 2; ++t)
         for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(base + C::kK + buf * C::kTile + c * C::kBox, &tkv, &k_full[buf], hd * D + c * 64, b, j * kRows);
-        mbar_arrive_expect_tx(&v_full[buf], C::kTile);
+          tma_load_3d(base + C::kQ + t * C::kTile + c * C::kBox, &tq, q_full, hd * D + c * 64, b,
+                      (2 * pair + t) * kRows);
+      for (int j = 0; j < ntk; ++j) {
+        const int st = j % kKS;
+        if (j >= kKS) wait_bar(&k_empty[st], ((j - kKS) / kKS) & 1, 1, j);
+        mbar_arrive_expect_tx(&k_full[st], C::kTile);
         for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(base + C::kV + buf * C::kTile + c * C::kBox, &tkv, &v_full[buf], hd * D + c * 64, batch + b,
+          tma_load_3d(base + C::kK + st * C::kTile + c * C::kBox, &tkv, &k_full[st], hd * D + c * 64, b, j * kRows);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // ---------------- TMA: the V ring ----------------
+      for (int j = 0; j < ntk; ++j) {
+        const int st = j % VS;
+        if (j >= VS) wait_bar(&v_empty[st], ((j - VS) / VS) & 1, 2, j);
+        mbar_arrive_expect_tx(&v_full[st], C::kTile);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(base + C::kV + st * C::kTile + c * C::kBox, &tkv, &v_full[st], hd * D + c * 64, batch + b,
                       j * kRows);
       }
     }
@@ -155,115 +270,102 @@ __global__ void __launch_bounds__(256, 1) prefill_tc_kernel(const __grid_constan
     if (lane == 0) {  // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc_s = umma_idesc_f16_f32(kRows, kRows);
       constexpr uint32_t idesc_o = umma_idesc_f16_f32(kRows, D) | (1u << 16);  // B (V) MN-major
-      wait_bar(q_full, 0, 2);
-      tc_fence_after();
-      for (int j = 0; j <= ntiles; ++j) {
-        if (j < ntiles) {  // S_j = Q K_j^T (its S buffer was released with P_{j-2})
-          const int buf = j & 1;
-          wait_bar(&k_full[buf], (j >> 1) & 1, 3, j);
-          tc_fence_after();
+      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+        const int st = j % kKS;
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c)
+        for (int c = 0; c < D / 64; ++c)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_f16(tmem + buf * kRows, umma_desc_k_sw128(base + C::kQ + c * C::kBox + k * 32),
-                       umma_desc_k_sw128(base + C::kK + buf * C::kTile + c * C::kBox + k * 32), idesc_s,
-                       (c | k) != 0);
-          umma_commit(&s_full[buf]);
+          for (int k = 0; k < 4; ++k)
+            umma_f16(tmem + t * kRows, umma_desc_k_sw128(base + C::kQ + t * C::kTile + c * C::kBox + k * 32),
+                     umma_desc_k_sw128(base + C::kK + st * C::kTile + c * C::kBox + k * 32), idesc_s, (c | k) != 0);
+        umma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int i) {  // O_t += P_t V_i
+        const int st = i % VS;
+        wait_bar(&v_full[st], (i / VS) & 1, 5, i);
+        tc_fence_after();
+        const uint32_t p = base + C::kP + t * C::kP1;
+#pragma unroll
+        for (int kk = 0; kk < kRows / 16; ++kk)
+          umma_f16(tmem + C::kO + t * D, umma_desc_k_sw128(p + (kk >> 2) * C::kBox + (kk & 3) * 32),
+                   desc_mn_sw128(base + C::kV + st * C::kTile + kk * 2048, C::kBox), idesc_o, (i | kk) != 0);
+        umma_commit(&pv_done[t]);
+      };
+      wait_bar(q_full, 0, 3);
+      for (int j = 0; j <= ntk; ++j) {
+        bool k_waited = false;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int ntt = t ? ntk : nt_a;
+          const bool prev = j >= 1 && j - 1 < ntt;  // P_t(j-1) exists
+          if (prev) wait_bar(&p_full[t], (j - 1) & 1, 4, j);  // also: S_t(j-1) consumed, S_t is free
+          if (j < ntt) {
+            if (!k_waited) wait_bar(&k_full[j % kKS], (j / kKS) & 1, 6, j);
+            k_waited = true;
+            tc_fence_after();
+            issue_s(t, j);
+          }
+          if (prev) issue_pv(t, j - 1);
         }
-        if (j >= 1) {  // O += P_{j-1} V_{j-1}
-          const int i = j - 1, ib = i & 1;
-          wait_bar(p_full, i & 1, 4, i);
-          wait_bar(&v_full[ib], (i >> 1) & 1, 5, i);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kRows / 16; ++kk)
-            umma_f16(tmem + C::kO, umma_desc_k_sw128(base + C::kP + (kk >> 2) * C::kBox + (kk & 3) * 32),
-                     desc_mn_sw128(base + C::kV + ib * C::kTile + kk * 2048, C::kBox), idesc_o, (i | kk) != 0);
-          umma_commit(pv_done);
-          umma_commit(&kv_empty[ib]);
-        }
+        if (j < ntk) umma_commit(&k_empty[j % kKS]);       // both tiles' S on K_j issued before
+        if (j >= 1) umma_commit(&v_empty[(j - 1) % VS]);   // both tiles' P V on V_{j-1} issued before
       }
     }
-  } else if (warp >= 4) {  // ---------------- softmax, O correction, epilogue ----------------
-    const int t = threadIdx.x - 128;
+  } else if (warp >= 4) {  // ---------------- softmax, O correction, epilogue of tile t ----------------
+    const int t = (warp - 4) >> 2;
+    const int tt = threadIdx.x - 128 * (t + 1);
     const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-    const int row = q0 + t;
+    const int qt = 2 * pair + t, row = qt * kRows + tt, ntt = t ? ntk : nt_a;
+    const uint32_t s_col = tmem + lanes + t * kRows, o_col = tmem + lanes + C::kO + t * D;
+    const uint32_t p_base = base + C::kP + t * C::kP1;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      const int buf = j & 1;
-      wait_bar(&s_full[buf], (j >> 1) & 1, 6, j);
+    for (int j = 0; j < ntt; ++j) {
+      // keys past the query (and past seq_len) masked: key index within the tile > lim (diagonal tile only)
+      const int lim = j == qt ? row - j * kRows : kRows;
+      wait_bar(&s_full[t], j & 1, 7, j);
       tc_fence_after();
-      float s[kRows];
-#pragma unroll
-      for (int cc = 0; cc < kRows / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + lanes + buf * kRows + cc * 32, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(r[i]) * qscale;
-      }
-      if (j == ntiles - 1) {  // diagonal tile: keys past the query (and past seq_len) masked
-#pragma unroll
-        for (int c = 0; c < kRows; ++c)
-          if (j * kRows + c > row) s[c] = -INFINITY;
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kRows; ++c) mx = fmaxf(mx, s[c]);
+      // pass 1: row max of the raw scores (the scale is folded into exp2 below)
+      const bool diag = j == qt;  // warp-uniform
+      float mx = diag ? tile_row_max<true>(s_col, lim) : tile_row_max<false>(s_col, lim);
+      mx *= qscale;  // qscale > 0: the max of the scaled scores (finite: key j*128 <= row on every tile)
       // lazy rescaling: keep the running max unless this tile exceeds it by more than 2^8 (P <= 256
       // stays exact enough in fp16 and O / l absorb the common factor), so most tiles after the first
-      // skip the O correction; the first tile always sets it (finite: key j*128 <= row on every tile)
+      // skip the O correction; the first tile always sets it
       mx = (mx > m + 8.f) ? mx : m;
-      const float alpha = exp2f(m - mx);
-      float sum = 0.f;
-#pragma unroll
-      for (int c = 0; c < kRows; ++c) {
-        s[c] = exp2f(s[c] - mx);
-        sum += s[c];
-      }
-      l = l * alpha + sum;
-      m = mx;
-      if (j >= 1) {  // P V of the previous tile is done: O and the P buffer are ours
-        wait_bar(pv_done, (j - 1) & 1, 7, j);
+      const float alpha = ex2_approx(m - mx);
+      if (j >= 1) {  // P V of the previous tile is done: O_t and the P_t buffer are ours
+        wait_bar(&pv_done[t], (j - 1) & 1, 8, j);
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld/st are .sync.aligned
 #pragma unroll 1
           for (int cc = 0; cc < D / 32; ++cc) {
             uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + lanes + C::kO + cc * 32, r);
+            tmem_ld_32x32b_x32(o_col + cc * 32, r);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st_x32(tmem + lanes + C::kO + cc * 32, r);
+            tmem_st_x32(o_col + cc * 32, r);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
-      // P row t -> shared memory, K-major with the 128-byte swizzle (16-byte unit u of row t at u ^ (t & 7))
-#pragma unroll
-      for (int u = 0; u < kRows / 8; ++u) {
-        uint4 v;
-        v.x = pack_half2(s[u * 8 + 0], s[u * 8 + 1]);
-        v.y = pack_half2(s[u * 8 + 2], s[u * 8 + 3]);
-        v.z = pack_half2(s[u * 8 + 4], s[u * 8 + 5]);
-        v.w = pack_half2(s[u * 8 + 6], s[u * 8 + 7]);
-        const uint32_t addr = base + C::kP + (u >> 3) * C::kBox + t * 128 + (((u & 7) ^ (t & 7)) << 4);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                     : "memory");
-      }
+      // pass 2: P and the row sum
+      const float sum = diag ? tile_exp_store<true>(s_col, lim, qscale, mx, p_base, tt, C::kBox)
+                             : tile_exp_store<false>(s_col, lim, qscale, mx, p_base, tt, C::kBox);
+      l = l * alpha + sum;
+      m = mx;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy P writes -> tcgen05 reads
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[t]);
     }
-    wait_bar(pv_done, (ntiles - 1) & 1, 8, ntiles);
+    wait_bar(&pv_done[t], (ntt - 1) & 1, 9, ntt);
     tc_fence_after();
     const float inv = 1.f / l;
     __half* o = out + (static_cast<long long>(row) * batch + b) * heads * D + hd * D;
 #pragma unroll 1
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + lanes + C::kO + cc * 32, r);
+      tmem_ld_32x32b_x32(o_col + cc * 32, r);
       tmem_ld_wait();
       if (row < seq_len) {
 #pragma unroll
@@ -280,7 +382,7 @@ __global__ void __launch_bounds__(256, 1) prefill_tc_kernel(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -310,8 +412,9 @@ int launch_prefill_tc(const __half* q, const __half* kv, __half* out, int batch,
     cudaFuncSetAttribute(tc::prefill_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (dev < 64) attr_done[dev] = 1;
   }
-  dim3 grid((seq_len + tc::kRows - 1) / tc::kRows, batch * heads);
-  tc::prefill_tc_kernel<D><<<grid, 256, C::kSmem, stream>>>(tq, tkv, out, batch, heads, seq_len, qscale);
+  const unsigned npair = (seq_len + 2 * tc::kRows - 1) / (2 * tc::kRows);  // query-tile pairs
+  const dim3 grid(npair, batch * heads);
+  tc::prefill_tc_kernel<D><<<grid, 384, C::kSmem, stream>>>(tq, tkv, out, batch, heads, seq_len, qscale);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return check_launch("prefill_attention");
 }
