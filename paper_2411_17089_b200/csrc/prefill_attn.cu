@@ -102,73 +102,56 @@ __device__ __forceinline__ void fadd2(float& s0, float& s1, float x0, float x1) 
   asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(sv));
 }
 
-// pass 1 of a 128-key tile: the row max of the raw scores, 8 independent chains of 3-input max
-// (FMNMX3); kMask: keys past `lim` (within the tile) are masked -- the diagonal tile only
-template <bool kMask>
-__device__ __forceinline__ float tile_row_max(uint32_t s_col, int lim) {
+// the row max of a 128-key score tile held in registers: 8 independent chains of 3-input max (FMNMX3)
+__device__ __forceinline__ float row_max128(const uint32_t (&r)[kRows]) {
   float mp[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) mp[i] = -INFINITY;
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {  // two 64-column halves, one TMEM-load wait each
-    uint32_t r[64];
-    tmem_ld_32x32b_x32(s_col + hh * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-    tmem_ld_32x32b_x32(s_col + hh * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 64; i += 2) {
-      float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
-      if (kMask) {
-        v0 = hh * 64 + i > lim ? -INFINITY : v0;
-        v1 = hh * 64 + i + 1 > lim ? -INFINITY : v1;
-      }
-      mp[(i >> 1) & 7] = fmaxf(mp[(i >> 1) & 7], fmaxf(v0, v1));
-    }
-  }
+  for (int i = 0; i < kRows; i += 2)
+    mp[(i >> 1) & 7] = fmaxf(mp[(i >> 1) & 7], fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
   return fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
 }
 
-// pass 2: p = exp2(s * scale - m') (FFMA2 + MUFU.EX2), the row sum (FADD2), P row tt -> shared memory,
-// K-major with the 128-byte swizzle (16-byte unit u of row tt at u ^ (tt & 7)); returns the row sum
-template <bool kMask>
-__device__ __forceinline__ float tile_exp_store(uint32_t s_col, int lim, float qscale, float mx, uint32_t p_base,
-                                                int tt, uint32_t box_bytes) {
+// p = exp2(s * scale - m') (FFMA2 + MUFU.EX2; masked scores are -inf -> 0), the row sum (FADD2), P row tt
+// -> shared memory, K-major with the 128-byte swizzle (16-byte unit u of row tt at u ^ (tt & 7))
+__device__ __forceinline__ float exp_store128(const uint32_t (&r)[kRows], float qscale, float mx, uint32_t p_base,
+                                              int tt, uint32_t box_bytes) {
   float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (kMask) asm volatile("mov.b32 %0, %0;" : "+r"(lim));  // opaque: pass 1's mask bits are not kept live
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    uint32_t r[64];
-    tmem_ld_32x32b_x32(s_col + hh * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-    tmem_ld_32x32b_x32(s_col + hh * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-    tmem_ld_wait();
+  for (int u = 0; u < kRows / 8; ++u) {
+    float p[8];
 #pragma unroll
-    for (int i = 0; i < 64; i += 2) {
-      float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
-      if (kMask) {
-        v0 = hh * 64 + i > lim ? -INFINITY : v0;
-        v1 = hh * 64 + i + 1 > lim ? -INFINITY : v1;
-      }
-      ffma2(v0, v1, v0, v1, qscale, -mx);
-      v0 = ex2_approx(v0);  // masked: ex2(-inf) = 0
-      v1 = ex2_approx(v1);
-      fadd2(sp[(i >> 1) & 3], sp[((i >> 1) & 3) + 4], v0, v1);
-      r[i] = __float_as_uint(v0);
-      r[i + 1] = __float_as_uint(v1);
+    for (int i = 0; i < 8; i += 2) {
+      ffma2(p[i], p[i + 1], __uint_as_float(r[u * 8 + i]), __uint_as_float(r[u * 8 + i + 1]), qscale, -mx);
+      p[i] = ex2_approx(p[i]);
+      p[i + 1] = ex2_approx(p[i + 1]);
+      fadd2(sp[i >> 1], sp[(i >> 1) + 4], p[i], p[i + 1]);
     }
-#pragma unroll
-    for (int uu = 0; uu < 8; ++uu) {
-      const int u = hh * 8 + uu;
-      const uint32_t addr = p_base + (u >> 3) * box_bytes + tt * 128 + (((u & 7) ^ (tt & 7)) << 4);
-      const uint32_t* w = r + uu * 8;
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
-                   "r"(pack_half2(__uint_as_float(w[0]), __uint_as_float(w[1]))),
-                   "r"(pack_half2(__uint_as_float(w[2]), __uint_as_float(w[3]))),
-                   "r"(pack_half2(__uint_as_float(w[4]), __uint_as_float(w[5]))),
-                   "r"(pack_half2(__uint_as_float(w[6]), __uint_as_float(w[7])))
-                   : "memory");
-    }
+    const uint32_t addr = p_base + (u >> 3) * box_bytes + tt * 128 + (((u & 7) ^ (tt & 7)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pack_half2(p[0], p[1])),
+                 "r"(pack_half2(p[2], p[3])), "r"(pack_half2(p[4], p[5])), "r"(pack_half2(p[6], p[7]))
+                 : "memory");
   }
   return ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+}
+
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -214,7 +197,8 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
   uint64_t* s_full = bars + 9;         // [2] per query tile
   uint64_t* p_full = bars + 11;        // [2]
   uint64_t* pv_done = bars + 13;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* s_free = bars + 15;        // [2] S_t read into registers: TMEM S_t may be overwritten
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   // long (late) pairs first within each (sequence, head); the pairs of one (sequence, head) are adjacent in
   // launch order so they share its K / V in L2 (pair-major order measured 3-12% slower)
@@ -232,6 +216,8 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
     mbar_init(&p_full[1], 128);
     mbar_init(&pv_done[0], 1);
     mbar_init(&pv_done[1], 1);
+    mbar_init(&s_free[0], 128);
+    mbar_init(&s_free[1], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -293,19 +279,23 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
       };
       wait_bar(q_full, 0, 3);
       for (int j = 0; j <= ntk; ++j) {
-        bool k_waited = false;
+        if (j < ntk) {
+          wait_bar(&k_full[j % kKS], (j / kKS) & 1, 6, j);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (j < (t ? ntk : nt_a)) {  // S_t(j) once softmax t holds S_t(j-1) in registers
+              if (j >= 1) wait_bar(&s_free[t], (j - 1) & 1, 4, j);
+              tc_fence_after();
+              issue_s(t, j);
+            }
+          }
+        }
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const int ntt = t ? ntk : nt_a;
-          const bool prev = j >= 1 && j - 1 < ntt;  // P_t(j-1) exists
-          if (prev) wait_bar(&p_full[t], (j - 1) & 1, 4, j);  // also: S_t(j-1) consumed, S_t is free
-          if (j < ntt) {
-            if (!k_waited) wait_bar(&k_full[j % kKS], (j / kKS) & 1, 6, j);
-            k_waited = true;
-            tc_fence_after();
-            issue_s(t, j);
+          if (j >= 1 && j - 1 < (t ? ntk : nt_a)) {  // O_t += P_t(j-1) V_{j-1} once P_t(j-1) is in smem
+            wait_bar(&p_full[t], (j - 1) & 1, 10, j);
+            issue_pv(t, j - 1);
           }
-          if (prev) issue_pv(t, j - 1);
         }
         if (j < ntk) umma_commit(&k_empty[j % kKS]);       // both tiles' S on K_j issued before
         if (j >= 1) umma_commit(&v_empty[(j - 1) % VS]);   // both tiles' P V on V_{j-1} issued before
@@ -320,14 +310,22 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
     const uint32_t p_base = base + C::kP + t * C::kP1;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < ntt; ++j) {
-      // keys past the query (and past seq_len) masked: key index within the tile > lim (diagonal tile only)
-      const int lim = j == qt ? row - j * kRows : kRows;
       wait_bar(&s_full[t], j & 1, 7, j);
       tc_fence_after();
-      // pass 1: row max of the raw scores (the scale is folded into exp2 below)
-      const bool diag = j == qt;  // warp-uniform
-      float mx = diag ? tile_row_max<true>(s_col, lim) : tile_row_max<false>(s_col, lim);
-      mx *= qscale;  // qscale > 0: the max of the scaled scores (finite: key j*128 <= row on every tile)
+      uint32_t r[kRows];  // this row's raw scores Q K^T (the scale is folded into exp2 below)
+#pragma unroll
+      for (int cc = 0; cc < kRows / 32; ++cc)
+        tmem_ld_32x32b_x32(s_col + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[t]);  // the MMA may now compute S_t(j+1) under this tile's softmax
+      if (j == qt) {  // diagonal tile (warp-uniform branch): keys past the query (and past seq_len) masked
+        const int lim = row - j * kRows;
+#pragma unroll
+        for (int i = 0; i < kRows; ++i)
+          if (i > lim) r[i] = __float_as_uint(-INFINITY);
+      }
+      float mx = row_max128(r) * qscale;  // qscale > 0: the max of the scaled scores (finite: key j*128 <= row)
       // lazy rescaling: keep the running max unless this tile exceeds it by more than 2^8 (P <= 256
       // stays exact enough in fp16 and O / l absorb the common factor), so most tiles after the first
       // skip the O correction; the first tile always sets it
@@ -338,21 +336,18 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld/st are .sync.aligned
 #pragma unroll 1
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(o_col + cc * 32, r);
+          for (int cc = 0; cc < D / 16; ++cc) {
+            uint32_t o[16];
+            tmem_ld_x16(o_col + cc * 16, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st_x32(o_col + cc * 32, r);
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_x16(o_col + cc * 16, o);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
-      // pass 2: P and the row sum
-      const float sum = diag ? tile_exp_store<true>(s_col, lim, qscale, mx, p_base, tt, C::kBox)
-                             : tile_exp_store<false>(s_col, lim, qscale, mx, p_base, tt, C::kBox);
-      l = l * alpha + sum;
+      l = l * alpha + exp_store128(r, qscale, mx, p_base, tt, C::kBox);
       m = mx;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy P writes -> tcgen05 reads
       tc_fence_before();

@@ -4,6 +4,7 @@
     ncu --set full -k regex:decode_attn -c 1 python tools/ncu_target.py k2
     ncu --set full -k regex:gemm_tcgen05_kernel -c 1 python tools/ncu_target.py c1   # config-1 shapes
     ncu --set full -k regex:prefill_tc -c 1 python tools/ncu_target.py prefill
+    ncu --set full -k regex:prefill_tc -c 1 python tools/ncu_target.py prefill40   # config 3 (40 heads)
 """
 import sys
 
@@ -14,8 +15,8 @@ from paper_2411_17089_b200 import kernels
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 dev = torch.device("cuda:0")
-if which == "prefill":  # causal prefill attention at the config-2 prompt (b32, 32 heads, d128, S = 1024)
-    b, heads, d, S = 32, 32, 128, 1024
+if which in ("prefill", "prefill40"):  # causal prefill attention at the config-2 (-3) prompt: b32, 32 (40) heads
+    b, heads, d, S = 32, 40 if which == "prefill40" else 32, 128, 1024
     pages = torch.randn(S, 2, b, heads * d, device=dev).half()
     q = torch.randn(S, b, heads * d, device=dev).half()
     o = torch.empty_like(q)
