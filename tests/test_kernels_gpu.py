@@ -407,6 +407,34 @@ def test_prefill_attention_causal(dev, batch, heads, d, seq):
     _close(out, ref)
 
 
+def _prefill_ref(q, pages, batch, heads, d, seq):
+    K = pages[:, 0].float().reshape(seq, batch, heads, d)
+    V = pages[:, 1].float().reshape(seq, batch, heads, d)
+    qh = q.float().reshape(seq, batch, heads, d)
+    logits = torch.einsum("tbhd,sbhd->bhts", qh, K) / math.sqrt(d)
+    mask = torch.triu(torch.ones(seq, seq, dtype=torch.bool, device=q.device), 1)
+    logits = logits.masked_fill(mask, float("-inf"))
+    return torch.einsum("bhts,sbhd->tbhd", torch.softmax(logits, -1), V).reshape(seq, batch, heads * d)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_prefill_attention_running_max_moves(dev, d):
+    """Scores that grow along the keys (0.6 per position, ~10 log2 units per 128-key tile): every
+    tile moves each row's running max past the lazy-rescale threshold (2^8), so the O correction in
+    TMEM runs on every tile of every row -- the path random inputs almost never take."""
+    batch, heads, seq = 2, 2, 700
+    h = heads * d
+    pos = torch.arange(seq, device=dev, dtype=torch.float32)
+    k = (pos * 0.6 / d)[:, None, None].expand(seq, batch, h)
+    v = _rand(seq, batch, h, seed=22).float()
+    pages = torch.stack([k, v], 1).half().contiguous()
+    q = torch.ones(seq, batch, h, dtype=torch.float16, device=dev)
+    out = torch.empty(seq, batch, h, dtype=torch.float16, device=dev)
+    kernels.prefill_attention(q, pages, out, batch, heads, d, seq)
+    torch.cuda.synchronize()
+    _close(out, _prefill_ref(q, pages, batch, heads, d, seq))
+
+
 @pytest.mark.parametrize("rows,hidden", [(32, 4096), (7, 768), (3, 7168), (1, 5120)])
 def test_layernorm(dev, rows, hidden):
     x = torch.randn(rows, hidden, device=dev) * 3 + 1
