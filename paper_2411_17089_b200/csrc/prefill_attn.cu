@@ -7,14 +7,14 @@
 // (the reference prices it nowhere: pipesim models decode layers only), but it gates long-prompt
 // runs (config 5, prompt 8192): the CUDA-core kernel of round 1 spent 36 ms per OPT-6.7B layer at
 // b32 s1024, a warp-MMA (mma.sync) flash kernel 1.27 ms, a one-query-tile tcgen05 version 0.67 ms, this
-// two-tile ping-pong 0.50 ms (profiles/r02_prefill_bench.jsonl).
+// persistent two-tile ping-pong 0.37 ms (profiles/r02_prefill_bench.jsonl).
 //
 // Layout (runtime.py prefill): q rows [pos][b][hidden]; KV pages [pos][2][b][hidden] -- one
 // (sequence, head) row of K or V is head_dim contiguous halves, rows of consecutive positions are
 // b*hidden (q) or 2*b*hidden (K, V) halves apart: 3-D TMA maps (h, b or 2b, pos) cut 64-column x
 // 128-position boxes straight out of them.  The output goes to [pos][b][hidden] like q.
 //
-// One CTA per (pair of 128-query tiles, sequence, head), heaviest (last) pairs first.
+// Persistent: one CTA per SM walks the work items (pair of 128-query tiles, sequence, head).
 #include <math.h>
 #include <stdlib.h>
 
@@ -178,6 +178,33 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo) {
   return d;
 }
 
+// One work item = (pair of query tiles, sequence, head).  Persistent: CTA c takes one item per round of
+// G = gridDim.x <= #SMs items (item_of below), so one item's epilogue (O out of TMEM) overlaps the next
+// item's Q / K / V loads and its first S MMAs; every barrier's phase runs on across items (per-role
+// running counters), with q_empty / o_free releasing Q and O_t to the next item.
+struct Item {
+  int pair, b, hd, nt_a, ntk;  // nt_a / ntk: key tiles of tiles A / B (ntk >= nt_a)
+};
+
+__device__ __forceinline__ Item item_at(int w, int npair, int heads, int ktot) {
+  // long (late) pairs first within each (sequence, head); the pairs of one (sequence, head) are adjacent
+  // in item order so they share its K / V in L2 (pair-major order measured 3-12% slower)
+  Item it;
+  const int bh = w / npair;
+  it.pair = npair - 1 - w % npair;
+  it.b = bh / heads;
+  it.hd = bh % heads;
+  it.nt_a = 2 * it.pair + 1;
+  it.ntk = min(2 * it.pair + 2, ktot);
+  return it;
+}
+
+// the k-th item of CTA c among G: rounds of G consecutive items, walked forwards on even rounds and
+// backwards on odd ones, so a CTA handed a heavy pair in one round gets a light one in the next (plain
+// striding hands every CTA the same pair index whenever the pair count divides G), while the items in
+// flight stay a contiguous range (the pairs of one (sequence, head) share its K / V in L2)
+__device__ __forceinline__ int item_of(int k, int c, int G) { return k * G + ((k & 1) ? G - 1 - c : c); }
+
 template <int D>
 __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                            const __grid_constant__ CUtensorMap tkv,
@@ -198,26 +225,25 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
   uint64_t* p_full = bars + 11;        // [2]
   uint64_t* pv_done = bars + 13;       // [2]
   uint64_t* s_free = bars + 15;        // [2] S_t read into registers: TMEM S_t may be overwritten
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* q_empty = bars + 17;       // [1] the item's last S MMAs done: Q may be reloaded
+  uint64_t* o_free = bars + 18;        // [2] the item's O_t read out: the next item's first P V may overwrite it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
-  // long (late) pairs first within each (sequence, head); the pairs of one (sequence, head) are adjacent in
-  // launch order so they share its K / V in L2 (pair-major order measured 3-12% slower)
-  const int pair = gridDim.x - 1 - blockIdx.x;
-  const int b = blockIdx.y / heads, hd = blockIdx.y % heads;
   const int ktot = (seq_len + kRows - 1) / kRows;
-  const int nt_a = 2 * pair + 1, ntk = min(2 * pair + 2, ktot);  // key tiles of A and of B (ntk >= nt_a)
+  const int npair = (ktot + 1) / 2, items = npair * batch * heads;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tkv);
     for (int i = 0; i < 11; ++i) mbar_init(bars + i, 1);
-    mbar_init(&p_full[0], 128);
-    mbar_init(&p_full[1], 128);
-    mbar_init(&pv_done[0], 1);
-    mbar_init(&pv_done[1], 1);
-    mbar_init(&s_free[0], 128);
-    mbar_init(&s_free[1], 128);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&p_full[t], 128);
+      mbar_init(&pv_done[t], 1);
+      mbar_init(&s_free[t], 128);
+      mbar_init(&o_free[t], 128);
+    }
+    mbar_init(q_empty, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -228,151 +254,187 @@ __global__ void __launch_bounds__(384, 1) prefill_tc_kernel(const __grid_constan
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA: Q_A, Q_B, then the K ring ----------------
-      mbar_arrive_expect_tx(q_full, 2 * C::kTile);
-      for (int t = 0; t < 2; ++t)
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(base + C::kQ + t * C::kTile + c * C::kBox, &tq, q_full, hd * D + c * 64, b,
-                      (2 * pair + t) * kRows);
-      for (int j = 0; j < ntk; ++j) {
-        const int st = j % kKS;
-        if (j >= kKS) wait_bar(&k_empty[st], ((j - kKS) / kKS) & 1, 1, j);
-        mbar_arrive_expect_tx(&k_full[st], C::kTile);
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(base + C::kK + st * C::kTile + c * C::kBox, &tkv, &k_full[st], hd * D + c * 64, b, j * kRows);
+      uint32_t kc = 0;  // K loads issued by this CTA
+      for (int n = 0; n * static_cast<int>(gridDim.x) < items; ++n) {  // n = items done (all rounds but the last are full)
+        const int w = item_of(n, blockIdx.x, gridDim.x);
+        if (w >= items) continue;
+        const Item it = item_at(w, npair, heads, ktot);
+        if (n >= 1) wait_bar(q_empty, (n - 1) & 1, 11, n);
+        mbar_arrive_expect_tx(q_full, 2 * C::kTile);
+        for (int t = 0; t < 2; ++t)
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(base + C::kQ + t * C::kTile + c * C::kBox, &tq, q_full, it.hd * D + c * 64, it.b,
+                        (2 * it.pair + t) * kRows);
+        for (int j = 0; j < it.ntk; ++j, ++kc) {
+          const uint32_t st = kc % kKS;
+          if (kc >= kKS) wait_bar(&k_empty[st], ((kc - kKS) / kKS) & 1, 1, j);
+          mbar_arrive_expect_tx(&k_full[st], C::kTile);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(base + C::kK + st * C::kTile + c * C::kBox, &tkv, &k_full[st], it.hd * D + c * 64, it.b,
+                        j * kRows);
+        }
       }
     }
   } else if (warp == 2) {
     if (lane == 0) {  // ---------------- TMA: the V ring ----------------
-      for (int j = 0; j < ntk; ++j) {
-        const int st = j % VS;
-        if (j >= VS) wait_bar(&v_empty[st], ((j - VS) / VS) & 1, 2, j);
-        mbar_arrive_expect_tx(&v_full[st], C::kTile);
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_3d(base + C::kV + st * C::kTile + c * C::kBox, &tkv, &v_full[st], hd * D + c * 64, batch + b,
-                      j * kRows);
+      uint32_t vc = 0;
+      for (int n = 0; n * static_cast<int>(gridDim.x) < items; ++n) {
+        const int w = item_of(n, blockIdx.x, gridDim.x);
+        if (w >= items) continue;
+        const Item it = item_at(w, npair, heads, ktot);
+        for (int j = 0; j < it.ntk; ++j, ++vc) {
+          const uint32_t st = vc % VS;
+          if (vc >= VS) wait_bar(&v_empty[st], ((vc - VS) / VS) & 1, 2, j);
+          mbar_arrive_expect_tx(&v_full[st], C::kTile);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(base + C::kV + st * C::kTile + c * C::kBox, &tkv, &v_full[st], it.hd * D + c * 64,
+                        batch + it.b, j * kRows);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc_s = umma_idesc_f16_f32(kRows, kRows);
       constexpr uint32_t idesc_o = umma_idesc_f16_f32(kRows, D) | (1u << 16);  // B (V) MN-major
-      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
-        const int st = j % kKS;
+      uint32_t kc = 0, vc = 0;            // K / V tiles consumed
+      uint32_t sc[2] = {0, 0}, pc[2] = {0, 0};  // S_t issued, P_t consumed (running over items)
+      for (int n = 0; n * static_cast<int>(gridDim.x) < items; ++n) {
+        const int w = item_of(n, blockIdx.x, gridDim.x);
+        if (w >= items) continue;
+        const Item it = item_at(w, npair, heads, ktot);
+        wait_bar(q_full, n & 1, 3, n);
+        for (int j = 0; j <= it.ntk; ++j) {
+          if (j < it.ntk) {
+            const uint32_t st = kc % kKS;
+            wait_bar(&k_full[st], (kc / kKS) & 1, 6, j);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
+            for (int t = 0; t < 2; ++t) {
+              if (j < (t ? it.ntk : it.nt_a)) {  // S_t(j) once softmax t holds its previous S in registers
+                if (sc[t] >= 1) wait_bar(&s_free[t], (sc[t] - 1) & 1, 4, j);
+                tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16(tmem + t * kRows, umma_desc_k_sw128(base + C::kQ + t * C::kTile + c * C::kBox + k * 32),
-                     umma_desc_k_sw128(base + C::kK + st * C::kTile + c * C::kBox + k * 32), idesc_s, (c | k) != 0);
-        umma_commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int t, int i) {  // O_t += P_t V_i
-        const int st = i % VS;
-        wait_bar(&v_full[st], (i / VS) & 1, 5, i);
-        tc_fence_after();
-        const uint32_t p = base + C::kP + t * C::kP1;
+                for (int c = 0; c < D / 64; ++c)
 #pragma unroll
-        for (int kk = 0; kk < kRows / 16; ++kk)
-          umma_f16(tmem + C::kO + t * D, umma_desc_k_sw128(p + (kk >> 2) * C::kBox + (kk & 3) * 32),
-                   desc_mn_sw128(base + C::kV + st * C::kTile + kk * 2048, C::kBox), idesc_o, (i | kk) != 0);
-        umma_commit(&pv_done[t]);
-      };
-      wait_bar(q_full, 0, 3);
-      for (int j = 0; j <= ntk; ++j) {
-        if (j < ntk) {
-          wait_bar(&k_full[j % kKS], (j / kKS) & 1, 6, j);
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (j < (t ? ntk : nt_a)) {  // S_t(j) once softmax t holds S_t(j-1) in registers
-              if (j >= 1) wait_bar(&s_free[t], (j - 1) & 1, 4, j);
-              tc_fence_after();
-              issue_s(t, j);
+                  for (int k = 0; k < 4; ++k)
+                    umma_f16(tmem + t * kRows, umma_desc_k_sw128(base + C::kQ + t * C::kTile + c * C::kBox + k * 32),
+                             umma_desc_k_sw128(base + C::kK + st * C::kTile + c * C::kBox + k * 32), idesc_s,
+                             (c | k) != 0);
+                umma_commit(&s_full[t]);
+                ++sc[t];
+              }
             }
+            umma_commit(&k_empty[st]);  // both tiles' S on K_j issued before
+            ++kc;
+            if (j == it.ntk - 1) umma_commit(q_empty);  // the item's last S MMAs: Q may be reloaded
           }
-        }
+          if (j >= 1) {
+            const uint32_t st = vc % VS;
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (j >= 1 && j - 1 < (t ? ntk : nt_a)) {  // O_t += P_t(j-1) V_{j-1} once P_t(j-1) is in smem
-            wait_bar(&p_full[t], (j - 1) & 1, 10, j);
-            issue_pv(t, j - 1);
+            for (int t = 0; t < 2; ++t) {
+              if (j - 1 < (t ? it.ntk : it.nt_a)) {  // O_t += P_t(j-1) V_{j-1} once P_t(j-1) is in smem
+                wait_bar(&p_full[t], pc[t] & 1, 10, j);
+                if (j == 1 && n >= 1) wait_bar(&o_free[t], (n - 1) & 1, 12, n);  // previous item's O_t read
+                wait_bar(&v_full[st], (vc / VS) & 1, 5, j);
+                tc_fence_after();
+                const uint32_t p = base + C::kP + t * C::kP1;
+#pragma unroll
+                for (int kk = 0; kk < kRows / 16; ++kk)
+                  umma_f16(tmem + C::kO + t * D, umma_desc_k_sw128(p + (kk >> 2) * C::kBox + (kk & 3) * 32),
+                           desc_mn_sw128(base + C::kV + st * C::kTile + kk * 2048, C::kBox), idesc_o,
+                           (j - 1 | kk) != 0);
+                umma_commit(&pv_done[t]);
+                ++pc[t];
+              }
+            }
+            umma_commit(&v_empty[st]);  // both tiles' P V on V_{j-1} issued before
+            ++vc;
           }
         }
-        if (j < ntk) umma_commit(&k_empty[j % kKS]);       // both tiles' S on K_j issued before
-        if (j >= 1) umma_commit(&v_empty[(j - 1) % VS]);   // both tiles' P V on V_{j-1} issued before
       }
     }
   } else if (warp >= 4) {  // ---------------- softmax, O correction, epilogue of tile t ----------------
     const int t = (warp - 4) >> 2;
     const int tt = threadIdx.x - 128 * (t + 1);
     const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-    const int qt = 2 * pair + t, row = qt * kRows + tt, ntt = t ? ntk : nt_a;
     const uint32_t s_col = tmem + lanes + t * kRows, o_col = tmem + lanes + C::kO + t * D;
     const uint32_t p_base = base + C::kP + t * C::kP1;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < ntt; ++j) {
-      wait_bar(&s_full[t], j & 1, 7, j);
-      tc_fence_after();
-      uint32_t r[kRows];  // this row's raw scores Q K^T (the scale is folded into exp2 below)
-#pragma unroll
-      for (int cc = 0; cc < kRows / 32; ++cc)
-        tmem_ld_32x32b_x32(s_col + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&s_free[t]);  // the MMA may now compute S_t(j+1) under this tile's softmax
-      if (j == qt) {  // diagonal tile (warp-uniform branch): keys past the query (and past seq_len) masked
-        const int lim = row - j * kRows;
-#pragma unroll
-        for (int i = 0; i < kRows; ++i)
-          if (i > lim) r[i] = __float_as_uint(-INFINITY);
-      }
-      float mx = row_max128(r) * qscale;  // qscale > 0: the max of the scaled scores (finite: key j*128 <= row)
-      // lazy rescaling: keep the running max unless this tile exceeds it by more than 2^8 (P <= 256
-      // stays exact enough in fp16 and O / l absorb the common factor), so most tiles after the first
-      // skip the O correction; the first tile always sets it
-      mx = (mx > m + 8.f) ? mx : m;
-      const float alpha = ex2_approx(m - mx);
-      if (j >= 1) {  // P V of the previous tile is done: O_t and the P_t buffer are ours
-        wait_bar(&pv_done[t], (j - 1) & 1, 8, j);
+    uint32_t sc = 0, pc = 0;  // S_t(.) received, P V of tile t done (running over items)
+    for (int n = 0; n * static_cast<int>(gridDim.x) < items; ++n) {
+      const int w = item_of(n, blockIdx.x, gridDim.x);
+      if (w >= items) continue;
+      const Item it = item_at(w, npair, heads, ktot);
+      const int qt = 2 * it.pair + t, row = qt * kRows + tt, ntt = t ? it.ntk : it.nt_a;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < ntt; ++j) {
+        wait_bar(&s_full[t], sc & 1, 7, j);
+        ++sc;
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld/st are .sync.aligned
-#pragma unroll 1
-          for (int cc = 0; cc < D / 16; ++cc) {
-            uint32_t o[16];
-            tmem_ld_x16(o_col + cc * 16, o);
-            tmem_ld_wait();
+        uint32_t r[kRows];  // this row's raw scores Q K^T (the scale is folded into exp2 below)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st_x16(o_col + cc * 16, o);
+        for (int cc = 0; cc < kRows / 32; ++cc)
+          tmem_ld_32x32b_x32(s_col + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[t]);  // the MMA may now compute S_t(j+1) under this tile's softmax
+        if (j == qt) {  // diagonal tile (warp-uniform branch): keys past the query (and past seq_len) masked
+          const int lim = row - j * kRows;
+#pragma unroll
+          for (int i = 0; i < kRows; ++i)
+            if (i > lim) r[i] = __float_as_uint(-INFINITY);
+        }
+        float mx = row_max128(r) * qscale;  // qscale > 0: the max of the scaled scores (finite: key j*128 <= row)
+        // lazy rescaling: keep the running max unless this tile exceeds it by more than 2^8 (P <= 256
+        // stays exact enough in fp16 and O / l absorb the common factor), so most tiles after the first
+        // skip the O correction; the first tile always sets it
+        mx = (mx > m + 8.f) ? mx : m;
+        const float alpha = ex2_approx(m - mx);
+        if (j >= 1) {  // P V of the previous tile is done: O_t and the P_t buffer are ours
+          wait_bar(&pv_done[t], pc & 1, 8, j);
+          ++pc;
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld/st are .sync.aligned
+#pragma unroll 1
+            for (int cc = 0; cc < D / 16; ++cc) {
+              uint32_t o[16];
+              tmem_ld_x16(o_col + cc * 16, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st_x16(o_col + cc * 16, o);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
+        l = l * alpha + exp_store128(r, qscale, mx, p_base, tt, C::kBox);
+        m = mx;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy P writes -> tcgen05 reads
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
       }
-      l = l * alpha + exp_store128(r, qscale, mx, p_base, tt, C::kBox);
-      m = mx;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy P writes -> tcgen05 reads
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
-    }
-    wait_bar(&pv_done[t], (ntt - 1) & 1, 9, ntt);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    __half* o = out + (static_cast<long long>(row) * batch + b) * heads * D + hd * D;
+      wait_bar(&pv_done[t], pc & 1, 9, ntt);  // the item's last P V (also frees P_t for the next item)
+      ++pc;
+      tc_fence_after();
+      const float inv = 1.f / l;
+      __half* o = out + (static_cast<long long>(row) * batch + it.b) * heads * D + it.hd * D;
 #pragma unroll 1
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(o_col + cc * 32, r);
-      tmem_ld_wait();
-      if (row < seq_len) {
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(o_col + cc * 32, r);
+        tmem_ld_wait();
+        if (row < seq_len) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 v;
-          v.x = pack_half2(__uint_as_float(r[u * 8 + 0]) * inv, __uint_as_float(r[u * 8 + 1]) * inv);
-          v.y = pack_half2(__uint_as_float(r[u * 8 + 2]) * inv, __uint_as_float(r[u * 8 + 3]) * inv);
-          v.z = pack_half2(__uint_as_float(r[u * 8 + 4]) * inv, __uint_as_float(r[u * 8 + 5]) * inv);
-          v.w = pack_half2(__uint_as_float(r[u * 8 + 6]) * inv, __uint_as_float(r[u * 8 + 7]) * inv);
-          reinterpret_cast<uint4*>(o + cc * 32)[u] = v;
+          for (int u = 0; u < 4; ++u) {
+            uint4 v;
+            v.x = pack_half2(__uint_as_float(r[u * 8 + 0]) * inv, __uint_as_float(r[u * 8 + 1]) * inv);
+            v.y = pack_half2(__uint_as_float(r[u * 8 + 2]) * inv, __uint_as_float(r[u * 8 + 3]) * inv);
+            v.z = pack_half2(__uint_as_float(r[u * 8 + 4]) * inv, __uint_as_float(r[u * 8 + 5]) * inv);
+            v.w = pack_half2(__uint_as_float(r[u * 8 + 6]) * inv, __uint_as_float(r[u * 8 + 7]) * inv);
+            reinterpret_cast<uint4*>(o + cc * 32)[u] = v;
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&o_free[t]);  // O_t read out: the next item's first P V may overwrite it
     }
   }
   tc_fence_before();
@@ -407,8 +469,11 @@ int launch_prefill_tc(const __half* q, const __half* kv, __half* out, int batch,
     cudaFuncSetAttribute(tc::prefill_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (dev < 64) attr_done[dev] = 1;
   }
-  const unsigned npair = (seq_len + 2 * tc::kRows - 1) / (2 * tc::kRows);  // query-tile pairs
-  const dim3 grid(npair, batch * heads);
+  static int sms[64] = {0};
+  if (dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const long long items = static_cast<long long>((seq_len + 2 * tc::kRows - 1) / (2 * tc::kRows)) * batch * heads;
+  const int nsm = dev < 64 && sms[dev] > 0 ? sms[dev] : 148;
+  const int grid = static_cast<int>(items < nsm ? items : nsm);  // persistent: one CTA per SM
   tc::prefill_tc_kernel<D><<<grid, 384, C::kSmem, stream>>>(tq, tkv, out, batch, heads, seq_len, qscale);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return check_launch("prefill_attention");
