@@ -222,7 +222,8 @@ int kvpr_decode_layer_tail_supported(int batch, int hidden, int heads, int ffn);
 int kvpr_decode_layer_tail(const kvpr_layer_tail_desc* desc, void* stream);
 
 /* Causal attention for the prompt (prefill that populates the host stores):
- * q/out [pos][batch][hidden], kv pages as above, positions [0, seq_len). */
+ * q/out [pos][batch][hidden], kv pages as above, positions [0, seq_len).  head_dim 64 or 128,
+ * batch * heads <= 65535 (else KVPR_EINVAL); one persistent launch of at most #SMs CTAs. */
 int kvpr_prefill_attention(const void* q, const void* kv_pages, void* out, int batch, int heads, int head_dim,
                            int seq_len, float scale, void* stream);
 
