@@ -389,8 +389,11 @@ def test_decode_attention_empty_cache_rejected(dev):
 
 
 @pytest.mark.parametrize("batch,heads,d,seq", [(2, 4, 64, 37), (3, 2, 128, 130), (1, 3, 64, 1), (2, 2, 128, 64),
-                                               (2, 4, 128, 1000), (1, 2, 64, 513)])
+                                               (2, 4, 128, 1000), (1, 2, 64, 513),
+                                               (3, 40, 64, 1000), (2, 37, 128, 777)])
 def test_prefill_attention_causal(dev, batch, heads, d, seq):
+    """Last two cases: more work items (query-tile pairs x sequences x heads: 480, 296) than SMs, so
+    the persistent CTAs walk several zigzag rounds, the last one partial."""
     h = heads * d
     pages = _rand(seq, 2, batch, h, seed=20)
     q = _rand(seq, batch, h, seed=21)
